@@ -1,0 +1,361 @@
+/*
+ * gpumux_b200.h — C-ABI of the B200-native space-time multiplexing path.
+ *
+ * This is the drop-in boundary for the reference's space-time scheduler
+ * (arxiv 1901.00041, artifact "gpumux").  The reference exposes a plain C++
+ * static-library API with no FFI layer; every entry point below names the
+ * reference function it replaces (file:line under /root/reference/proj).
+ *
+ *   - plain C types only: POD structs, pointers, sizes; no torch, no STL
+ *   - every function returns an int status (GM_OK == 0); the message of the
+ *     last failure is gm_last_error() (per-thread) — messages equal the
+ *     reference's std::invalid_argument::what() texts
+ *   - objects (queue, plans, cache, ctx) are opaque handles; a handle is a
+ *     single logical actor and is not thread-safe; use one
+ *     gm_ctx per GPU on one host thread (tenant-sharded placement)
+ *
+ * Status codes mirror the reference's exception classes and CLI exit codes
+ * (proj/tools/gpumux.cpp:26-30).
+ */
+#ifndef GPUMUX_B200_H
+#define GPUMUX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GM_ABI_VERSION 1
+
+enum gm_status {
+  GM_OK = 0,
+  GM_EINVAL = 1,     /* std::invalid_argument (misuse)                    */
+  GM_ECONFIG = 2,    /* gpumux::ConfigError      (CLI exit 1)             */
+  GM_EOOM = 3,       /* gpumux::InfeasibleError / device OOM (CLI exit 2) */
+  GM_EINTERNAL = 4,  /* anything else            (CLI exit 3)             */
+  GM_ECUDA = 5,      /* CUDA runtime/driver failure                       */
+  GM_ERANGE = 6,     /* caller-provided output buffer too small           */
+  GM_ENODEV = 7      /* no sm_100 device / CUDA path unavailable          */
+};
+
+/* ---- L0 domain types (proj/include/gpumux/gemm.hpp:11-31) ---------------- */
+
+typedef struct gm_gemm_shape {      /* GemmShape, gemm.hpp:11-20 */
+  int64_t m, n, k;
+} gm_gemm_shape;
+
+typedef struct gm_conv_spec {       /* ConvSpec, gemm.hpp:23-31 */
+  int64_t image_h, image_w, kernel_h, kernel_w;
+  int64_t in_channels, out_channels, stride, padding;
+} gm_conv_spec;
+
+/* DeviceSpec, proj/include/gpumux/device.hpp:13-30 (field order kept). */
+typedef struct gm_device_spec {
+  double peak_flops;
+  double mem_bandwidth;
+  int64_t sm_count;
+  int64_t blocks_per_sm;
+  double launch_overhead;
+  double context_switch_overhead;
+  double planning_overhead;
+  double mem_capacity;
+  double process_context_bytes;
+  int64_t tile_m;
+  int64_t tile_n;
+  double space_sched_penalty;
+  double launch_serialization;
+} gm_device_spec;
+
+typedef struct gm_kernel_cost {     /* KernelCost, cost_model.hpp:14-20 */
+  int64_t flops;
+  int64_t bytes;
+  int64_t blocks;
+  double duration;                  /* seconds */
+  int64_t waves;
+} gm_kernel_cost;
+
+typedef struct gm_kernel_group {    /* KernelGroup, cost_model.hpp:24-27 */
+  gm_gemm_shape shape;
+  int64_t count;
+} gm_kernel_group;
+
+/* KernelRequest, scheduler.hpp:17-25.  `batch` is a B200 extension (query
+ * coalescing, gemm.hpp:54-56); the planner never reads it (default 1). */
+typedef struct gm_kernel_request {
+  uint64_t request_id;
+  int32_t tenant_index;
+  int32_t layer_index;
+  gm_gemm_shape shape;
+  int64_t enqueue_time;             /* ns */
+  int64_t slo_deadline;             /* absolute ns */
+  uint32_t pass_index;
+  uint32_t batch;
+} gm_kernel_request;
+
+typedef struct gm_batch_policy {    /* BatchPolicy, scheduler.hpp:28-34 */
+  double max_wait;                  /* seconds */
+  int64_t target_batch;
+  int32_t allow_variable_size;
+  int32_t reserved0;
+  double slo_safety_margin;
+  double variable_inefficiency;
+} gm_batch_policy;
+
+typedef struct gm_tenant_health {   /* TenantHealth, scheduler.hpp:44-50 */
+  int32_t tenant_index;
+  int32_t evicted;
+  double ewma_latency;
+  double ewma_alpha;
+  int64_t observed_count;
+} gm_tenant_health;
+
+typedef struct gm_detector {        /* DetectorParams, sim.hpp:32-37 */
+  double ewma_alpha;
+  int64_t min_observations;
+  double threshold_ratio;
+  int32_t evict_stragglers;
+  int32_t reserved0;
+} gm_detector;
+
+/* One entry of the per-CTA tile-dispatch table.  Entries are
+ * flattened in member order, then m-tile-major, then n-tile, so the table
+ * length equals plan_super_kernel(...).blocks under the same DeviceSpec. */
+typedef struct gm_tile {
+  uint16_t member;                  /* index into the plan's member list */
+  uint16_t flags;                   /* reserved (0) */
+  uint16_t m_tile;
+  uint16_t n_tile;
+} gm_tile;
+
+/* Summary of one formed SuperKernel (scheduler.hpp:37-42). */
+typedef struct gm_plan_info {
+  int32_t uniform;
+  int32_t reserved0;
+  int64_t n_members;
+  gm_kernel_cost planned_cost;
+  const char* signature;            /* owned by the gm_plans handle */
+} gm_plan_info;
+
+/* ---- defaults and profiles ---------------------------------------------- */
+
+const char* gm_last_error(void);
+int gm_abi_version(void);
+
+void gm_device_spec_default(gm_device_spec* out);  /* DeviceSpec{} defaults   */
+void gm_device_spec_v100(gm_device_spec* out);     /* v100_profile(), device.cpp:41-59 */
+/* B200 profile: tile_m/tile_n = the super-kernel CTA tile, sm_count = 148,
+ * blocks_per_sm = 1 (one persistent CTA per SM).  Peaks from the measured
+ * roofline (MEASURED_PEAKS.json); overheads fitted to B200 launches. */
+void gm_device_spec_b200(gm_device_spec* out);
+int gm_device_spec_validate(const gm_device_spec* d);  /* DeviceSpec::validate, device.cpp:19-39 */
+void gm_batch_policy_default(gm_batch_policy* out);
+void gm_detector_default(gm_detector* out);
+
+/* ---- L0/L1: shapes and cost model --------------------------------------- */
+
+int64_t gm_gemm_flops(const gm_gemm_shape* s);                 /* gemm.hpp:33-35 */
+int64_t gm_gemm_bytes(const gm_gemm_shape* s, int64_t elem);   /* gemm.hpp:38-40 */
+int gm_im2col_gemm_dims(const gm_conv_spec* c, gm_gemm_shape* out); /* gemm.hpp:44-51 */
+void gm_batch_inputs(const gm_gemm_shape* s, int64_t batch, gm_gemm_shape* out); /* gemm.hpp:54-56 */
+int gm_shape_key(const gm_gemm_shape* s, char* buf, size_t cap); /* gemm.hpp:58-60 */
+int64_t gm_to_ns(double seconds);                              /* vtime.hpp:13-15 */
+double gm_to_seconds(int64_t ns);                              /* vtime.hpp:17-19 */
+int64_t gm_thread_blocks(const gm_gemm_shape* s, const gm_device_spec* d); /* cost_model.cpp:14-16 */
+/* dispatch_duration, cost_model.cpp:18-46 */
+int gm_dispatch_duration(const gm_kernel_group* groups, size_t n, const gm_device_spec* d,
+                         int64_t slot_budget, int64_t launches, gm_kernel_cost* out);
+
+/* ---- L2b: space-time scheduler (scheduler.hpp:59-122) ------------------- */
+
+typedef struct gm_queue gm_queue;   /* RequestQueue */
+typedef struct gm_plans gm_plans;   /* std::vector<SuperKernel> */
+typedef struct gm_cache gm_cache;   /* SuperKernelCache */
+
+int gm_queue_create(gm_queue** out);
+void gm_queue_destroy(gm_queue* q);
+int gm_queue_enqueue(gm_queue* q, const gm_kernel_request* r);  /* scheduler.cpp:8-16 */
+int64_t gm_queue_size(const gm_queue* q);
+/* Pending requests in group order (ascending m,n,k), FIFO within a group. */
+int gm_queue_snapshot(const gm_queue* q, gm_kernel_request* out, size_t cap, size_t* n);
+int gm_queue_group_count(const gm_queue* q, size_t* n);
+/* RequestQueue::cancel_tenant, scheduler.cpp:18-35 */
+int gm_queue_cancel_tenant(gm_queue* q, int32_t tenant, gm_kernel_request* out, size_t cap,
+                           size_t* n);
+
+/* form_batches, scheduler.cpp:96-199.  Mutates the queue; *out receives a
+ * new plans handle (possibly empty) that the caller destroys. */
+int gm_form_batches(gm_queue* q, int64_t now, const gm_batch_policy* p,
+                    const gm_device_spec* d, gm_plans** out);
+size_t gm_plans_count(const gm_plans* p);
+int gm_plans_get(const gm_plans* p, size_t i, gm_plan_info* out);
+int gm_plans_members(const gm_plans* p, size_t i, gm_kernel_request* out, size_t cap, size_t* n);
+void gm_plans_destroy(gm_plans* p);
+/* Tile-dispatch table of plan i under device d. */
+int gm_build_tile_table(const gm_plans* p, size_t i, const gm_device_spec* d, gm_tile* out,
+                        size_t cap, size_t* n);
+
+/* plan_super_kernel, scheduler.cpp:43-61 */
+int gm_plan_super_kernel(const gm_kernel_request* members, size_t n, int uniform,
+                         const gm_batch_policy* p, const gm_device_spec* d, gm_kernel_cost* out);
+/* slo_headroom, scheduler.cpp:37-41 */
+double gm_slo_headroom(const gm_kernel_request* r, int64_t now, double predicted,
+                       const gm_batch_policy* p);
+
+int gm_cache_create(gm_cache** out);
+void gm_cache_destroy(gm_cache* c);
+/* dispatch_cost, scheduler.cpp:201-212 */
+int gm_dispatch_cost(const gm_plans* p, size_t i, gm_cache* c, const gm_device_spec* d,
+                     double* duration, int* cache_hit);
+int gm_cache_stats(const gm_cache* c, int64_t* hits, int64_t* misses, int64_t* entries);
+
+/* record_latency / detect_stragglers / evict, scheduler.cpp:214-271 */
+int gm_record_latency(gm_tenant_health* h, double observed_seconds);
+int gm_detect_stragglers(const gm_tenant_health* h, size_t n, double threshold_ratio,
+                         int64_t min_observations, int32_t* out, size_t cap, size_t* n_out);
+int gm_evict(gm_tenant_health* h, size_t n, gm_queue* q, int32_t tenant,
+             gm_kernel_request* out, size_t cap, size_t* n_out);
+
+/* ---- L4: metrics (metrics.cpp:10-28) ------------------------------------ */
+int gm_percentile_nearest_rank(const double* v, size_t n, double pct, double* out);
+int gm_geomean(const double* v, size_t n, double* out);
+
+/* ---- L3: space-time driver, virtual clock (sim.cpp:398-581) -------------
+ * Closed-loop run_space_time over homogeneous tenants (same layer list).
+ * Produces the dispatch sequence the reference engine produces; the B200
+ * runtime replays that plan stream on the GPU. */
+typedef struct gm_sim_config {
+  gm_device_spec device;
+  gm_batch_policy scheduler;
+  gm_detector detector;
+  const gm_gemm_shape* layers;      /* shared layer list */
+  size_t n_layers;
+  int32_t n_tenants;
+  int32_t concurrency;
+  double slo_latency;               /* seconds per pass */
+  double duration;                  /* virtual seconds */
+  double warmup;
+  int32_t microbench;               /* 1 = keep layer 0 only (SimMode::kMicrobench) */
+  int32_t degrade_tenant;           /* -1 = none (inject_degradation, sim.cpp:60-68) */
+  double degrade_slowdown;
+  double degrade_start;
+} gm_sim_config;
+
+typedef struct gm_sim_event {       /* DispatchEvent (policies.hpp) for space-time */
+  int64_t start, end;
+  int64_t flops;
+  double occupancy;
+  int64_t member_offset;            /* into the member-id array */
+  int64_t n_members;
+} gm_sim_event;
+
+typedef struct gm_sim_completion {  /* RequestLifecycle, sim.hpp:62-71 */
+  uint64_t request_id;
+  int32_t tenant_index;
+  int32_t slo_met;
+  int64_t enqueue_time, dispatch_time, complete_time;
+  int64_t flops;
+} gm_sim_completion;
+
+typedef struct gm_sim_trace gm_sim_trace;
+int gm_simulate_space_time(const gm_sim_config* cfg, gm_sim_trace** out);
+int gm_sim_trace_counts(const gm_sim_trace* t, size_t* n_events, size_t* n_members,
+                        size_t* n_completions, size_t* n_cancelled, int64_t* cache_hits,
+                        int64_t* cache_misses);
+int gm_sim_trace_events(const gm_sim_trace* t, gm_sim_event* ev, size_t cap_ev,
+                        uint64_t* member_ids, size_t cap_ids);
+int gm_sim_trace_completions(const gm_sim_trace* t, gm_sim_completion* out, size_t cap);
+int gm_sim_trace_evictions(const gm_sim_trace* t, int32_t* tenants, int64_t* times, size_t cap,
+                           size_t* n);
+int gm_sim_trace_flops(const gm_sim_trace* t, int64_t* dispatched, int64_t* completed);
+void gm_sim_trace_destroy(gm_sim_trace* t);
+
+/* ---- B200 runtime: tenants, super-kernel dispatch ------------------------ */
+
+enum gm_layer_kind { GM_LAYER_GEMM = 0, GM_LAYER_CONV = 1 };
+
+/* One operator of a tenant's graph, with its device buffers (bf16).
+ *   CONV: x = NHWC [batch, H, W, Cin]; w = KRSC [Cout, R, S, Cin] with a row
+ *         stride of ldw elements (ldw >= R*S*Cin, ldw % 8 == 0);
+ *         y = NHWC [batch, P, Q, Cout]  (== row-major [M, N])
+ *   GEMM: x = A [m, k] row-major (row stride ldx), w = B [n, k] (row stride
+ *         ldw), y = C [m, n] row-major. */
+typedef struct gm_layer_desc {
+  int32_t kind;
+  int32_t batch;                    /* CONV only: images per query batch */
+  gm_conv_spec conv;
+  gm_gemm_shape gemm;
+  const void* x;
+  const void* w;
+  void* y;
+  int64_t ldx;                      /* 0 = dense */
+  int64_t ldw;                      /* 0 = dense */
+  int32_t relu;                     /* fuse max(0, .) into the epilogue */
+  int32_t reserved0;
+} gm_layer_desc;
+
+typedef struct gm_tenant_desc {     /* Tenant, workload.hpp:14-22 */
+  const char* tenant_id;
+  const gm_layer_desc* layers;
+  size_t n_layers;
+  double slo_latency;
+  int32_t concurrency;
+  int32_t reserved0;
+} gm_tenant_desc;
+
+typedef struct gm_ctx gm_ctx;       /* one per GPU */
+
+/* cuda_device < 0 creates a host-only context (planner, no launches). */
+int gm_create(const gm_device_spec* d, const gm_batch_policy* p, const gm_detector* det,
+              int cuda_device, gm_ctx** out);
+void gm_destroy(gm_ctx* ctx);
+int gm_ctx_queue(gm_ctx* ctx, gm_queue** q);
+int gm_ctx_cache(gm_ctx* ctx, gm_cache** c);
+int gm_ctx_device_spec(const gm_ctx* ctx, gm_device_spec* out);
+
+/* Registers a tenant and builds its per-layer member descriptors (TMA maps)
+ * on the device.  Replaces make_tenants (workload.cpp:113-128). */
+int gm_register_tenant(gm_ctx* ctx, const gm_tenant_desc* t, int32_t* tenant_index);
+int gm_layer_shape(gm_ctx* ctx, int32_t tenant, int32_t layer, gm_gemm_shape* out);
+int gm_tenant_count(const gm_ctx* ctx, int32_t* n);
+
+/* Prepare (host→device upload on a miss, never inside graph capture) and
+ * launch the super-kernel of plan i on `stream` (a cudaStream_t; 0 = legacy
+ * default).  planned_s/cache_hit follow dispatch_cost (scheduler.cpp:201-212)
+ * against the ctx's SuperKernelCache.  Launches are CUDA-graph capturable once
+ * prepared. */
+int gm_prepare(gm_ctx* ctx, const gm_plans* p, size_t i);
+int gm_dispatch(gm_ctx* ctx, const gm_plans* p, size_t i, uint64_t stream, double* planned_s,
+                int* cache_hit);
+/* Launch an explicit member list (tenant, layer pairs) as one super-kernel;
+ * n == 1 is the single-problem kernel used by the time-only / space-only
+ * baseline modes.  Returns the number of kernels launched in *launches. */
+int gm_launch_members(gm_ctx* ctx, const int32_t* tenants, const int32_t* layers, size_t n,
+                      uint64_t stream, int32_t* launches);
+/* Number of kernels one dispatch of this member list launches (the super-kernel
+ * plus an explicit-im2col pre-pass when a member needs one). */
+int gm_members_launch_count(gm_ctx* ctx, const int32_t* tenants, const int32_t* layers, size_t n,
+                            int32_t* launches);
+/* One closed-loop space-time round over registered tenants: each listed tenant
+ * submits one forward pass at `now`; the run_space_time loop (sim.cpp:452-576:
+ * dispatch FIFO, formation when the FIFO is empty, completion fan-out, wake
+ * timer) runs on the virtual clock until every pass completes.  Uses the ctx's
+ * BatchPolicy (target_batch 0 = auto), DeviceSpec and SuperKernelCache.
+ * Returns the dispatch sequence as a plans handle (gm_plans_times gives each
+ * dispatch's virtual window). */
+int gm_plan_round(gm_ctx* ctx, const int32_t* tenants, size_t n, int64_t now, gm_plans** out);
+int gm_plans_times(const gm_plans* p, size_t i, int64_t* start, int64_t* end);
+/* Launch every plan of a handle in order on `stream` (prepares on a miss;
+ * capturable once prepared).  *launches = kernels launched. */
+int gm_dispatch_plans(gm_ctx* ctx, const gm_plans* p, uint64_t stream, int32_t* launches);
+int gm_prepare_plans(gm_ctx* ctx, const gm_plans* p);
+/* Total super-kernel launches and tiles issued by this ctx so far. */
+int gm_ctx_launch_stats(const gm_ctx* ctx, int64_t* superkernels, int64_t* prepasses,
+                        int64_t* tiles);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif  /* GPUMUX_B200_H */

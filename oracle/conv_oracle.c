@@ -1,0 +1,106 @@
+/*
+ * TEST INFRASTRUCTURE ONLY — the CPU fp32 checker for super-kernel activations.
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg load it.
+ *
+ * Restates the operator semantics the reference models but never computes
+ * (it has no tensor numerics: SURVEY §0, "activation parity unpinned"):
+ *   - conv lowered to its im2col GEMM: rows = output positions (n, p, q),
+ *     cols = C_out, inner = the unrolled (r, s, c) filter patch
+ *     (proj/include/gpumux/gemm.hpp:42-51), input batching multiplies the rows
+ *     (gemm.hpp:54-56);
+ *   - GEMM C[m, n] = sum_k A[m, k] * B[n, k]  (gemm.hpp:11-16, B stored K-major).
+ * Layouts match the product: X NHWC, W KRSC with row stride ldw, Y NHWC.
+ * Accumulation is in double, so the oracle is at least as accurate as any fp32
+ * reference path; inputs are the same bf16-rounded values the GPU reads.
+ * Cross-checked against torch.nn.functional.conv2d in tests/test_oracle.py.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+/* Round-to-nearest-even fp32 -> bf16 -> fp32 (the rounding torch applies in
+ * tensor.to(torch.bfloat16)); NaN stays NaN. */
+void oracle_round_bf16(float* v, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) {
+    uint32_t u;
+    memcpy(&u, &v[i], 4);
+    if ((u & 0x7f800000u) == 0x7f800000u && (u & 0x007fffffu)) continue;
+    const uint32_t lsb = (u >> 16) & 1u;
+    u = (u + 0x7fffu + lsb) & 0xffff0000u;
+    memcpy(&v[i], &u, 4);
+  }
+}
+
+/* y[b, p, q, o] = sum_{r,s,c} x[b, p*st - pad + r, q*st - pad + s, c] * w[o, (r*S + s)*Cin + c] */
+void oracle_conv2d_nhwc(const float* x, const float* w, float* y, int64_t batch, int64_t H, int64_t W,
+                        int64_t Cin, int64_t Cout, int64_t R, int64_t S, int64_t stride, int64_t pad,
+                        int64_t ldw, int32_t relu) {
+  const int64_t P = (H + 2 * pad - R) / stride + 1;
+  const int64_t Q = (W + 2 * pad - S) / stride + 1;
+  if (ldw <= 0) ldw = R * S * Cin;
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int64_t b = 0; b < batch; ++b) {
+    for (int64_t p = 0; p < P; ++p) {
+      for (int64_t q = 0; q < Q; ++q) {
+        float* out = y + ((b * P + p) * Q + q) * Cout;
+        for (int64_t o = 0; o < Cout; ++o) {
+          double acc = 0.0;
+          const float* wo = w + o * ldw;
+          for (int64_t r = 0; r < R; ++r) {
+            const int64_t ih = p * stride - pad + r;
+            if (ih < 0 || ih >= H) continue;
+            for (int64_t s = 0; s < S; ++s) {
+              const int64_t iw = q * stride - pad + s;
+              if (iw < 0 || iw >= W) continue;
+              const float* xi = x + ((b * H + ih) * W + iw) * Cin;
+              const float* wi = wo + (r * S + s) * Cin;
+              for (int64_t c = 0; c < Cin; ++c) acc += (double)xi[c] * (double)wi[c];
+            }
+          }
+          float v = (float)acc;
+          out[o] = (relu && v < 0.0f) ? 0.0f : v;
+        }
+      }
+    }
+  }
+}
+
+/* c[m, n] = sum_k a[m*lda + k] * b[n*ldb + k] */
+void oracle_gemm_nt(const float* a, const float* b, float* c, int64_t M, int64_t N, int64_t K, int64_t lda,
+                    int64_t ldb, int32_t relu) {
+  if (lda <= 0) lda = K;
+  if (ldb <= 0) ldb = K;
+#pragma omp parallel for schedule(static)
+  for (int64_t m = 0; m < M; ++m) {
+    for (int64_t n = 0; n < N; ++n) {
+      double acc = 0.0;
+      const float* am = a + m * lda;
+      const float* bn = b + n * ldb;
+      for (int64_t k = 0; k < K; ++k) acc += (double)am[k] * (double)bn[k];
+      float v = (float)acc;
+      c[m * N + n] = (relu && v < 0.0f) ? 0.0f : v;
+    }
+  }
+}
+
+/* Explicit im2col of one NHWC tensor into [M, ldk] rows (zero padding),
+ * k = (r*S + s)*Cin + c — the layout the GPU pre-pass writes. */
+void oracle_im2col_nhwc(const float* x, float* out, int64_t batch, int64_t H, int64_t W, int64_t Cin, int64_t R,
+                        int64_t S, int64_t stride, int64_t pad, int64_t ldk) {
+  const int64_t P = (H + 2 * pad - R) / stride + 1;
+  const int64_t Q = (W + 2 * pad - S) / stride + 1;
+  const int64_t K = R * S * Cin;
+#pragma omp parallel for schedule(static)
+  for (int64_t m = 0; m < batch * P * Q; ++m) {
+    const int64_t b = m / (P * Q), p = (m / Q) % P, q = m % Q;
+    float* row = out + m * ldk;
+    for (int64_t k = 0; k < ldk; ++k) row[k] = 0.0f;
+    for (int64_t r = 0; r < R; ++r)
+      for (int64_t s = 0; s < S; ++s) {
+        const int64_t ih = p * stride - pad + r, iw = q * stride - pad + s;
+        if (ih < 0 || ih >= H || iw < 0 || iw >= W) continue;
+        memcpy(row + (r * S + s) * Cin, x + ((b * H + ih) * W + iw) * Cin, (size_t)Cin * sizeof(float));
+      }
+    (void)K;
+  }
+}

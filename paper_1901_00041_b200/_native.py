@@ -1,0 +1,225 @@
+"""ctypes view of the C-ABI in include/gpumux_b200.h.
+
+The shared library is built in-tree (``paper_1901_00041_b200/_lib``) by
+``__graft_entry__.build()``.  Loading fails loudly: there is no Python
+fallback for anything this module exposes.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libgpumux_b200.so")
+
+GM_OK, GM_EINVAL, GM_ECONFIG, GM_EOOM, GM_EINTERNAL, GM_ECUDA, GM_ERANGE, GM_ENODEV = range(8)
+GM_LAYER_GEMM, GM_LAYER_CONV = 0, 1
+
+
+class gm_gemm_shape(C.Structure):
+    _fields_ = [("m", C.c_int64), ("n", C.c_int64), ("k", C.c_int64)]
+
+
+class gm_conv_spec(C.Structure):
+    _fields_ = [(f, C.c_int64) for f in ("image_h", "image_w", "kernel_h", "kernel_w", "in_channels",
+                                          "out_channels", "stride", "padding")]
+
+
+class gm_device_spec(C.Structure):
+    _fields_ = [
+        ("peak_flops", C.c_double), ("mem_bandwidth", C.c_double), ("sm_count", C.c_int64),
+        ("blocks_per_sm", C.c_int64), ("launch_overhead", C.c_double), ("context_switch_overhead", C.c_double),
+        ("planning_overhead", C.c_double), ("mem_capacity", C.c_double), ("process_context_bytes", C.c_double),
+        ("tile_m", C.c_int64), ("tile_n", C.c_int64), ("space_sched_penalty", C.c_double),
+        ("launch_serialization", C.c_double),
+    ]
+
+
+class gm_kernel_cost(C.Structure):
+    _fields_ = [("flops", C.c_int64), ("bytes", C.c_int64), ("blocks", C.c_int64), ("duration", C.c_double),
+                ("waves", C.c_int64)]
+
+
+class gm_kernel_group(C.Structure):
+    _fields_ = [("shape", gm_gemm_shape), ("count", C.c_int64)]
+
+
+class gm_kernel_request(C.Structure):
+    _fields_ = [("request_id", C.c_uint64), ("tenant_index", C.c_int32), ("layer_index", C.c_int32),
+                ("shape", gm_gemm_shape), ("enqueue_time", C.c_int64), ("slo_deadline", C.c_int64),
+                ("pass_index", C.c_uint32), ("batch", C.c_uint32)]
+
+
+class gm_batch_policy(C.Structure):
+    _fields_ = [("max_wait", C.c_double), ("target_batch", C.c_int64), ("allow_variable_size", C.c_int32),
+                ("reserved0", C.c_int32), ("slo_safety_margin", C.c_double), ("variable_inefficiency", C.c_double)]
+
+
+class gm_tenant_health(C.Structure):
+    _fields_ = [("tenant_index", C.c_int32), ("evicted", C.c_int32), ("ewma_latency", C.c_double),
+                ("ewma_alpha", C.c_double), ("observed_count", C.c_int64)]
+
+
+class gm_detector(C.Structure):
+    _fields_ = [("ewma_alpha", C.c_double), ("min_observations", C.c_int64), ("threshold_ratio", C.c_double),
+                ("evict_stragglers", C.c_int32), ("reserved0", C.c_int32)]
+
+
+class gm_tile(C.Structure):
+    _fields_ = [("member", C.c_uint16), ("flags", C.c_uint16), ("m_tile", C.c_uint16), ("n_tile", C.c_uint16)]
+
+
+class gm_plan_info(C.Structure):
+    _fields_ = [("uniform", C.c_int32), ("reserved0", C.c_int32), ("n_members", C.c_int64),
+                ("planned_cost", gm_kernel_cost), ("signature", C.c_char_p)]
+
+
+class gm_sim_config(C.Structure):
+    _fields_ = [("device", gm_device_spec), ("scheduler", gm_batch_policy), ("detector", gm_detector),
+                ("layers", C.POINTER(gm_gemm_shape)), ("n_layers", C.c_size_t), ("n_tenants", C.c_int32),
+                ("concurrency", C.c_int32), ("slo_latency", C.c_double), ("duration", C.c_double),
+                ("warmup", C.c_double), ("microbench", C.c_int32), ("degrade_tenant", C.c_int32),
+                ("degrade_slowdown", C.c_double), ("degrade_start", C.c_double)]
+
+
+class gm_sim_event(C.Structure):
+    _fields_ = [("start", C.c_int64), ("end", C.c_int64), ("flops", C.c_int64), ("occupancy", C.c_double),
+                ("member_offset", C.c_int64), ("n_members", C.c_int64)]
+
+
+class gm_sim_completion(C.Structure):
+    _fields_ = [("request_id", C.c_uint64), ("tenant_index", C.c_int32), ("slo_met", C.c_int32),
+                ("enqueue_time", C.c_int64), ("dispatch_time", C.c_int64), ("complete_time", C.c_int64),
+                ("flops", C.c_int64)]
+
+
+class gm_layer_desc(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("batch", C.c_int32), ("conv", gm_conv_spec), ("gemm", gm_gemm_shape),
+                ("x", C.c_void_p), ("w", C.c_void_p), ("y", C.c_void_p), ("ldx", C.c_int64), ("ldw", C.c_int64),
+                ("relu", C.c_int32), ("reserved0", C.c_int32)]
+
+
+class gm_tenant_desc(C.Structure):
+    _fields_ = [("tenant_id", C.c_char_p), ("layers", C.POINTER(gm_layer_desc)), ("n_layers", C.c_size_t),
+                ("slo_latency", C.c_double), ("concurrency", C.c_int32), ("reserved0", C.c_int32)]
+
+
+P = C.POINTER
+_SIGS = {
+    "gm_last_error": (C.c_char_p, []),
+    "gm_abi_version": (C.c_int, []),
+    "gm_device_spec_default": (None, [P(gm_device_spec)]),
+    "gm_device_spec_v100": (None, [P(gm_device_spec)]),
+    "gm_device_spec_b200": (None, [P(gm_device_spec)]),
+    "gm_device_spec_validate": (C.c_int, [P(gm_device_spec)]),
+    "gm_batch_policy_default": (None, [P(gm_batch_policy)]),
+    "gm_detector_default": (None, [P(gm_detector)]),
+    "gm_gemm_flops": (C.c_int64, [P(gm_gemm_shape)]),
+    "gm_gemm_bytes": (C.c_int64, [P(gm_gemm_shape), C.c_int64]),
+    "gm_im2col_gemm_dims": (C.c_int, [P(gm_conv_spec), P(gm_gemm_shape)]),
+    "gm_batch_inputs": (None, [P(gm_gemm_shape), C.c_int64, P(gm_gemm_shape)]),
+    "gm_shape_key": (C.c_int, [P(gm_gemm_shape), C.c_char_p, C.c_size_t]),
+    "gm_to_ns": (C.c_int64, [C.c_double]),
+    "gm_to_seconds": (C.c_double, [C.c_int64]),
+    "gm_thread_blocks": (C.c_int64, [P(gm_gemm_shape), P(gm_device_spec)]),
+    "gm_dispatch_duration": (C.c_int, [P(gm_kernel_group), C.c_size_t, P(gm_device_spec), C.c_int64, C.c_int64,
+                                       P(gm_kernel_cost)]),
+    "gm_queue_create": (C.c_int, [P(C.c_void_p)]),
+    "gm_queue_destroy": (None, [C.c_void_p]),
+    "gm_queue_enqueue": (C.c_int, [C.c_void_p, P(gm_kernel_request)]),
+    "gm_queue_size": (C.c_int64, [C.c_void_p]),
+    "gm_queue_snapshot": (C.c_int, [C.c_void_p, P(gm_kernel_request), C.c_size_t, P(C.c_size_t)]),
+    "gm_queue_group_count": (C.c_int, [C.c_void_p, P(C.c_size_t)]),
+    "gm_queue_cancel_tenant": (C.c_int, [C.c_void_p, C.c_int32, P(gm_kernel_request), C.c_size_t, P(C.c_size_t)]),
+    "gm_form_batches": (C.c_int, [C.c_void_p, C.c_int64, P(gm_batch_policy), P(gm_device_spec), P(C.c_void_p)]),
+    "gm_plans_count": (C.c_size_t, [C.c_void_p]),
+    "gm_plans_get": (C.c_int, [C.c_void_p, C.c_size_t, P(gm_plan_info)]),
+    "gm_plans_members": (C.c_int, [C.c_void_p, C.c_size_t, P(gm_kernel_request), C.c_size_t, P(C.c_size_t)]),
+    "gm_plans_destroy": (None, [C.c_void_p]),
+    "gm_build_tile_table": (C.c_int, [C.c_void_p, C.c_size_t, P(gm_device_spec), P(gm_tile), C.c_size_t,
+                                      P(C.c_size_t)]),
+    "gm_plan_super_kernel": (C.c_int, [P(gm_kernel_request), C.c_size_t, C.c_int, P(gm_batch_policy),
+                                       P(gm_device_spec), P(gm_kernel_cost)]),
+    "gm_slo_headroom": (C.c_double, [P(gm_kernel_request), C.c_int64, C.c_double, P(gm_batch_policy)]),
+    "gm_cache_create": (C.c_int, [P(C.c_void_p)]),
+    "gm_cache_destroy": (None, [C.c_void_p]),
+    "gm_dispatch_cost": (C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p, P(gm_device_spec), P(C.c_double),
+                                   P(C.c_int)]),
+    "gm_cache_stats": (C.c_int, [C.c_void_p, P(C.c_int64), P(C.c_int64), P(C.c_int64)]),
+    "gm_record_latency": (C.c_int, [P(gm_tenant_health), C.c_double]),
+    "gm_detect_stragglers": (C.c_int, [P(gm_tenant_health), C.c_size_t, C.c_double, C.c_int64, P(C.c_int32),
+                                       C.c_size_t, P(C.c_size_t)]),
+    "gm_evict": (C.c_int, [P(gm_tenant_health), C.c_size_t, C.c_void_p, C.c_int32, P(gm_kernel_request),
+                           C.c_size_t, P(C.c_size_t)]),
+    "gm_percentile_nearest_rank": (C.c_int, [P(C.c_double), C.c_size_t, C.c_double, P(C.c_double)]),
+    "gm_geomean": (C.c_int, [P(C.c_double), C.c_size_t, P(C.c_double)]),
+    "gm_simulate_space_time": (C.c_int, [P(gm_sim_config), P(C.c_void_p)]),
+    "gm_sim_trace_counts": (C.c_int, [C.c_void_p, P(C.c_size_t), P(C.c_size_t), P(C.c_size_t), P(C.c_size_t),
+                                      P(C.c_int64), P(C.c_int64)]),
+    "gm_sim_trace_events": (C.c_int, [C.c_void_p, P(gm_sim_event), C.c_size_t, P(C.c_uint64), C.c_size_t]),
+    "gm_sim_trace_completions": (C.c_int, [C.c_void_p, P(gm_sim_completion), C.c_size_t]),
+    "gm_sim_trace_evictions": (C.c_int, [C.c_void_p, P(C.c_int32), P(C.c_int64), C.c_size_t, P(C.c_size_t)]),
+    "gm_sim_trace_flops": (C.c_int, [C.c_void_p, P(C.c_int64), P(C.c_int64)]),
+    "gm_sim_trace_destroy": (None, [C.c_void_p]),
+    "gm_create": (C.c_int, [P(gm_device_spec), P(gm_batch_policy), P(gm_detector), C.c_int, P(C.c_void_p)]),
+    "gm_destroy": (None, [C.c_void_p]),
+    "gm_ctx_queue": (C.c_int, [C.c_void_p, P(C.c_void_p)]),
+    "gm_ctx_cache": (C.c_int, [C.c_void_p, P(C.c_void_p)]),
+    "gm_ctx_device_spec": (C.c_int, [C.c_void_p, P(gm_device_spec)]),
+    "gm_register_tenant": (C.c_int, [C.c_void_p, P(gm_tenant_desc), P(C.c_int32)]),
+    "gm_layer_shape": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, P(gm_gemm_shape)]),
+    "gm_tenant_count": (C.c_int, [C.c_void_p, P(C.c_int32)]),
+    "gm_prepare": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
+    "gm_dispatch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint64, P(C.c_double), P(C.c_int)]),
+    "gm_launch_members": (C.c_int, [C.c_void_p, P(C.c_int32), P(C.c_int32), C.c_size_t, C.c_uint64,
+                                    P(C.c_int32)]),
+    "gm_members_launch_count": (C.c_int, [C.c_void_p, P(C.c_int32), P(C.c_int32), C.c_size_t, P(C.c_int32)]),
+    "gm_plan_round": (C.c_int, [C.c_void_p, P(C.c_int32), C.c_size_t, C.c_int64, P(C.c_void_p)]),
+    "gm_plans_times": (C.c_int, [C.c_void_p, C.c_size_t, P(C.c_int64), P(C.c_int64)]),
+    "gm_prepare_plans": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gm_dispatch_plans": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, P(C.c_int32)]),
+    "gm_ctx_launch_stats": (C.c_int, [C.c_void_p, P(C.c_int64), P(C.c_int64), P(C.c_int64)]),
+}
+
+_lib = None
+
+
+class NativeError(RuntimeError):
+    """A failure status from the C-ABI that has no closer Python analogue."""
+
+    def __init__(self, code: int, message: str):
+        super().__init__(message)
+        self.code = code
+
+
+class CudaUnavailable(NativeError):
+    pass
+
+
+def lib() -> C.CDLL:
+    """The loaded product library; raises if it has not been built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() (no fallback path exists)")
+        handle = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def check(status: int) -> None:
+    """Map a gm_status to the Python exception of the matching reference class."""
+    if status == GM_OK:
+        return
+    msg = lib().gm_last_error().decode()
+    if status == GM_EINVAL:
+        raise ValueError(msg)  # std::invalid_argument
+    if status == GM_ENODEV:
+        raise CudaUnavailable(status, msg)
+    if status == GM_EOOM:
+        raise MemoryError(msg)
+    raise NativeError(status, msg)

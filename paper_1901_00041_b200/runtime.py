@@ -1,0 +1,157 @@
+"""Per-GPU context (gm_ctx): tenant registration and super-kernel dispatch.
+
+Device buffers are torch tensors (PyTorch is plumbing here: allocation,
+streams, graphs); all compute runs in the sm_100a kernels of
+``libgpumux_b200.so``.  There is no CPU or PyTorch fallback: a missing
+library or a non-sm_100 device raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+from . import _native as N
+from ._native import check, lib
+from .scheduler import (BatchPolicy, ConvSpec, DeviceSpec, GemmShape, RequestQueue, SuperKernel, SuperKernelCache,
+                        TenantHealth, _Plans, _unpack_plans, b200_profile)
+from .sim import DetectorParams
+
+
+@dataclass
+class LayerBuffers:
+    """One operator of a tenant graph with its device tensors (bf16).
+
+    conv: x NHWC [b, H, W, Cin], w [Cout, ldw] (KRSC rows), y NHWC [b, P, Q, Cout]
+    gemm: x [M, ldx], w [N, ldw], y [M, N]
+    """
+    kind: str
+    x: object
+    w: object
+    y: object
+    conv: Optional[ConvSpec] = None
+    batch: int = 1
+    gemm: Optional[GemmShape] = None
+    relu: bool = False
+
+
+class Context:
+    """gm_ctx: one scheduler + device runtime per GPU."""
+
+    def __init__(self, device_index: int = 0, device: Optional[DeviceSpec] = None,
+                 policy: Optional[BatchPolicy] = None, detector: Optional[DetectorParams] = None):
+        self.device = device or b200_profile()
+        self.policy = policy or BatchPolicy(target_batch=0)
+        self.detector = detector or DetectorParams()
+        h = C.c_void_p()
+        check(lib().gm_create(C.byref(self.device._c()), C.byref(self.policy._c()), C.byref(self.detector._c()),
+                              int(device_index), C.byref(h)))
+        self.handle = h.value
+        self.device_index = device_index
+        self._keepalive: List[object] = []
+        q, c = C.c_void_p(), C.c_void_p()
+        check(lib().gm_ctx_queue(self.handle, C.byref(q)))
+        check(lib().gm_ctx_cache(self.handle, C.byref(c)))
+        self.queue = RequestQueue(_borrowed=q.value)
+        self.cache = SuperKernelCache(_borrowed=c.value)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            lib().gm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        self.close()
+
+    # ------------------------------------------------------------ tenants
+    def register_tenant(self, layers: Sequence[LayerBuffers], slo_latency: float = 0.1, concurrency: int = 1,
+                        tenant_id: str = "") -> int:
+        descs = (N.gm_layer_desc * len(layers))()
+        for i, L in enumerate(layers):
+            d = descs[i]
+            d.x, d.w, d.y = L.x.data_ptr(), L.w.data_ptr(), L.y.data_ptr()
+            d.relu = int(bool(L.relu))
+            if L.kind == "conv":
+                d.kind = N.GM_LAYER_CONV
+                d.batch = L.batch
+                d.conv = L.conv._c()
+                d.ldw = L.w.stride(0)
+            elif L.kind == "gemm":
+                d.kind = N.GM_LAYER_GEMM
+                d.gemm = L.gemm._c()
+                d.ldx = L.x.stride(0)
+                d.ldw = L.w.stride(0)
+            else:
+                raise ValueError(f"unknown layer kind {L.kind!r}")
+        t = N.gm_tenant_desc(tenant_id.encode(), descs, len(layers), float(slo_latency), int(concurrency), 0)
+        idx = C.c_int32()
+        check(lib().gm_register_tenant(self.handle, C.byref(t), C.byref(idx)))
+        self._keepalive.append(list(layers))
+        return int(idx.value)
+
+    def layer_shape(self, tenant: int, layer: int) -> GemmShape:
+        out = N.gm_gemm_shape()
+        check(lib().gm_layer_shape(self.handle, tenant, layer, C.byref(out)))
+        return GemmShape._from(out)
+
+    # ------------------------------------------------------------ dispatch
+    def dispatch(self, sk: SuperKernel, stream: int = 0):
+        """Launch one formed SuperKernel; returns (planned seconds, cache hit)."""
+        d, hit = C.c_double(), C.c_int()
+        check(lib().gm_dispatch(self.handle, sk._plans.handle, sk._index, int(stream), C.byref(d), C.byref(hit)))
+        return float(d.value), bool(hit.value)
+
+    def launch_members(self, members: Sequence[tuple], stream: int = 0) -> int:
+        """Launch an explicit (tenant, layer) list as one super-kernel."""
+        n = len(members)
+        ts = (C.c_int32 * n)(*[m[0] for m in members])
+        ls = (C.c_int32 * n)(*[m[1] for m in members])
+        out = C.c_int32()
+        check(lib().gm_launch_members(self.handle, ts, ls, n, int(stream), C.byref(out)))
+        return int(out.value)
+
+    def launch_count(self, members: Sequence[tuple]) -> int:
+        n = len(members)
+        ts = (C.c_int32 * n)(*[m[0] for m in members])
+        ls = (C.c_int32 * n)(*[m[1] for m in members])
+        out = C.c_int32()
+        check(lib().gm_members_launch_count(self.handle, ts, ls, n, C.byref(out)))
+        return int(out.value)
+
+    def plan_round(self, tenants: Sequence[int], now: int = 0) -> "Round":
+        arr = (C.c_int32 * max(1, len(tenants)))(*tenants)
+        h = C.c_void_p()
+        check(lib().gm_plan_round(self.handle, arr, len(tenants), int(now), C.byref(h)))
+        return Round(self, h.value)
+
+    def launch_stats(self):
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib().gm_ctx_launch_stats(self.handle, C.byref(a), C.byref(b), C.byref(c)))
+        return {"superkernels": a.value, "prepasses": b.value, "tiles": c.value}
+
+
+class Round:
+    """The dispatch sequence of one space-time round (gm_plan_round)."""
+
+    def __init__(self, ctx: Context, handle: int):
+        self.ctx = ctx
+        self._owner = _Plans(handle)
+        self.kernels: List[SuperKernel] = _unpack_plans(handle, self._owner)
+        self.handle = handle
+        self.times = []
+        for i in range(len(self.kernels)):
+            s, e = C.c_int64(), C.c_int64()
+            check(lib().gm_plans_times(handle, i, C.byref(s), C.byref(e)))
+            self.times.append((int(s.value), int(e.value)))
+
+    @property
+    def signatures(self) -> List[str]:
+        return [k.shape_signature for k in self.kernels]
+
+    def prepare(self) -> None:
+        check(lib().gm_prepare_plans(self.ctx.handle, self.handle))
+
+    def launch(self, stream: int = 0) -> int:
+        out = C.c_int32()
+        check(lib().gm_dispatch_plans(self.ctx.handle, self.handle, int(stream), C.byref(out)))
+        return int(out.value)
