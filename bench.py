@@ -1,0 +1,460 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 space-time multiplexing path (BASELINE.json metric).
+
+Metric: packed multi-tenant conv TFLOP/s vs time-/space-only; p99 query latency.
+Workload (BASELINE.json configs[1]): 4 tenants x ResNet-50@224 conv layers + fc
+per GPU, batch 8 per tenant query, bf16 in / fp32 accumulate, synthetic data.
+A step = one space-time round: every tenant submits one query batch, the
+scheduler forms super-kernels layer by layer, each runs as one sm_100a launch.
+
+  python bench.py [--gpus N --steps K --warmup W]          # our B200 path
+  python bench.py --impl reference [...]                  # reference CPU arm
+
+Multi-GPU (torchrun): tenant-sharded, no collective on the hot path; each rank
+serves its own tenants (weak scaling); timing is on-device, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--tenants", type=int, default=4, help="tenants per GPU")
+    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--model", default="resnet50")
+    ap.add_argument("--image", type=int, default=224)
+    ap.add_argument("--table1", default="2,4,8,10,16,20,32,40,64,80,100,120",
+                    help="R values of the conv2_2 microbench sweep ('' to skip)")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--max-waves", type=int, default=1,
+                    help="planner wave cap per super-kernel (1 = reference plan parity; >1 = b200 extension)")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["bf16_tflops"], p["bf16_tflops_sustained"], p["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def model_layers(name, image):
+    from paper_1901_00041_b200 import workload as W
+    if name in ("resnet50", "resnet18", "vgg16"):
+        return getattr(W, name)(image)
+    return W.MODELS[name]()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.gpu), "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ helpers
+def nearest_rank(values, pct):
+    from paper_1901_00041_b200.scheduler import percentile_nearest_rank
+    return percentile_nearest_rank(values, pct)
+
+
+def time_graph(torch, graph, stream, steps, flush=None):
+    """Per-step device times (ms) of `steps` replays, plus first-to-last span."""
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        t0.record(stream)
+        for a, b in ev:
+            if flush is not None:
+                flush()
+            a.record(stream)
+            graph.launch(stream.cuda_stream)
+            b.record(stream)
+        t1.record(stream)
+    torch.cuda.synchronize()
+    per = [a.elapsed_time(b) for a, b in ev]
+    return per, t0.elapsed_time(t1)
+
+
+class CpuPort:
+    """The numpy fp32 port (oracle/cpu_conv.py) over one tenant's operators."""
+
+    def __init__(self, layers, batch, seed=42):
+        import numpy as np
+        sys.path.insert(0, os.path.join(HERE, "oracle"))
+        import cpu_conv  # test infra: CPU baseline / reference arm only
+        self.cpu_conv = cpu_conv
+        rng = np.random.default_rng(seed)
+        self.tensors = []
+        for L in layers:
+            s = L.gemm_shape(batch)
+            if L.kind == "conv":
+                c = L.conv
+                x = rng.uniform(-1, 1, (batch, c.image_h, c.image_w, c.in_channels)).astype(np.float32)
+                w = rng.uniform(-1, 1, (c.out_channels, c.kernel_h, c.kernel_w, c.in_channels)).astype(np.float32)
+            else:
+                x = rng.uniform(-1, 1, (s.m, s.k)).astype(np.float32)
+                w = rng.uniform(-1, 1, (s.n, s.k)).astype(np.float32)
+            self.tensors.append((L, x, w))
+        self.flops_pass = sum(L.flops(batch) for L in layers)
+        self.cores = cpu_conv.threads()
+
+    def run_pass(self):
+        for L, x, w in self.tensors:
+            if L.kind == "conv":
+                self.cpu_conv.conv2d_nhwc(x, w, L.conv.stride, L.conv.padding)
+            else:
+                self.cpu_conv.gemm_nt(x, w)
+
+    def sample(self, seconds):
+        done, t0 = 0, time.perf_counter()
+        while True:
+            self.run_pass()
+            done += 1
+            el = time.perf_counter() - t0
+            if el >= seconds:
+                return done * self.flops_pass / el / 1e12, done, el
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    """The reference's own CPU path on this box's host cores.
+
+    The reference artifact computes no tensors (it is a roofline simulator),
+    so its CPU implementation of the path is: the reference planner
+    (oracle/_ref/libgpumux_ref.so, the unmodified gpumux_core) forming the
+    round's super-kernels, plus the fp32 CPU port of the members' conv/GEMM
+    math (oracle/cpu_conv.py) on all host threads.  Each step is a bounded
+    sample: one tenant's full pass at the configured batch, cycling tenants.
+    """
+    import ctypes
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    layers = model_layers(args.model, args.image)
+    flops_pass = sum(L.flops(args.batch) for L in layers)
+    ref_path = os.path.join(HERE, "oracle", "_ref", "libgpumux_ref.so")
+    planner_ok = os.path.exists(ref_path)
+    if planner_ok:
+        ref = ctypes.CDLL(ref_path)
+        ref.gm_ref_call.restype = ctypes.c_char_p
+        ref.gm_ref_call.argtypes = [ctypes.c_char_p]
+        shapes = [list(L.gemm_shape(args.batch).__dict__.values()) for L in layers]
+    port = CpuPort(layers, args.batch)
+    cores = port.cores
+    steps = []
+    total = args.warmup + args.steps
+    for i in range(total):
+        t0 = time.perf_counter()
+        if planner_ok:  # one round of the reference planner over the configured tenants
+            req = {"op": "run_space_time", "tenants": args.tenants * args.gpus, "layers": shapes,
+                   "duration": 1e-3, "microbench": False, "scheduler": {"target_batch": 0}}
+            ref.gm_ref_call(json.dumps(req).encode())
+        port.run_pass()
+        if i >= args.warmup:
+            steps.append(time.perf_counter() - t0)
+    mean_s = sum(steps) / len(steps)
+    value = flops_pass / mean_s / 1e12
+    kind = "reference" if planner_ok else "port"
+    line = {
+        "impl": "reference", "metric": "packed multi-tenant conv TFLOP/s vs time-/space-only; p99 query latency",
+        "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": mean_s * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.tenants} tenants x {args.model}@{args.image} conv layers + fc, batch "
+                               f"{args.batch} (configs[1]); CPU sample per step: 1 tenant pass"},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": kind,
+                         "sample": f"one {args.model}@{args.image} b{args.batch} tenant pass per step "
+                                   f"({flops_pass / 1e9:.1f} GFLOP) + reference planner round"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    from paper_1901_00041_b200.engine import SpaceTimeEngine
+    from paper_1901_00041_b200 import workload as W
+
+    burst, sustained, hbm, peak_src = load_peaks()
+    layers = model_layers(args.model, args.image)
+    T = args.tenants
+    eng = SpaceTimeEngine([layers] * T, [args.batch] * T, device_index=local, tenant_offset=rank * T)
+    stream = torch.cuda.Stream(device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    from paper_1901_00041_b200.scheduler import BatchPolicy
+    # The reference planner exactly (one-wave cap per super-kernel, plan parity).
+    rnd = eng.plan_round(BatchPolicy(target_batch=0, max_waves=args.max_waves))
+    # headline: the round program (all of the round's super-kernels in one
+    # persistent launch, per-tenant layer dependencies on device)
+    g_packed = eng.capture_round(rnd)
+    # the reference's literal dispatch unit: one launch per formed super-kernel
+    g_parity = eng.capture_packed(rnd)
+    g_timed = eng.capture_packed(rnd, timed=True)
+    g_time = eng.capture_serial("time_only")
+    g_space = eng.capture_serial("space_only")
+    flops_round = eng.flops_per_round()
+
+    for g in (g_packed, g_parity, g_time, g_space, g_timed):
+        for _ in range(args.warmup):
+            g.launch(stream.cuda_stream)
+    torch.cuda.synchronize()
+
+    results = {}
+    with ClockSampler(local) as clocks:
+        for name, g in (("packed", g_packed), ("packed_per_plan", g_parity), ("time_only", g_time),
+                        ("space_only", g_space)):
+            barrier()
+            per, span = time_graph(torch, g, stream, args.steps)
+            barrier()
+            span = max_over_ranks(span)
+            results[name] = {"ms_per_step": span / args.steps, "per_step_ms": per, "launches": g.kernels}
+    # kernel-level timing of the dominant kernel (external event pairs around each super-kernel)
+    sk_ms = [0.0] * g_timed.superkernels
+    for _ in range(max(3, args.steps // 2)):
+        g_timed.launch(stream.cuda_stream)
+        for i, t in enumerate(g_timed.kernel_times_ms()):
+            sk_ms[i] += t
+    reps = max(3, args.steps // 2)
+    sk_avg = [t / reps for t in sk_ms]
+
+    # e2e through the public serving call with pinned host buffers
+    h_in = [m.query_input.cpu().pin_memory() for m in eng.models]
+    h_out = [torch.empty_like(m.query_output, device="cpu").pin_memory() for m in eng.models]
+    for _ in range(args.warmup):
+        eng.serve_round(h_in, h_out, stream)
+    barrier()
+    e2e_times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        eng.serve_round(h_in, h_out, stream)
+        e2e_times.append(time.perf_counter() - t0)
+    barrier()
+    e2e_s = max_over_ranks(sum(e2e_times) / len(e2e_times))
+    h2d = sum(t.numel() * t.element_size() for t in h_in)
+    d2h = sum(t.numel() * t.element_size() for t in h_out)
+
+    # Table-1 analogue: R tenants x conv2_2 (256,128,1152) b1, L2 flushed between steps
+    table1 = None
+    if args.table1 and rank == 0 and world == 1:
+        table1 = run_table1(torch, [int(r) for r in args.table1.split(",")], dev, stream)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    tf = lambda ms: world * flops_round / (ms / 1e3) / 1e12  # noqa: E731
+    packed = results["packed"]
+    value = tf(packed["ms_per_step"])
+    p99 = nearest_rank(packed["per_step_ms"], 99.0)
+    # roofline of the super-kernel (dominant kernel): algorithmic flops per launch / event-timed duration
+    sk_flops = [k.planned_cost.flops for k in rnd.kernels]
+    achieved = sum(sk_flops) / (sum(sk_avg) / 1e3) / 1e12
+    traffic = None
+    prof = os.path.join(HERE, "profiles", "superkernel_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    attain_s = sum(max(L.flops(args.batch) / (burst * 1e12), L.compulsory_bytes(args.batch) / (hbm * 1e9))
+                   for L in layers) * T
+    cpu = None
+    if world == 1:
+        port = CpuPort(layers, args.batch)
+        cpu_tf, reps_cpu, el = port.sample(args.cpu_seconds)
+        cores = port.cores
+        cpu = {"value": cpu_tf, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+               "sample": f"{reps_cpu} x one {args.model}@{args.image} b{args.batch} tenant pass "
+                         f"(numpy fp32 im2col+BLAS, oracle/cpu_conv.py), {el:.1f} s"}
+    line = {
+        "metric": "packed multi-tenant conv TFLOP/s vs time-/space-only; p99 query latency",
+        "value": value,
+        "unit": "TFLOP/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": packed["ms_per_step"],
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (U(-1,1) inputs, Kaiming-normal weights, seed 42)",
+        "config": {
+            "workload": f"{T} tenants/GPU x {args.model}@{args.image} ({len(layers)} ops: convs + fc), "
+                        f"batch {args.batch} per tenant query (BASELINE configs[1])",
+            "tenants_per_gpu": T, "batch": args.batch, "placement": "tenant-sharded, no collective",
+            "planner": f"space-time form_batches (max_waves={args.max_waves}; 1 = reference plan parity); "
+                       f"packed = round program (1 persistent launch/round), modes.packed_per_plan = 1 launch "
+                       f"per formed super-kernel",
+            "superkernels_per_round": len(rnd.kernels), "tiles_per_round": sum(k.planned_cost.blocks
+                                                                             for k in rnd.kernels),
+            "l2": f"inputs larger than L2 ({eng.compulsory_bytes_per_round() / 1e6:.0f} MB compulsory/round)",
+        },
+        "modes": {
+            name: {"tflops": tf(r["ms_per_step"]), "ms_per_step": r["ms_per_step"], "launches_per_step": r["launches"],
+                   "p99_ms": nearest_rank(r["per_step_ms"], 99.0)}
+            for name, r in results.items()
+        },
+        "packed_over_space_only": results["space_only"]["ms_per_step"] / packed["ms_per_step"],
+        "packed_over_time_only": results["time_only"]["ms_per_step"] / packed["ms_per_step"],
+        "p99_query_latency_ms": p99,
+        "roofline": {
+            "bound": "tensor", "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
+            "frac": achieved / sustained, "traffic": traffic,
+            "peak_source": f"{peak_src} bf16 sustained (MEASURED_PEAKS.json bf16_tflops_sustained)",
+            "kernel": "gmb::dev::superkernel", "launches_per_round": len(sk_avg),
+            "avg_launch_us": sum(sk_avg) / len(sk_avg) * 1e3,
+            "attainable_tflops": flops_round / attain_s / 1e12 if attain_s else None,
+            "frac_of_attainable": (value / world) / (flops_round / attain_s / 1e12) if attain_s else None,
+        },
+        "e2e": {"value": world * flops_round / e2e_s / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
+                "api": "SpaceTimeEngine.serve_round (plan_round + cached graph replay), pinned host buffers"},
+        "gpu_launches": args.steps * g_packed.kernels,
+        "clocks": clocks.summary(),
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    if table1 is not None:
+        line["table1"] = table1
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_table1(torch, rs, dev, stream):
+    """Paper Table 1 analogue on B200: R tenants each issuing conv2_2 (b1)."""
+    from paper_1901_00041_b200.engine import SpaceTimeEngine
+    from paper_1901_00041_b200 import workload as W
+    flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def flush():
+        flush_buf.fill_(1)
+
+    rows = []
+    for r in rs:
+        eng = SpaceTimeEngine([W.conv2_2()] * r, [1] * r, device_index=dev.index)
+        rnd = eng.plan_round()
+        gs = {"packed": eng.capture_round(rnd), "time_only": eng.capture_serial("time_only"),
+              "space_only": eng.capture_serial("space_only")}
+        row = {"R": r, "superkernels": len(rnd.kernels)}
+        for name, g in gs.items():
+            for _ in range(3):
+                g.launch(stream.cuda_stream)
+            per, _ = time_graph(torch, g, stream, 10, flush=flush)
+            ms = sum(per) / len(per)
+            row[name + "_tflops"] = eng.flops_per_round() / (ms / 1e3) / 1e12
+        row["over_space_only"] = row["packed_tflops"] / row["space_only_tflops"]
+        row["over_time_only"] = row["packed_tflops"] / row["time_only_tflops"]
+        rows.append(row)
+        del eng, gs
+    from paper_1901_00041_b200.scheduler import geomean
+    return {"workload": "conv2_2 (256,128,1152) b1 per tenant, L2 flushed between steps",
+            "rows": rows,
+            "geomean_over_space_only": geomean([r["over_space_only"] for r in rows]),
+            "geomean_over_time_only": geomean([r["over_time_only"] for r in rows])}
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

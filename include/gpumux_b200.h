@@ -98,7 +98,8 @@ typedef struct gm_batch_policy {    /* BatchPolicy, scheduler.hpp:28-34 */
   double max_wait;                  /* seconds */
   int64_t target_batch;
   int32_t allow_variable_size;
-  int32_t reserved0;
+  int32_t max_waves;                /* B200 extension: waves one super-kernel may fill;
+                                       0/1 = the reference's one-wave cap */
   double slo_safety_margin;
   double variable_inefficiency;
 } gm_batch_policy;
@@ -313,6 +314,16 @@ void gm_destroy(gm_ctx* ctx);
 int gm_ctx_queue(gm_ctx* ctx, gm_queue** q);
 int gm_ctx_cache(gm_ctx* ctx, gm_cache** c);
 int gm_ctx_device_spec(const gm_ctx* ctx, gm_device_spec* out);
+/* Replace the BatchPolicy gm_plan_round uses (e.g. parity vs b200 mode). */
+int gm_ctx_set_policy(gm_ctx* ctx, const gm_batch_policy* p);
+/* Execution options of the device runtime (none changes results):
+ *   "pdl"               programmatic dependent launch between launches (1)
+ *   "split_k"           round programs split few-tile long-K members (0)
+ *   "max_splits"        split-K fan-out cap (4)
+ *   "narrow_min_tiles"  narrow a member's N tile (256/128/64) until it has at
+ *                       least this many tiles; 0 = off; applies to tenants
+ *                       registered afterwards (0) */
+int gm_ctx_set_option(gm_ctx* ctx, const char* name, int64_t value);
 
 /* Registers a tenant and builds its per-layer member descriptors (TMA maps)
  * on the device.  Replaces make_tenants (workload.cpp:113-128). */
@@ -350,6 +361,41 @@ int gm_plans_times(const gm_plans* p, size_t i, int64_t* start, int64_t* end);
  * capturable once prepared).  *launches = kernels launched. */
 int gm_dispatch_plans(gm_ctx* ctx, const gm_plans* p, uint64_t stream, int32_t* launches);
 int gm_prepare_plans(gm_ctx* ctx, const gm_plans* p);
+/* ---- CUDA-graph launch programs (the B200 meaning of "cache super-kernels
+ * as workloads stabilize"): a steady-state plan stream is
+ * captured once and replayed with one cudaGraphLaunch. */
+enum gm_mode { GM_MODE_PACKED = 0, GM_MODE_TIME_ONLY = 1, GM_MODE_SPACE_ONLY = 2 };
+typedef struct gm_graph gm_graph;
+/* Packed: every plan of `p`, in order, one super-kernel launch each. */
+int gm_graph_capture_plans(gm_ctx* ctx, const gm_plans* p, int timed, gm_graph** out);
+/* Baselines over the same kernel code (run_time_mux sim.cpp:188-292 /
+ * run_spatial sim.cpp:298-373 mode definitions): every layer of every listed
+ * tenant as its own single-member launch — TIME_ONLY serially on one stream in
+ * tenant order, SPACE_ONLY on one stream per tenant, forked and joined. */
+int gm_graph_capture_serial(gm_ctx* ctx, const int32_t* tenants, size_t n, int mode, int timed,
+                            gm_graph** out);
+/* Round program: every plan of `p` (a round from gm_plan_round) in ONE
+ * persistent super-kernel launch.  Tiles keep plan order; a member's
+ * activations are loaded only after every tile of the same tenant's previous
+ * layer is stored (device-side completion counters), weights stream ahead.
+ * The per-plan launch boundary of the reference (one SuperKernel = one
+ * launch) becomes a dependency edge, so no SM drains between plans. */
+int gm_dispatch_round(gm_ctx* ctx, const gm_plans* p, uint64_t stream, int32_t* launches);
+int gm_graph_capture_round(gm_ctx* ctx, const gm_plans* p, int timed, gm_graph** out);
+/* Profiling: run the round program once with in-kernel %globaltimer stamps,
+ * 6 per tile in round-tile order: producer first issue, activation gate
+ * passed, first stage landed (MMA), last MMA committed, accumulator ready
+ * (epilogue), stores issued.  gm_round_tiles lists the round's tiles
+ * (member = registered slot, flags = plan index). */
+int gm_trace_round(gm_ctx* ctx, const gm_plans* p, uint64_t stream, uint64_t* out, size_t cap, size_t* n_tiles);
+int gm_round_tiles(gm_ctx* ctx, const gm_plans* p, gm_tile* out, size_t cap, size_t* n);
+int gm_graph_launch(gm_graph* g, uint64_t stream);
+int gm_graph_launch_count(const gm_graph* g, int32_t* superkernels, int32_t* kernels);
+/* timed graphs: synchronizes on the last launch and returns the elapsed ms of
+ * every super-kernel launch (external event pairs captured around each). */
+int gm_graph_kernel_times(gm_graph* g, float* ms, size_t cap, size_t* n);
+void gm_graph_destroy(gm_graph* g);
+
 /* Total super-kernel launches and tiles issued by this ctx so far. */
 int gm_ctx_launch_stats(const gm_ctx* ctx, int64_t* superkernels, int64_t* prepasses,
                         int64_t* tiles);

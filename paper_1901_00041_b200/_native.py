@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libgpumux_b200.so")
 
 GM_OK, GM_EINVAL, GM_ECONFIG, GM_EOOM, GM_EINTERNAL, GM_ECUDA, GM_ERANGE, GM_ENODEV = range(8)
 GM_LAYER_GEMM, GM_LAYER_CONV = 0, 1
+GM_MODE_PACKED, GM_MODE_TIME_ONLY, GM_MODE_SPACE_ONLY = 0, 1, 2
 
 
 class gm_gemm_shape(C.Structure):
@@ -52,7 +53,7 @@ class gm_kernel_request(C.Structure):
 
 class gm_batch_policy(C.Structure):
     _fields_ = [("max_wait", C.c_double), ("target_batch", C.c_int64), ("allow_variable_size", C.c_int32),
-                ("reserved0", C.c_int32), ("slo_safety_margin", C.c_double), ("variable_inefficiency", C.c_double)]
+                ("max_waves", C.c_int32), ("slo_safety_margin", C.c_double), ("variable_inefficiency", C.c_double)]
 
 
 class gm_tenant_health(C.Structure):
@@ -166,6 +167,8 @@ _SIGS = {
     "gm_ctx_queue": (C.c_int, [C.c_void_p, P(C.c_void_p)]),
     "gm_ctx_cache": (C.c_int, [C.c_void_p, P(C.c_void_p)]),
     "gm_ctx_device_spec": (C.c_int, [C.c_void_p, P(gm_device_spec)]),
+    "gm_ctx_set_policy": (C.c_int, [C.c_void_p, P(gm_batch_policy)]),
+    "gm_ctx_set_option": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64]),
     "gm_register_tenant": (C.c_int, [C.c_void_p, P(gm_tenant_desc), P(C.c_int32)]),
     "gm_layer_shape": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, P(gm_gemm_shape)]),
     "gm_tenant_count": (C.c_int, [C.c_void_p, P(C.c_int32)]),
@@ -178,6 +181,17 @@ _SIGS = {
     "gm_plans_times": (C.c_int, [C.c_void_p, C.c_size_t, P(C.c_int64), P(C.c_int64)]),
     "gm_prepare_plans": (C.c_int, [C.c_void_p, C.c_void_p]),
     "gm_dispatch_plans": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, P(C.c_int32)]),
+    "gm_graph_capture_plans": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, P(C.c_void_p)]),
+    "gm_graph_capture_serial": (C.c_int, [C.c_void_p, P(C.c_int32), C.c_size_t, C.c_int, C.c_int,
+                                          P(C.c_void_p)]),
+    "gm_dispatch_round": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, P(C.c_int32)]),
+    "gm_graph_capture_round": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, P(C.c_void_p)]),
+    "gm_trace_round": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, P(C.c_uint64), C.c_size_t, P(C.c_size_t)]),
+    "gm_round_tiles": (C.c_int, [C.c_void_p, C.c_void_p, P(gm_tile), C.c_size_t, P(C.c_size_t)]),
+    "gm_graph_launch": (C.c_int, [C.c_void_p, C.c_uint64]),
+    "gm_graph_launch_count": (C.c_int, [C.c_void_p, P(C.c_int32), P(C.c_int32)]),
+    "gm_graph_kernel_times": (C.c_int, [C.c_void_p, P(C.c_float), C.c_size_t, P(C.c_size_t)]),
+    "gm_graph_destroy": (None, [C.c_void_p]),
     "gm_ctx_launch_stats": (C.c_int, [C.c_void_p, P(C.c_int64), P(C.c_int64), P(C.c_int64)]),
 }
 

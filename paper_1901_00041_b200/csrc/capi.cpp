@@ -58,6 +58,7 @@ Policy to_policy(const gm_batch_policy& p) {
   o.max_wait = p.max_wait;
   o.target_batch = p.target_batch;
   o.allow_variable_size = p.allow_variable_size != 0;
+  o.max_waves = p.max_waves < 1 ? 1 : p.max_waves;
   o.slo_safety_margin = p.slo_safety_margin;
   o.variable_inefficiency = p.variable_inefficiency;
   return o;
@@ -167,6 +168,7 @@ void gm_batch_policy_default(gm_batch_policy* out) {
   out->max_wait = p.max_wait;
   out->target_batch = p.target_batch;
   out->allow_variable_size = p.allow_variable_size;
+  out->max_waves = static_cast<int32_t>(p.max_waves);
   out->slo_safety_margin = p.slo_safety_margin;
   out->variable_inefficiency = p.variable_inefficiency;
 }

@@ -79,7 +79,7 @@ Device b200_device() {
   d.mem_capacity = 180e9;
   d.process_context_bytes = 500e6;
   d.tile_m = 128;                // super-kernel CTA tile (UMMA M)
-  d.tile_n = 128;                // super-kernel CTA tile (UMMA N)
+  d.tile_n = 256;                // super-kernel CTA tile (max UMMA N)
   d.space_sched_penalty = 1.0;
   d.launch_serialization = 1.0;
   return d;
@@ -237,7 +237,8 @@ Cost plan_cost(std::span<const Request> members, bool uniform, const Policy& p, 
 std::vector<Plan> form_plans(Queue& q, TimeNs now, const Policy& p, const Device& d) {
   std::vector<Plan> out;
   const TimeNs max_wait_ns = to_ns(p.max_wait);
-  const std::int64_t slots = d.slots();
+  // block slots one super-kernel may fill (reference: exactly one wave)
+  const std::int64_t slots = d.slots() * std::max<std::int64_t>(1, p.max_waves);
 
   if (p.allow_variable_size) {
     // Variable-size (MAGMA-style) mode: one pool in arrival order, chunks

@@ -112,6 +112,11 @@ struct Policy {
   bool allow_variable_size = false;
   double slo_safety_margin = 0.0;
   double variable_inefficiency = 1.10;
+  // B200 extension (not in the reference): a formed super-kernel may fill up
+  // to `max_waves` waves of block slots.  1 == the reference's one-wave cap
+  // (scheduler.cpp:170-171, :135-144) and is the plan-parity setting; the
+  // persistent super-kernel makes larger values meaningful ("b200 mode").
+  std::int64_t max_waves = 1;
 };
 
 // scheduler.hpp:37-42

@@ -39,12 +39,28 @@ void* driver_entry(const char* name) {
 
 // tcgen05 kind::f16 instruction descriptor: D fp32, A/B bf16, both K-major,
 // N>>3 at [17,23), M>>4 at [24,29).
-uint32_t make_idesc(int n) {
-  const uint32_t umma_n = static_cast<uint32_t>(std::min(dev::kBN, (n + 15) / 16 * 16));
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((umma_n >> 3) << 17) | (static_cast<uint32_t>(dev::kBM >> 4) << 24);
+uint32_t make_idesc(int umma_n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(umma_n >> 3) << 17) |
+         (static_cast<uint32_t>(dev::kBM >> 4) << 24);
 }
 
+// Box rows per member: only real rows move (a small-M member's A box and a
+// small-N member's B box shrink; the MMA's extra A rows are discarded).
+int a_box_rows(int64_t m) { return static_cast<int>(std::min<int64_t>(dev::kBM, (m + 7) / 8 * 8)); }
+int b_box_rows(int64_t n, int bn) { return static_cast<int>(std::min<int64_t>(bn, (n + 15) / 16 * 16)); }
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Tile width per member: the widest of {bn, bn/2, ..., 64} that still gives
+// the member >= 32 tiles, so few-tile (small-M) members spread their long K
+// loops over more SMs instead of serialising on a handful.
+int pick_n_tile(const Shape& s, int bn, int64_t min_tiles) {
+  if (min_tiles <= 0) return bn;
+  const int64_t mt = (s.m + dev::kBM - 1) / dev::kBM;
+  for (int w = bn; w > 64; w /= 2)
+    if (mt * ((s.n + w - 1) / w) >= min_tiles) return w;
+  return 64;
+}
 
 }  // namespace
 
@@ -55,6 +71,8 @@ struct Operator {
   Conv conv;
   int batch = 1;
   int slot = -1;    // index into the device MemberDesc array
+  int tenant = -1, layer = -1;
+  int n_tile = 256;  // output columns per tile (<= the kernel's BN)
   bool prepass = false;
   const void* x = nullptr;
   void* scratch = nullptr;  // explicit-im2col rows [M, ldk]
@@ -65,6 +83,25 @@ struct Prepared {
   dev::TileEntry* tiles = nullptr;
   int n_tiles = 0;
   std::vector<int> prepass_ops;  // indices into Runtime::flat
+  // round programs only: one completion counter per member instance
+  uint32_t* counters = nullptr;
+  uint32_t* targets = nullptr;
+  int n_counters = 0;
+  // split-K workspace: fp32 [n_ws * 128, bn] + per (tile, quarter) arrivals
+  float* ws = nullptr;
+  CUtensorMap* ws_map = nullptr;  // device copy, 64 B aligned
+  uint32_t* split_ctr = nullptr;
+  int n_ws = 0;
+  std::vector<uint16_t> tile_plan;  // round programs: plan index of every tile (profiling)
+
+  void release() {
+    cudaFree(tiles);
+    cudaFree(counters);
+    cudaFree(targets);
+    cudaFree(ws);
+    cudaFree(ws_map);
+    cudaFree(split_ctr);
+  }
 };
 
 struct Runtime {
@@ -80,18 +117,30 @@ struct Runtime {
   dev::MemberDesc* d_desc = nullptr;
   size_t d_cap = 0;
   std::unordered_map<std::string, Prepared> prepared;
+  std::unordered_map<std::string, Prepared> rounds;
   int64_t n_superkernels = 0, n_prepasses = 0, n_tiles = 0;
+  bool pdl = true;      // programmatic dependent launch between consecutive super-kernels
+  bool split_k = false;      // round programs split few-tile long-K members (opt-in)
+  int64_t max_splits = 4;
+  int64_t narrow_min_tiles = 0;  // >0: narrow a member's N tile until it has this many tiles
+  int bn = 256;     // N tile of the super-kernel (== DeviceSpec.tile_n)
+  int smem_bytes = 0;
+  const void* kernel = nullptr;
 
   ~Runtime() {
     if (device < 0) return;
     cudaSetDevice(device);
     cudaDeviceSynchronize();
-    for (auto& [k, p] : prepared) cudaFree(p.tiles);
+    for (auto& [k, p] : prepared) p.release();
+    for (auto& [k, p] : rounds) p.release();
     for (Operator& op : flat) cudaFree(op.scratch);
     cudaFree(d_desc);
   }
 
-  void init(int dev_index) {
+  void init(int dev_index, const Device& spec) {
+    if (spec.tile_m != dev::kBM || (spec.tile_n != 128 && spec.tile_n != 256))
+      throw std::invalid_argument("b200 runtime needs tile_m 128 and tile_n 128 or 256 (the super-kernel tile)");
+    bn = static_cast<int>(spec.tile_n);
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) throw NoDevice("no CUDA device visible");
     if (dev_index >= count) throw NoDevice("CUDA device index out of range");
@@ -106,7 +155,14 @@ struct Runtime {
     cuda_check(cudaDriverGetVersion(&driver_version), "cudaDriverGetVersion");
     encode_tiled = reinterpret_cast<EncodeTiledFn>(driver_entry("cuTensorMapEncodeTiled"));
     encode_im2col = reinterpret_cast<EncodeIm2colFn>(driver_entry("cuTensorMapEncodeIm2col"));
-    cuda_check(cudaFuncSetAttribute(dev::superkernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kSmemBytes),
+    if (bn == 256) {
+      kernel = reinterpret_cast<const void*>(&dev::superkernel<256>);
+      smem_bytes = dev::Cfg<256>::kSmemBytes;
+    } else {
+      kernel = reinterpret_cast<const void*>(&dev::superkernel<128>);
+      smem_bytes = dev::Cfg<128>::kSmemBytes;
+    }
+    cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes),
                "cudaFuncSetAttribute");
   }
 
@@ -127,7 +183,21 @@ struct Runtime {
   // NHWC activation as an im2col source (fprop, dilation 1).  Corner arrays
   // are in {W, H} order (CUTLASS convention); all convs routed here are
   // square with symmetric padding, so the order is immaterial.
-  void im2col_map(CUtensorMap* map, const void* x, const Conv& c, int batch) {
+  // Output [rows, cols] row-major: 32 x 32 store boxes, 64 B swizzle (the
+  // epilogue staging layout).
+  void store_map(CUtensorMap* map, void* base, int64_t rows, int64_t cols) {
+    if (!aligned16(base)) throw std::invalid_argument("register_tenant: output must be 16-byte aligned");
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols * 2)};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(dev::kEpiChunk), 32};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_tiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled(store) failed (" + std::to_string(int(r)) + ")");
+  }
+
+  void im2col_map(CUtensorMap* map, const void* x, const Conv& c, int batch, int pixels) {
     if (!aligned16(x)) throw std::invalid_argument("conv input must be 16-byte aligned");
     const cuuint64_t dims[4] = {static_cast<cuuint64_t>(c.in_channels), static_cast<cuuint64_t>(c.image_w),
                                 static_cast<cuuint64_t>(c.image_h), static_cast<cuuint64_t>(batch)};
@@ -138,7 +208,8 @@ struct Runtime {
     const int upper[2] = {static_cast<int>(c.padding - (c.kernel_w - 1)), static_cast<int>(c.padding - (c.kernel_h - 1))};
     const cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(c.stride), static_cast<cuuint32_t>(c.stride), 1};
     const CUresult r = encode_im2col(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides,
-                                     lower, upper, dev::kBK, dev::kBM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                     lower, upper, dev::kBK, static_cast<cuuint32_t>(pixels), estr,
+                                     CU_TENSOR_MAP_INTERLEAVE_NONE,
                                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeIm2col failed (" + std::to_string(int(r)) + ")");
@@ -160,27 +231,30 @@ struct Runtime {
       std::memset(&md, 0, sizeof(md));
       op.kind = L.kind;
       op.x = L.x;
+      op.tenant = static_cast<int>(tenant_ops.size());
+      op.layer = static_cast<int>(i);
       if (!L.x || !L.w || !L.y) throw std::invalid_argument("register_tenant: null operand pointer");
       if (!aligned16(L.y)) throw std::invalid_argument("register_tenant: output must be 16-byte aligned");
       if (L.kind == GM_LAYER_CONV) {
         op.conv = to_conv(L.conv);
         op.batch = L.batch < 1 ? 1 : L.batch;
         op.shape = with_batch(lower_conv(op.conv), op.batch);
+        op.n_tile = pick_n_tile(op.shape, bn, narrow_min_tiles);
         const Conv& c = op.conv;
         const int64_t K = op.shape.k;
         const int64_t ldw = L.ldw > 0 ? L.ldw : K;
         if (ldw < K) throw std::invalid_argument("register_tenant: ldw < R*S*Cin");
-        tiled_map(&md.b, L.w, op.shape.n, K, ldw, dev::kBN);
+        tiled_map(&md.b, L.w, op.shape.n, K, ldw, b_box_rows(op.shape.n, op.n_tile));
         const int64_t P = (c.image_h + 2 * c.padding - c.kernel_h) / c.stride + 1;
         const int64_t Q = (c.image_w + 2 * c.padding - c.kernel_w) / c.stride + 1;
         const bool pointwise = c.kernel_h == 1 && c.kernel_w == 1 && c.stride == 1 && c.padding == 0;
         if (pointwise && c.in_channels % 8 == 0) {
           md.a_mode = dev::kATiled;  // 1x1 stride-1 conv == GEMM over NHWC rows
-          tiled_map(&md.a, L.x, op.shape.m, c.in_channels, c.in_channels, dev::kBM);
+          tiled_map(&md.a, L.x, op.shape.m, c.in_channels, c.in_channels, a_box_rows(op.shape.m));
         } else if (c.in_channels % dev::kBK == 0 && c.kernel_h == c.kernel_w && c.stride <= 8 &&
                    c.padding <= 127 && c.kernel_h - 1 - c.padding <= 128) {
           md.a_mode = dev::kAIm2col;  // implicit GEMM through the TMA im2col unit
-          im2col_map(&md.a, L.x, c, op.batch);
+          im2col_map(&md.a, L.x, c, op.batch, a_box_rows(op.shape.m));
           md.pq = static_cast<int32_t>(P * Q);
           md.q = static_cast<int32_t>(Q);
           md.stride = static_cast<int32_t>(c.stride);
@@ -192,29 +266,31 @@ struct Runtime {
           op.prepass = true;
           op.ldk = (K + 7) / 8 * 8;
           cuda_check(cudaMalloc(&op.scratch, static_cast<size_t>(op.shape.m * op.ldk * 2)), "cudaMalloc(im2col)");
-          tiled_map(&md.a, op.scratch, op.shape.m, K, op.ldk, dev::kBM);
+          tiled_map(&md.a, op.scratch, op.shape.m, K, op.ldk, a_box_rows(op.shape.m));
         }
       } else if (L.kind == GM_LAYER_GEMM) {
         op.shape = to_shape(L.gemm);
+        op.n_tile = pick_n_tile(op.shape, bn, narrow_min_tiles);
         if (!op.shape.valid()) throw std::invalid_argument("register_tenant: invalid GEMM shape");
         const int64_t ldx = L.ldx > 0 ? L.ldx : op.shape.k;
         const int64_t ldw = L.ldw > 0 ? L.ldw : op.shape.k;
         md.a_mode = dev::kATiled;
-        tiled_map(&md.a, L.x, op.shape.m, op.shape.k, ldx, dev::kBM);
-        tiled_map(&md.b, L.w, op.shape.n, op.shape.k, ldw, dev::kBN);
+        tiled_map(&md.a, L.x, op.shape.m, op.shape.k, ldx, a_box_rows(op.shape.m));
+        tiled_map(&md.b, L.w, op.shape.n, op.shape.k, ldw, b_box_rows(op.shape.n, op.n_tile));
       } else {
         throw std::invalid_argument("register_tenant: unknown layer kind");
       }
       if (op.shape.n % 8 != 0) throw std::invalid_argument("register_tenant: output channels must be a multiple of 8");
       if (op.shape.m > int64_t(0xFFFF) * dev::kBM || op.shape.m > INT32_MAX)
         throw std::invalid_argument("register_tenant: M too large for the tile table");
-      md.y = static_cast<__nv_bfloat16*>(L.y);
-      md.ldy = op.shape.n;
+      store_map(&md.c, L.y, op.shape.m, op.shape.n);
       md.m = static_cast<int32_t>(op.shape.m);
       md.n = static_cast<int32_t>(op.shape.n);
       md.k_blocks = static_cast<int32_t>((op.shape.k + dev::kBK - 1) / dev::kBK);
-      md.idesc = make_idesc(static_cast<int>(op.shape.n));
+      md.idesc = make_idesc(b_box_rows(op.shape.n, op.n_tile));
+      md.tx_bytes = static_cast<uint32_t>((a_box_rows(op.shape.m) + b_box_rows(op.shape.n, op.n_tile)) * dev::kBK * 2);
       md.relu = L.relu ? 1 : 0;
+      md.n_tile = op.n_tile;
       op.slot = static_cast<int>(host_desc.size() + descs.size());
       if (op.slot > 0xFFFF) throw std::invalid_argument("register_tenant: too many registered operators");
       descs.push_back(md);
@@ -282,11 +358,11 @@ struct Runtime {
     for (int f : members) {
       const Operator& op = flat[f];
       const int64_t mt = (op.shape.m + dev::kBM - 1) / dev::kBM;
-      const int64_t nt = (op.shape.n + dev::kBN - 1) / dev::kBN;
+      const int64_t nt = (op.shape.n + op.n_tile - 1) / op.n_tile;
       for (int64_t a = 0; a < mt; ++a)
         for (int64_t b = 0; b < nt; ++b)
           table.push_back(dev::TileEntry{static_cast<uint16_t>(op.slot), 0, static_cast<uint16_t>(a),
-                                         static_cast<uint16_t>(b)});
+                                         static_cast<uint16_t>(b), -1, -1, 0, 0, -1});
       if (op.prepass) p.prepass_ops.push_back(f);
     }
     p.n_tiles = static_cast<int>(table.size());
@@ -296,14 +372,113 @@ struct Runtime {
     return prepared.emplace(key, std::move(p)).first->second;
   }
 
-  int launch(Prepared& p, cudaStream_t stream) {
+  // Round program: every plan of a round, in plan order, as ONE persistent
+  // launch.  Member instances get completion counters; a member depends on the
+  // same tenant's previous layer when that layer ran earlier in the round.
+  Prepared& prepare_round(const std::vector<std::vector<int>>& plans) {
+    std::string key = "R";
+    for (const auto& pl : plans) {
+      for (int f : pl) {
+        key += std::to_string(f);
+        key += ',';
+      }
+      key += '|';
+    }
+    auto it = rounds.find(key);
+    if (it != rounds.end()) return it->second;
+    Prepared p;
+    std::vector<dev::TileEntry> table;
+    std::vector<uint32_t> targets;
+    std::unordered_map<int, int> last_instance;  // flat op -> instance id
+    int n_ws = 0;
+    for (const auto& pl : plans) {
+      int64_t plan_tiles = 0;
+      for (int f : pl)
+        plan_tiles += ((flat[f].shape.m + dev::kBM - 1) / dev::kBM) * ((flat[f].shape.n + flat[f].n_tile - 1) / flat[f].n_tile);
+      for (int f : pl) {
+        const Operator& op = flat[f];
+        const int inst = static_cast<int>(targets.size());
+        int dep = -1;
+        if (op.layer > 0) {
+          auto prev = last_instance.find(tenant_ops[op.tenant][op.layer - 1]);
+          if (prev != last_instance.end()) dep = prev->second;
+        }
+        last_instance[f] = inst;
+        const int64_t mt = (op.shape.m + dev::kBM - 1) / dev::kBM;
+        const int64_t nt = (op.shape.n + op.n_tile - 1) / op.n_tile;
+        const int kb = static_cast<int>((op.shape.k + dev::kBK - 1) / dev::kBK);
+        // Split-K when the plan cannot fill the SMs and the K loop is long:
+        // about two waves of tiles, at least 4 k-blocks per split.
+        int splits = 1;
+        if (split_k && plan_tiles < sms && kb >= 16) {
+          splits = static_cast<int>(std::min<int64_t>({kb / 8, (sms + plan_tiles - 1) / plan_tiles, max_splits}));
+          const int chunk = (kb + splits - 1) / splits;
+          splits = (kb + chunk - 1) / chunk;
+        }
+        targets.push_back(static_cast<uint32_t>(mt * nt * 4));  // 4 epilogue warps arrive per output tile
+        for (int64_t a = 0; a < mt; ++a)
+          for (int64_t b = 0; b < nt; ++b) {
+            if (splits == 1) {
+              table.push_back(dev::TileEntry{static_cast<uint16_t>(op.slot), 1, static_cast<uint16_t>(a),
+                                             static_cast<uint16_t>(b), inst, dep, 0, 0, -1});
+              continue;
+            }
+            const int chunk = (kb + splits - 1) / splits;
+            for (int s = 0; s < splits; ++s)
+              table.push_back(dev::TileEntry{static_cast<uint16_t>(op.slot), static_cast<uint16_t>(splits),
+                                             static_cast<uint16_t>(a), static_cast<uint16_t>(b), inst, dep,
+                                             static_cast<uint16_t>(s * chunk),
+                                             static_cast<uint16_t>(std::min(kb, (s + 1) * chunk)), n_ws});
+            ++n_ws;
+          }
+        if (op.prepass) p.prepass_ops.push_back(f);
+      }
+      p.tile_plan.resize(table.size(), static_cast<uint16_t>(&pl - plans.data()));
+    }
+    p.n_tiles = static_cast<int>(table.size());
+    p.n_counters = static_cast<int>(targets.size());
+    p.n_ws = n_ws;
+    if (n_ws > 0) {
+      const size_t ws_bytes = static_cast<size_t>(n_ws) * dev::kBM * bn * sizeof(float);
+      cuda_check(cudaMalloc(&p.ws, ws_bytes), "cudaMalloc(split workspace)");
+      cuda_check(cudaMemset(p.ws, 0, ws_bytes), "clear split workspace");
+      cuda_check(cudaMalloc(&p.split_ctr, static_cast<size_t>(n_ws) * 4 * sizeof(uint32_t)), "cudaMalloc(split ctr)");
+      cuda_check(cudaMemset(p.split_ctr, 0, static_cast<size_t>(n_ws) * 4 * sizeof(uint32_t)), "clear split ctr");
+      alignas(64) CUtensorMap map;
+      const cuuint64_t dims[2] = {static_cast<cuuint64_t>(bn), static_cast<cuuint64_t>(n_ws) * dev::kBM};
+      const cuuint64_t strides[1] = {static_cast<cuuint64_t>(bn) * 4};
+      const cuuint32_t box[2] = {16, 32};
+      const cuuint32_t estr[2] = {1, 1};
+      const CUresult r = encode_tiled(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, p.ws, dims, strides, box, estr,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled(workspace) failed (" + std::to_string(int(r)) + ")");
+      cuda_check(cudaMalloc(&p.ws_map, sizeof(CUtensorMap)), "cudaMalloc(ws map)");
+      cuda_check(cudaMemcpy(p.ws_map, &map, sizeof(CUtensorMap), cudaMemcpyHostToDevice), "upload ws map");
+    }
+    cuda_check(cudaMalloc(&p.tiles, std::max<size_t>(1, table.size()) * sizeof(dev::TileEntry)), "cudaMalloc(tiles)");
+    cuda_check(cudaMemcpy(p.tiles, table.data(), table.size() * sizeof(dev::TileEntry), cudaMemcpyHostToDevice),
+               "upload round tiles");
+    cuda_check(cudaMalloc(&p.counters, std::max<size_t>(1, targets.size()) * sizeof(uint32_t)), "cudaMalloc(counters)");
+    cuda_check(cudaMalloc(&p.targets, std::max<size_t>(1, targets.size()) * sizeof(uint32_t)), "cudaMalloc(targets)");
+    cuda_check(cudaMemcpy(p.targets, targets.data(), targets.size() * sizeof(uint32_t), cudaMemcpyHostToDevice),
+               "upload round targets");
+    return rounds.emplace(key, std::move(p)).first->second;
+  }
+
+  // Enqueue one plan: explicit-im2col pre-passes (if any), then the
+  // super-kernel.  `ev` (optional) brackets the super-kernel with external
+  // event records so a captured graph can time it.  `count` is false while
+  // capturing (the graph counts its launches per replay).
+  int launch(Prepared& p, cudaStream_t stream, bool count = true, cudaEvent_t ev_begin = nullptr,
+             cudaEvent_t ev_end = nullptr, uint64_t* trace = nullptr) {
     int launches = 0;
     for (int f : p.prepass_ops) {
       const Operator& op = flat[f];
       const Conv& c = op.conv;
       const int P = static_cast<int>((c.image_h + 2 * c.padding - c.kernel_h) / c.stride + 1);
       const int Q = static_cast<int>((c.image_w + 2 * c.padding - c.kernel_w) / c.stride + 1);
-      const int64_t total = op.shape.m * op.ldk;
+      const int64_t total = op.shape.m * (op.ldk / 8);
       const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, int64_t(sms) * 16));
       dev::im2col_prepass<<<grid, 256, 0, stream>>>(
           static_cast<const __nv_bfloat16*>(op.x), static_cast<__nv_bfloat16*>(op.scratch), op.batch,
@@ -312,14 +487,37 @@ struct Runtime {
           static_cast<int>(c.padding), P, Q, static_cast<int>(op.ldk));
       cuda_check(cudaGetLastError(), "launch im2col_prepass");
       ++launches;
-      ++n_prepasses;
+      if (count) ++n_prepasses;
     }
+    if (p.counters)
+      cuda_check(cudaMemsetAsync(p.counters, 0, static_cast<size_t>(p.n_counters) * sizeof(uint32_t), stream),
+                 "reset round counters");
+    if (ev_begin) cuda_check(cudaEventRecordWithFlags(ev_begin, stream, cudaEventRecordExternal), "event record");
     const int grid = std::max(1, std::min(p.n_tiles, sms));
-    dev::superkernel<<<grid, dev::kThreads, dev::kSmemBytes, stream>>>(d_desc, p.tiles, p.n_tiles);
-    cuda_check(cudaGetLastError(), "launch superkernel");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(dev::kThreads);
+    cfg.dynamicSmemBytes = smem_bytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const dev::MemberDesc* slots = d_desc;
+    const dev::TileEntry* tiles = p.tiles;
+    int n = p.n_tiles;
+    uint32_t* counters = p.counters;
+    const uint32_t* targets = p.targets;
+    dev::RoundArgs ra{counters, targets, p.ws_map, p.ws, p.split_ctr, trace};
+    void* args[4] = {&slots, &tiles, &n, &ra};
+    cuda_check(cudaLaunchKernelExC(&cfg, kernel, args), "launch superkernel");
+    if (ev_end) cuda_check(cudaEventRecordWithFlags(ev_end, stream, cudaEventRecordExternal), "event record");
     ++launches;
-    ++n_superkernels;
-    n_tiles += p.n_tiles;
+    if (count) {
+      ++n_superkernels;
+      n_tiles += p.n_tiles;
+    }
     return launches;
   }
 };
@@ -349,6 +547,71 @@ Runtime& runtime_of(gm_ctx* ctx) {
 }  // namespace
 }  // namespace gmb
 
+// A captured launch program (see gm_graph_* in the header).
+struct gm_graph {
+  gm_ctx* ctx = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<cudaEvent_t> events;  // begin/end pairs when timed
+  std::vector<cudaStream_t> streams;
+  std::vector<cudaEvent_t> joins;
+  int32_t superkernels = 0, kernels = 0;
+  int64_t tiles = 0;
+  ~gm_graph() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    for (cudaEvent_t e : events) cudaEventDestroy(e);
+    for (cudaEvent_t e : joins) cudaEventDestroy(e);
+    for (cudaStream_t s : streams) cudaStreamDestroy(s);
+  }
+};
+
+namespace gmb {
+namespace {
+
+// Capture `body(stream, graph)` on a private stream (thread-local capture
+// mode, so other host threads are unaffected) and instantiate it.
+template <class Body>
+gm_graph* capture(gm_ctx* ctx, Body body) {
+  Runtime& rt = runtime_of(ctx);
+  cuda_check(cudaSetDevice(rt.device), "cudaSetDevice");
+  auto* g = new gm_graph();
+  g->ctx = ctx;
+  try {
+    cudaStream_t cs;
+    cuda_check(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "cudaStreamCreate");
+    g->streams.push_back(cs);
+    cuda_check(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+    try {
+      body(cs, *g);
+    } catch (...) {
+      cudaGraph_t junk = nullptr;
+      cudaStreamEndCapture(cs, &junk);
+      if (junk) cudaGraphDestroy(junk);
+      throw;
+    }
+    cuda_check(cudaStreamEndCapture(cs, &g->graph), "cudaStreamEndCapture");
+    cuda_check(cudaGraphInstantiate(&g->exec, g->graph, 0), "cudaGraphInstantiate");
+  } catch (...) {
+    delete g;
+    throw;
+  }
+  return g;
+}
+
+std::pair<cudaEvent_t, cudaEvent_t> timing_pair(gm_graph& g, bool timed) {
+  if (!timed) return {nullptr, nullptr};
+  cudaEvent_t a, b;
+  cuda_check(cudaEventCreate(&a), "cudaEventCreate");
+  cuda_check(cudaEventCreate(&b), "cudaEventCreate");
+  g.events.push_back(a);
+  g.events.push_back(b);
+  return {a, b};
+}
+
+}  // namespace
+}  // namespace gmb
+
 using namespace gmb;
 
 extern "C" {
@@ -366,7 +629,7 @@ int gm_create(const gm_device_spec* d, const gm_batch_policy* p, const gm_detect
     ctx->cuda_device = cuda_device;
     if (cuda_device >= 0) {
       ctx->rt = new Runtime();
-      ctx->rt->init(cuda_device);
+      ctx->rt->init(cuda_device, ctx->dev);
     }
   } catch (...) {
     delete ctx->rt;
@@ -402,6 +665,33 @@ int gm_ctx_device_spec(const gm_ctx* ctx, gm_device_spec* out) {
   GM_API_BEGIN
   if (!ctx || !out) throw std::invalid_argument("null argument");
   *out = from_device(ctx->dev);
+  GM_API_END
+}
+
+int gm_ctx_set_option(gm_ctx* ctx, const char* name, int64_t value) {
+  GM_API_BEGIN
+  if (!name) throw std::invalid_argument("null argument: name");
+  Runtime& rt = runtime_of(ctx);
+  const std::string n(name);
+  if (n == "pdl") {
+    rt.pdl = value != 0;
+  } else if (n == "split_k") {
+    rt.split_k = value != 0;
+  } else if (n == "max_splits") {
+    if (value < 2 || value > 64) throw std::invalid_argument("max_splits must be in [2, 64]");
+    rt.max_splits = value;
+  } else if (n == "narrow_min_tiles") {
+    rt.narrow_min_tiles = value;  // applies to tenants registered afterwards
+  } else {
+    throw std::invalid_argument("unknown option " + n);
+  }
+  GM_API_END
+}
+
+int gm_ctx_set_policy(gm_ctx* ctx, const gm_batch_policy* p) {
+  GM_API_BEGIN
+  if (!ctx || !p) throw std::invalid_argument("null argument");
+  ctx->pol = to_policy(*p);
   GM_API_END
 }
 
@@ -530,6 +820,175 @@ int gm_dispatch_plans(gm_ctx* ctx, const gm_plans* p, uint64_t stream, int32_t* 
   if (launches) *launches = l;
   GM_API_END
 }
+
+int gm_graph_capture_plans(gm_ctx* ctx, const gm_plans* p, int timed, gm_graph** out) {
+  GM_API_BEGIN
+  if (!p || !out) throw std::invalid_argument("null argument");
+  Runtime& rt = runtime_of(ctx);
+  std::vector<Prepared*> preps;
+  for (const Plan& plan : p->plans) preps.push_back(&rt.prepare(members_of(rt, plan)));
+  *out = capture(ctx, [&](cudaStream_t cs, gm_graph& g) {
+    for (Prepared* pr : preps) {
+      auto ev = timing_pair(g, timed != 0);
+      g.kernels += rt.launch(*pr, cs, false, ev.first, ev.second);
+      g.superkernels += 1;
+      g.tiles += pr->n_tiles;
+    }
+  });
+  GM_API_END
+}
+
+int gm_graph_capture_serial(gm_ctx* ctx, const int32_t* tenants, size_t n, int mode, int timed, gm_graph** out) {
+  GM_API_BEGIN
+  if (!out || (n && !tenants)) throw std::invalid_argument("null argument");
+  if (mode != GM_MODE_TIME_ONLY && mode != GM_MODE_SPACE_ONLY) throw std::invalid_argument("unknown serial mode");
+  Runtime& rt = runtime_of(ctx);
+  std::vector<std::vector<Prepared*>> per_tenant;
+  for (size_t j = 0; j < n; ++j) {
+    rt.op_of(tenants[j], 0);
+    std::vector<Prepared*> v;
+    for (int f : rt.tenant_ops[tenants[j]]) v.push_back(&rt.prepare({f}));
+    per_tenant.push_back(std::move(v));
+  }
+  *out = capture(ctx, [&](cudaStream_t cs, gm_graph& g) {
+    if (mode == GM_MODE_TIME_ONLY) {
+      for (auto& v : per_tenant)
+        for (Prepared* pr : v) {
+          auto ev = timing_pair(g, timed != 0);
+          g.kernels += rt.launch(*pr, cs, false, ev.first, ev.second);
+          g.superkernels += 1;
+          g.tiles += pr->n_tiles;
+        }
+      return;
+    }
+    cudaEvent_t fork;
+    cuda_check(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "cudaEventCreate");
+    g.joins.push_back(fork);
+    cuda_check(cudaEventRecord(fork, cs), "cudaEventRecord");
+    std::vector<cudaEvent_t> done;
+    for (auto& v : per_tenant) {
+      cudaStream_t s;
+      cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+      g.streams.push_back(s);
+      cuda_check(cudaStreamWaitEvent(s, fork, 0), "cudaStreamWaitEvent");
+      for (Prepared* pr : v) {
+        auto ev = timing_pair(g, timed != 0);
+        g.kernels += rt.launch(*pr, s, false, ev.first, ev.second);
+        g.superkernels += 1;
+        g.tiles += pr->n_tiles;
+      }
+      cudaEvent_t e;
+      cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+      g.joins.push_back(e);
+      cuda_check(cudaEventRecord(e, s), "cudaEventRecord");
+      done.push_back(e);
+    }
+    for (cudaEvent_t e : done) cuda_check(cudaStreamWaitEvent(cs, e, 0), "cudaStreamWaitEvent");
+  });
+  GM_API_END
+}
+
+int gm_dispatch_round(gm_ctx* ctx, const gm_plans* p, uint64_t stream, int32_t* launches) {
+  GM_API_BEGIN
+  if (!p) throw std::invalid_argument("null argument: plans");
+  Runtime& rt = runtime_of(ctx);
+  std::vector<std::vector<int>> plans;
+  for (const Plan& plan : p->plans) plans.push_back(members_of(rt, plan));
+  const int l = rt.launch(rt.prepare_round(plans), reinterpret_cast<cudaStream_t>(stream));
+  if (launches) *launches = l;
+  GM_API_END
+}
+
+int gm_trace_round(gm_ctx* ctx, const gm_plans* p, uint64_t stream, uint64_t* out, size_t cap, size_t* n_tiles) {
+  GM_API_BEGIN
+  if (!p) throw std::invalid_argument("null argument: plans");
+  Runtime& rt = runtime_of(ctx);
+  std::vector<std::vector<int>> plans;
+  for (const Plan& plan : p->plans) plans.push_back(members_of(rt, plan));
+  Prepared& pr = rt.prepare_round(plans);
+  if (n_tiles) *n_tiles = static_cast<size_t>(pr.n_tiles);
+  const size_t words = static_cast<size_t>(pr.n_tiles) * 6;
+  if (!out || cap < words) throw RangeError("output buffer too small");
+  uint64_t* d_trace = nullptr;
+  cuda_check(cudaMalloc(&d_trace, words * sizeof(uint64_t)), "cudaMalloc(trace)");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(d_trace, 0, words * sizeof(uint64_t), s);
+  rt.launch(pr, s, true, nullptr, nullptr, d_trace);
+  cudaError_t e = cudaMemcpyAsync(out, d_trace, words * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(d_trace);
+  cuda_check(e, "trace copy");
+  GM_API_END
+}
+
+int gm_round_tiles(gm_ctx* ctx, const gm_plans* p, gm_tile* out, size_t cap, size_t* n) {
+  GM_API_BEGIN
+  if (!p) throw std::invalid_argument("null argument: plans");
+  Runtime& rt = runtime_of(ctx);
+  std::vector<std::vector<int>> plans;
+  for (const Plan& plan : p->plans) plans.push_back(members_of(rt, plan));
+  Prepared& pr = rt.prepare_round(plans);
+  std::vector<dev::TileEntry> table(pr.n_tiles);
+  cuda_check(cudaMemcpy(table.data(), pr.tiles, table.size() * sizeof(dev::TileEntry), cudaMemcpyDeviceToHost),
+             "read round tiles");
+  std::vector<gm_tile> v;
+  for (size_t i = 0; i < table.size(); ++i)  // flags = plan index of the tile
+    v.push_back(gm_tile{table[i].member, pr.tile_plan[i], table[i].m_tile, table[i].n_tile});
+  if (n) *n = v.size();
+  if (!out || cap < v.size()) throw RangeError("output buffer too small");
+  std::copy(v.begin(), v.end(), out);
+  GM_API_END
+}
+
+int gm_graph_capture_round(gm_ctx* ctx, const gm_plans* p, int timed, gm_graph** out) {
+  GM_API_BEGIN
+  if (!p || !out) throw std::invalid_argument("null argument");
+  Runtime& rt = runtime_of(ctx);
+  std::vector<std::vector<int>> plans;
+  for (const Plan& plan : p->plans) plans.push_back(members_of(rt, plan));
+  Prepared* pr = &rt.prepare_round(plans);
+  *out = capture(ctx, [&](cudaStream_t cs, gm_graph& g) {
+    auto ev = timing_pair(g, timed != 0);
+    g.kernels += rt.launch(*pr, cs, false, ev.first, ev.second);
+    g.superkernels += 1;
+    g.tiles += pr->n_tiles;
+  });
+  GM_API_END
+}
+
+int gm_graph_launch(gm_graph* g, uint64_t stream) {
+  GM_API_BEGIN
+  if (!g) throw std::invalid_argument("null graph");
+  Runtime& rt = runtime_of(g->ctx);
+  cuda_check(cudaGraphLaunch(g->exec, reinterpret_cast<cudaStream_t>(stream)), "cudaGraphLaunch");
+  rt.n_superkernels += g->superkernels;
+  rt.n_prepasses += g->kernels - g->superkernels;
+  rt.n_tiles += g->tiles;
+  GM_API_END
+}
+
+int gm_graph_launch_count(const gm_graph* g, int32_t* superkernels, int32_t* kernels) {
+  GM_API_BEGIN
+  if (!g) throw std::invalid_argument("null graph");
+  if (superkernels) *superkernels = g->superkernels;
+  if (kernels) *kernels = g->kernels;
+  GM_API_END
+}
+
+int gm_graph_kernel_times(gm_graph* g, float* ms, size_t cap, size_t* n) {
+  GM_API_BEGIN
+  if (!g) throw std::invalid_argument("null graph");
+  const size_t pairs = g->events.size() / 2;
+  if (n) *n = pairs;
+  if (pairs == 0) return GM_OK;
+  if (!ms || cap < pairs) throw RangeError("output buffer too small");
+  cuda_check(cudaEventSynchronize(g->events.back()), "cudaEventSynchronize");
+  for (size_t i = 0; i < pairs; ++i)
+    cuda_check(cudaEventElapsedTime(&ms[i], g->events[2 * i], g->events[2 * i + 1]), "cudaEventElapsedTime");
+  GM_API_END
+}
+
+void gm_graph_destroy(gm_graph* g) { delete g; }
 
 int gm_ctx_launch_stats(const gm_ctx* ctx, int64_t* superkernels, int64_t* prepasses, int64_t* tiles) {
   GM_API_BEGIN

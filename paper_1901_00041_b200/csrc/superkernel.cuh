@@ -6,18 +6,22 @@
 // the paper's batched-SGEMM super-kernel).  The CTA walks a
 // tile-dispatch table (member, m-tile, n-tile) built by the host planner.
 //
-// Per CTA (256 threads, 1 CTA per SM):
-//   warp 0   TMA producer: A tile (2-D tiled map, or 4-D im2col map for
-//            implicit-GEMM conv) + B tile (weights, K-major) into a
-//            kStages-deep ring of 128B-swizzled smem stages
-//   warp 1   MMA issuer: one elected thread issues tcgen05.mma
-//            (kind::f16, bf16 x bf16 -> fp32, M=128, N = member width)
-//            into a double-buffered TMEM accumulator
-//   warp 2   TMEM allocator (256 columns)
-//   warps 4-7 epilogue: tcgen05.ld 32x32b -> bf16 -> global (row per thread)
-// Pipelines: smem full/empty mbarriers (TMA <-> MMA, tcgen05.commit frees a
-// stage), TMEM full/empty mbarriers (MMA <-> epilogue), so the epilogue of
-// tile i overlaps the mainloop of tile i+1.
+// Per CTA (256 threads, 1 CTA per SM), templated on the N tile (128 | 256):
+//   warp 0    TMA producer: A tile (2-D tiled map, or 4-D im2col map for
+//             implicit-GEMM conv) + B tile (weights, K-major) into a ring of
+//             128B-swizzled smem stages; boxes are sized per member, so a
+//             small-M or small-N member moves only its real bytes
+//   warp 1    MMA issuer: one thread issues tcgen05.mma (kind::f16,
+//             bf16 x bf16 -> fp32, M=128, N = the member's box) into a
+//             double-buffered TMEM accumulator
+//   warp 2    TMEM allocator (2 x BN columns)
+//   warps 4-7 epilogue: tcgen05.ld 32x32b -> bf16 -> 64B-swizzled smem
+//             staging -> TMA bulk store (coalesced, clipped at M/N edges)
+// Pipelines: smem full/empty mbarriers (TMA <-> MMA; tcgen05.commit frees a
+// stage), TMEM full/empty mbarriers (MMA <-> epilogue), bulk-group waits on
+// the double-buffered store staging.  Launches chain with programmatic
+// dependent launch: the weights of the first stages stream before
+// griddepcontrol.wait, activations after it.
 #pragma once
 
 #include <cuda.h>
@@ -28,15 +32,22 @@ namespace gmb {
 namespace dev {
 
 constexpr int kBM = 128;  // UMMA M; == b200 DeviceSpec.tile_m
-constexpr int kBN = 128;  // max UMMA N per tile; == b200 DeviceSpec.tile_n
 constexpr int kBK = 64;   // 64 bf16 = 128 B = one SWIZZLE_128B row
-constexpr int kStages = 6;
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;  // 4 control warps + 2 epilogue warpgroups
 constexpr int kABytes = kBM * kBK * 2;
-constexpr int kBBytes = kBN * kBK * 2;
-constexpr int kAccCols = kBN;
-constexpr int kTmemCols = 2 * kAccCols;
-constexpr int kSmemBytes = kStages * (kABytes + kBBytes) + 1024 /*align slack*/ + 256 /*barriers*/;
+constexpr int kEpiChunk = 32;                         // columns per store box
+constexpr int kEpiBufBytes = 32 * kEpiChunk * 2;      // 32 rows x 32 cols bf16
+constexpr int kEpiBytes = 8 * 2 * kEpiBufBytes;       // 8 epilogue warps x double buffer
+
+template <int BN>
+struct Cfg {
+  static_assert(BN == 128 || BN == 256, "N tile must be 128 or 256");
+  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
 
 enum : int32_t { kATiled = 0, kAIm2col = 1 };
 
@@ -44,23 +55,58 @@ enum : int32_t { kATiled = 0, kAIm2col = 1 };
 struct alignas(128) MemberDesc {
   CUtensorMap a;        // A operand: [M, K] tiled, or NHWC im2col
   CUtensorMap b;        // B operand: weights [N, K], K-major
-  __nv_bfloat16* y;     // output [M, N] row-major
-  int64_t ldy;
+  CUtensorMap c;        // output [M, N] row-major, store box 32 x 32
   int32_t m, n;
   int32_t k_blocks;     // ceil(K / kBK)
-  uint32_t idesc;       // tcgen05 instruction descriptor (N of this member)
+  uint32_t idesc;       // tcgen05 instruction descriptor (N = B box rows)
+  uint32_t tx_bytes;    // A box + B box bytes per k-block
   int32_t a_mode;
   int32_t pq, q;        // im2col: output pixels per image, output width
   int32_t stride, pad;
   int32_t s_taps;       // filter width S
   int32_t c_blocks;     // Cin / kBK
   int32_t relu;
+  int32_t n_tile;       // output columns per tile (<= BN): narrower for few-tile members
 };
 
 // Device tile-table entry; `member` is the registered slot index.
+// In a round program (one persistent launch for a whole space-time round),
+// `done` names the completion counter of the tile's member instance and
+// `dep` the counter of the same tenant's previous layer (-1 = none): a tile's
+// activations are loaded only once every tile of its dependency is stored.
+//
+// Split-K (round programs, few-tile long-K members): `splits` > 1 tiles each
+// cover k-blocks [kb_begin, kb_end) of output tile `ws`; they reduce-add fp32
+// partials into a workspace tile with TMA, and the last split to arrive
+// converts the sum to bf16, stores it, clears the workspace and publishes.
 struct TileEntry {
-  uint16_t member, flags, m_tile, n_tile;
+  uint16_t member, splits, m_tile, n_tile;
+  int32_t done, dep;
+  uint16_t kb_begin, kb_end;  // kb_end == 0: the whole K
+  int32_t ws;                 // split workspace tile (-1 = not split)
 };
+
+// Round-program side state (all null for a plain super-kernel launch).
+struct RoundArgs {
+  uint32_t* counters;         // per member instance: tile-quarters stored
+  const uint32_t* targets;
+  const CUtensorMap* ws_map;  // fp32 [n_ws * 128, BN], 16 x 32 reduce boxes
+  float* ws;
+  uint32_t* split_ctr;        // per workspace tile and quarter: splits arrived
+  uint64_t* trace;            // 6 %globaltimer stamps per tile (profiling)
+};
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // ---------------------------------------------------------------- PTX helpers
 
@@ -114,6 +160,13 @@ __device__ __forceinline__ void tma_load_im2col(void* dst, const CUtensorMap* ma
       : "memory");
 }
 
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -161,7 +214,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi, int relu) {
+__device__ __forceinline__ uint32_t pack_bf16(uint32_t lo_bits, uint32_t hi_bits, int relu) {
+  float lo = __uint_as_float(lo_bits), hi = __uint_as_float(hi_bits);
   if (relu) {
     lo = fmaxf(lo, 0.f);
     hi = fmaxf(hi, 0.f);
@@ -172,13 +226,20 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi, int relu) {
 
 // ---------------------------------------------------------------- kernel
 
+template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
-    superkernel(const MemberDesc* __restrict__ slots, const TileEntry* __restrict__ tiles, int n_tiles) {
+    superkernel(const MemberDesc* __restrict__ slots, const TileEntry* __restrict__ tiles, int n_tiles,
+                const RoundArgs ra) {
+  using C = Cfg<BN>;
+  uint32_t* __restrict__ counters = ra.counters;
+  const uint32_t* __restrict__ targets = ra.targets;
+  uint64_t* __restrict__ trace = ra.trace;
+  constexpr int kStages = C::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + kStages * kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBBytes);
+  uint8_t* ring = smem;                                // kStages x (A | B)
+  uint8_t* epi = smem + kStages * C::kStageBytes;     // store staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi + kEpiBytes);
   uint64_t* empty = full + kStages;
   uint64_t* acc_full = empty + kStages;
   uint64_t* acc_empty = acc_full + 2;
@@ -200,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(kTmemCols)
+                 "r"(C::kTmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -208,17 +269,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Let the next launch in the stream (programmatic dependent launch) start
+  // its prologue on SMs this grid frees; it waits in griddepcontrol.wait.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
       uint32_t stage = 0, phase = 0;
+      bool first = true;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         const TileEntry te = tiles[t];
         const MemberDesc* md = slots + te.member;
-        const int k_blocks = md->k_blocks;
+        prefetch_tmap(&md->a);
+        prefetch_tmap(&md->b);
+        const int kb_lo = te.kb_end ? te.kb_begin : 0;
+        const int k_blocks = te.kb_end ? te.kb_end : md->k_blocks;
+        const uint32_t tx = md->tx_bytes;
         const int m0 = te.m_tile * kBM;
-        const int n0 = te.n_tile * kBN;
+        const int n0 = te.n_tile * md->n_tile;
         const bool im2col = md->a_mode == kAIm2col;
         int img = 0, h0 = 0, w0 = 0, c_blocks = 1, s_taps = 1;
         if (im2col) {
@@ -231,27 +300,73 @@ __global__ void __launch_bounds__(kThreads, 1)
           c_blocks = md->c_blocks;
           s_taps = md->s_taps;
         }
-        for (int kb = 0; kb < k_blocks; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], kABytes + kBBytes);
-          uint8_t* a_dst = sA + stage * kABytes;
+        auto load_a = [&](int kb, uint32_t st) {
+          uint8_t* a_dst = ring + st * C::kStageBytes;
           if (im2col) {
             const int tap = kb / c_blocks;
             const int c0 = (kb - tap * c_blocks) * kBK;
             const int r = tap / s_taps;
             const int s = tap - r * s_taps;
-            tma_load_im2col(a_dst, &md->a, &full[stage], c0, w0, h0, img, static_cast<uint16_t>(s),
+            tma_load_im2col(a_dst, &md->a, &full[st], c0, w0, h0, img, static_cast<uint16_t>(s),
                             static_cast<uint16_t>(r));
           } else {
-            tma_load_2d(a_dst, &md->a, &full[stage], kb * kBK, m0);
+            tma_load_2d(a_dst, &md->a, &full[st], kb * kBK, m0);
           }
-          tma_load_2d(sB + stage * kBBytes, &md->b, &full[stage], kb * kBK, n0);
+        };
+        auto load_b = [&](int kb, uint32_t st) {
+          tma_load_2d(ring + st * C::kStageBytes + kABytes, &md->b, &full[st], kb * kBK, n0);
+        };
+        // Activation gate: the prerequisite grid (PDL) before the first tile,
+        // and in a round program the tenant's previous layer (all its tiles
+        // stored).  Weights never wait on either.
+        auto gate = [&]() {
+          if (first) asm volatile("griddepcontrol.wait;" ::: "memory");
+          if (te.dep >= 0) {
+            while (ld_acquire(counters + te.dep) < targets[te.dep]) __nanosleep(32);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+          }
+        };
+        if (trace) trace[6 * t + 0] = globaltimer();
+        int kb = kb_lo;
+        if (first) {
+          // All stages are free: stream the first stages' B tiles, then gate.
+          const int pre = min(k_blocks - kb_lo, kStages);
+          for (int j = 0; j < pre; ++j) {
+            mbar_expect_tx(&full[j], tx);
+            load_b(kb_lo + j, j);
+          }
+          gate();
+          if (trace) trace[6 * t + 1] = globaltimer();
+          first = false;
+          for (int j = 0; j < pre; ++j) load_a(kb_lo + j, j);
+          kb = kb_lo + pre;
+          stage = pre % kStages;
+          phase = pre == kStages ? 1u : 0u;
+        } else if (te.dep >= 0) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], tx);
+          load_b(kb_lo, stage);
+          gate();
+          if (trace) trace[6 * t + 1] = globaltimer();
+          load_a(kb_lo, stage);
+          kb = kb_lo + 1;
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        for (; kb < k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], tx);
+          load_a(kb, stage);
+          load_b(kb, stage);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
       }
+      if (first) asm volatile("griddepcontrol.wait;" ::: "memory");
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -260,21 +375,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         const TileEntry te = tiles[t];
         const MemberDesc* md = slots + te.member;
-        const int k_blocks = md->k_blocks;
+        const int kb_lo = te.kb_end ? te.kb_begin : 0;
+        const int k_blocks = te.kb_end ? te.kb_end : md->k_blocks;
         const uint32_t idesc = md->idesc;
         mbar_wait(&acc_empty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * kAccCols;
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb_lo; kb < k_blocks; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + stage * kABytes);
-          const uint32_t b_addr = smem_u32(sB + stage * kBBytes);
+          if (trace && kb == kb_lo) trace[6 * t + 2] = globaltimer();
+          const uint32_t a_addr = smem_u32(ring + stage * C::kStageBytes);
+          const uint32_t b_addr = a_addr + kABytes;
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             // advance 16 bf16 (32 B) along K inside the 128 B swizzle atom
             umma_bf16(d_tmem, sw128_desc(a_addr + k * 32), sw128_desc(b_addr + k * 32), idesc,
-                      (kb | k) != 0 ? 1u : 0u);
+                      (kb != kb_lo || k != 0) ? 1u : 0u);
           }
           umma_commit(&empty[stage]);  // frees the smem stage once these MMAs retire
           if (++stage == kStages) {
@@ -283,82 +400,202 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         umma_commit(&acc_full[acc]);  // accumulator ready for the epilogue
+        if (trace) trace[6 * t + 3] = globaltimer();
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
     }
   } else if (warp >= 4) {
-    // -------------------------------------------------- epilogue (128 threads)
-    const int quarter = warp - 4;  // == warp % 4: the TMEM lane quarter this warp may access
-    uint32_t acc = 0, acc_phase = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    // -------------------------------------------------- epilogue: 2 warpgroups
+    // Warpgroup g drains accumulator buffer g, i.e. every other tile, so one
+    // group's store-completion wait (needed before publishing a round
+    // counter) overlaps the other group's TMEM drain.
+    const int quarter = warp & 3;  // the TMEM lane quarter this warp may access
+    const uint32_t acc = static_cast<uint32_t>((warp - 4) >> 2);
+    uint8_t* stage_buf = epi + (warp - 4) * 2 * kEpiBufBytes;
+    uint32_t acc_phase = 0, buf = 0;
+    int issued = 0, local = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++local) {
+      if ((local & 1) != static_cast<int>(acc)) continue;
       const TileEntry te = tiles[t];
       const MemberDesc* md = slots + te.member;
-      const int m0 = te.m_tile * kBM;
-      const int n0 = te.n_tile * kBN;
-      const int cols = min(kBN, md->n - n0);  // multiple of 8
-      const int row = m0 + quarter * 32 + lane;
-      const bool row_ok = row < md->m;
+      const int m0 = te.m_tile * kBM + quarter * 32;
+      const int n0 = te.n_tile * md->n_tile;
+      const int cols = min(md->n_tile, md->n - n0);
       const int relu = md->relu;
-      __nv_bfloat16* yrow = md->y + static_cast<int64_t>(row) * md->ldy + n0;
+      const int sw = (lane >> 1) & 3;  // SWIZZLE_64B: 16B chunk j of a 64 B row -> j ^ row[2:1]
+      // Claim the next staging buffer once the store issued from it two
+      // chunks ago has finished reading it.
+      auto claim = [&]() -> uint8_t* {
+        if (lane == 0 && issued >= 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        return stage_buf + buf * kEpiBufBytes;
+      };
+      auto issue = [&]() {
+        ++issued;
+        buf ^= 1;
+      };
+      // 32 fp32 accumulators of this lane's row -> bf16 -> one 32x32 store box.
+      auto store_bf16 = [&](const uint32_t (&v)[32], int c) {
+        uint8_t* sbuf = claim();
+        uint8_t* row = sbuf + lane * 64;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint4 pk;
+          pk.x = pack_bf16(v[8 * j + 0], v[8 * j + 1], relu);
+          pk.y = pack_bf16(v[8 * j + 2], v[8 * j + 3], relu);
+          pk.z = pack_bf16(v[8 * j + 4], v[8 * j + 5], relu);
+          pk.w = pack_bf16(v[8 * j + 6], v[8 * j + 7], relu);
+          *reinterpret_cast<uint4*>(row + ((j ^ sw) << 4)) = pk;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&md->c, sbuf, n0 + c, m0);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        issue();
+      };
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * kAccCols;
-      for (int c = 0; c < cols; c += 32) {
-        uint32_t v[32];
-        tmem_ld32(taddr + c, v);
-        if (row_ok) {
+      if (trace && quarter == 0 && lane == 0) trace[6 * t + 4] = globaltimer();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
+      bool publish = te.done >= 0;
+      if (te.splits > 1) {
+        // ---- split-K partial: reduce-add fp32 into the workspace tile
+        const int ws_row = te.ws * kBM + quarter * 32;
+        for (int c = 0; c < cols; c += kEpiChunk) {
+          uint32_t v[32];
+          tmem_ld32(taddr + c, v);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            if (c + 8 * j < cols) {
-              uint4 pk;
-              pk.x = pack_bf16(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]), relu);
-              pk.y = pack_bf16(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]), relu);
-              pk.z = pack_bf16(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]), relu);
-              pk.w = pack_bf16(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]), relu);
-              *reinterpret_cast<uint4*>(yrow + c + 8 * j) = pk;
+          for (int h = 0; h < 2; ++h) {
+            if (c + 16 * h < cols) {
+              uint8_t* sbuf = claim();
+              uint8_t* row = sbuf + lane * 64;
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                *reinterpret_cast<uint4*>(row + ((j ^ sw) << 4)) =
+                    make_uint4(v[16 * h + 4 * j], v[16 * h + 4 * j + 1], v[16 * h + 4 * j + 2], v[16 * h + 4 * j + 3]);
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              __syncwarp();
+              if (lane == 0) {
+                asm volatile(
+                    "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                        reinterpret_cast<uint64_t>(ra.ws_map)),
+                    "r"(smem_u32(sbuf)), "r"(c + 16 * h), "r"(ws_row)
+                    : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+              }
+              issue();
             }
           }
         }
+        tc_fence_before();
+        mbar_arrive(&acc_empty[acc]);  // TMEM is free; the rest works from the workspace
+        uint32_t prev = 0;
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          __threadfence();
+          prev = atomicAdd(ra.split_ctr + te.ws * 4 + quarter, 1u);
+        }
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        publish = publish && prev + 1 == te.splits;
+        if (prev + 1 == te.splits) {
+          // ---- last split: sum is complete; convert, store, clear the workspace
+          __threadfence();
+          float* wrow = ra.ws + static_cast<int64_t>(ws_row + lane) * BN;
+          for (int c = 0; c < cols; c += kEpiChunk) {
+            uint32_t v[32];
+            float4* src = reinterpret_cast<float4*>(wrow + c);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 f = __ldcg(src + j);
+              v[4 * j] = __float_as_uint(f.x);
+              v[4 * j + 1] = __float_as_uint(f.y);
+              v[4 * j + 2] = __float_as_uint(f.z);
+              v[4 * j + 3] = __float_as_uint(f.w);
+              __stcg(src + j, make_float4(0.f, 0.f, 0.f, 0.f));
+            }
+            if (m0 < md->m) store_bf16(v, c);
+          }
+          if (lane == 0) ra.split_ctr[te.ws * 4 + quarter] = 0;
+        }
+      } else {
+        if (m0 < md->m) {  // warp-uniform: this quarter holds at least one real row
+          for (int c = 0; c < cols; c += kEpiChunk) {
+            uint32_t v[32];
+            tmem_ld32(taddr + c, v);
+            store_bf16(v, c);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&acc_empty[acc]);
       }
-      tc_fence_before();
-      mbar_arrive(&acc_empty[acc]);
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      acc_phase ^= 1;
+      if (trace && quarter == 0 && lane == 0) trace[6 * t + 5] = globaltimer();
+      if (publish && lane == 0) {
+        // publish: this warp's stores of the tile are complete and visible
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __threadfence();
+        atomicAdd(counters + te.done, 1u);
+      }
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
 
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::kTmemCols)
+                 : "memory");
   }
 }
 
-// Explicit im2col pre-pass for convs whose Cin does not fill a 128 B TMA
-// channel box (e.g. the 3-channel stem): writes [M, ldk] bf16 rows with
-// k = (r*S + s)*Cin + c and zero padding, consumed as a plain GEMM A operand.
+// One thread per (row m, 8-element chunk of k): 32-bit index math, one
+// coalesced 16-byte store per thread; ldk % 8 == 0.  Explicit im2col for
+// convs whose Cin does not fill a 128 B TMA channel box (the 3-channel stem).
 __global__ void im2col_prepass(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ out, int batch, int H,
                                int W, int Cin, int R, int S, int stride, int pad, int P, int Q, int ldk) {
-  const int64_t total = static_cast<int64_t>(batch) * P * Q * ldk;
+  const int chunks = ldk >> 3;
+  const int rows = batch * P * Q;
   const int K = R * S * Cin;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t m = i / ldk;
-    const int k = static_cast<int>(i - m * ldk);
-    __nv_bfloat16 v = __float2bfloat16(0.f);
-    if (k < K) {
-      const int c = k % Cin;
-      const int tap = k / Cin;
-      const int s = tap % S, r = tap / S;
-      const int q = static_cast<int>(m % Q);
-      const int p = static_cast<int>((m / Q) % P);
-      const int b = static_cast<int>(m / (static_cast<int64_t>(P) * Q));
-      const int ih = p * stride - pad + r, iw = q * stride - pad + s;
-      if (ih >= 0 && ih < H && iw >= 0 && iw < W) v = x[((static_cast<int64_t>(b) * H + ih) * W + iw) * Cin + c];
+  const unsigned short* xs = reinterpret_cast<const unsigned short*>(x);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows * chunks; i += gridDim.x * blockDim.x) {
+    const int m = i / chunks;
+    const int k0 = (i - m * chunks) << 3;
+    const int q = m % Q;
+    const int t = m / Q;
+    const int p = t % P;
+    const int b = t / P;
+    const int h0 = p * stride - pad, w0 = q * stride - pad;
+    int c = k0 % Cin;
+    int tap = k0 / Cin;
+    int s = tap % S, r = tap / S;
+    uint32_t packed[4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      unsigned short v = 0;
+      if (k0 + j < K) {
+        const int ih = h0 + r, iw = w0 + s;
+        if (ih >= 0 && ih < H && iw >= 0 && iw < W) v = __ldg(xs + ((b * H + ih) * W + iw) * Cin + c);
+      }
+      if (j & 1)
+        packed[j >> 1] |= static_cast<uint32_t>(v) << 16;
+      else
+        packed[j >> 1] = v;
+      if (++c == Cin) {
+        c = 0;
+        if (++s == S) {
+          s = 0;
+          ++r;
+        }
+      }
     }
-    out[i] = v;
+    *reinterpret_cast<uint4*>(out + static_cast<int64_t>(m) * ldk + k0) =
+        make_uint4(packed[0], packed[1], packed[2], packed[3]);
   }
 }
 

@@ -1,0 +1,201 @@
+"""Space-time serving engine on one GPU: tenants, rounds, launch programs.
+
+A *round* is the hot path of BASELINE.json's north star on one GPU: every
+registered tenant submits one query batch; the space-time scheduler
+(gm_plan_round: dynamic batcher + packing planner) turns the layer requests
+into super-kernels; each super-kernel executes the members' conv/GEMM tiles
+in one sm_100a launch.  The same kernel code also runs the two baseline
+modes the paper compares against (time-only: serial per-tenant launches;
+space-only: one stream per tenant), so ratios isolate packing.
+
+Steady-state rounds are captured as CUDA graphs keyed by the plan's
+signature sequence (the B200 form of "cache super-kernels as workloads
+stabilize"); ``serve_round`` re-plans every round on the host
+and replays the cached graph while the sequence is unchanged.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import torch
+
+from . import _native as N
+from ._native import check, lib
+from .runtime import Context, LayerBuffers, Round
+from .scheduler import BatchPolicy
+from .workload import Layer
+
+_MASK = (1 << 64) - 1
+
+
+def mix64(*parts: int) -> int:
+    """splitmix64 chained over the parts (hash, never XOR)."""
+    h = 0x9E3779B97F4A7C15
+    for p in parts:
+        h = (h + (int(p) & _MASK) + 0x9E3779B97F4A7C15) & _MASK
+        z = h
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _MASK
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _MASK
+        h = z ^ (z >> 31)
+    return h & ((1 << 63) - 1)
+
+
+KIND_INPUT, KIND_WEIGHT = 1, 2
+
+
+class Graph:
+    """A captured launch program (gm_graph)."""
+
+    def __init__(self, handle: int, timed: bool):
+        self.handle = handle
+        self.timed = timed
+        sk, k = C.c_int32(), C.c_int32()
+        check(lib().gm_graph_launch_count(handle, C.byref(sk), C.byref(k)))
+        self.superkernels, self.kernels = int(sk.value), int(k.value)
+
+    def launch(self, stream: int) -> None:
+        check(lib().gm_graph_launch(self.handle, int(stream)))
+
+    def kernel_times_ms(self) -> List[float]:
+        n = C.c_size_t()
+        arr = (C.c_float * max(1, self.superkernels))()
+        check(lib().gm_graph_kernel_times(self.handle, arr, self.superkernels, C.byref(n)))
+        return [float(arr[i]) for i in range(n.value)]
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            lib().gm_graph_destroy(self.handle)
+            self.handle = None
+
+
+class TenantModel:
+    """Device buffers of one tenant's operator graph with synthetic data.
+
+    Inputs U(-1, 1), weights Kaiming-normal (std sqrt(2 / fan_in)); each tensor
+    from its own generator seeded by mix64(seed, tenant, layer, kind).  Weight
+    rows are padded to a multiple of 8 elements (16-byte TMA strides).
+    """
+
+    def __init__(self, layers: Sequence[Layer], batch: int, seed: int, tenant: int, device: torch.device):
+        self.layers = list(layers)
+        self.batch = batch
+        self.buffers: List[LayerBuffers] = []
+        for li, L in enumerate(self.layers):
+            if L.kind == "dwconv":
+                raise NotImplementedError(f"{L.name}: depthwise conv has no tensor-core tile type yet")
+            s = L.gemm_shape(batch)
+            g_in = torch.Generator(device=device).manual_seed(mix64(seed, tenant, li, KIND_INPUT))
+            g_w = torch.Generator(device=device).manual_seed(mix64(seed, tenant, li, KIND_WEIGHT))
+            kpad = (s.k + 7) // 8 * 8
+            w = torch.zeros(s.n, kpad, device=device, dtype=torch.bfloat16)
+            w[:, : s.k] = (torch.randn(s.n, s.k, device=device, generator=g_w) * (2.0 / s.k) ** 0.5).to(torch.bfloat16)
+            if L.kind == "conv":
+                c = L.conv
+                x = (torch.rand(batch, c.image_h, c.image_w, c.in_channels, device=device, generator=g_in) * 2 - 1)
+                x = x.to(torch.bfloat16)
+                y = torch.empty(s.m, s.n, device=device, dtype=torch.bfloat16)
+                self.buffers.append(LayerBuffers("conv", x, w, y, conv=c, batch=batch))
+            else:
+                xfull = torch.zeros(s.m, kpad, device=device, dtype=torch.bfloat16)
+                xfull[:, : s.k] = (torch.rand(s.m, s.k, device=device, generator=g_in) * 2 - 1).to(torch.bfloat16)
+                y = torch.empty(s.m, s.n, device=device, dtype=torch.bfloat16)
+                self.buffers.append(LayerBuffers("gemm", xfull, w, y, gemm=s))
+
+    @property
+    def query_input(self) -> torch.Tensor:
+        return self.buffers[0].x
+
+    @property
+    def query_output(self) -> torch.Tensor:
+        return self.buffers[-1].y
+
+    def flops(self) -> int:
+        return sum(L.flops(self.batch) for L in self.layers)
+
+    def compulsory_bytes(self) -> int:
+        return sum(L.compulsory_bytes(self.batch) for L in self.layers)
+
+
+class SpaceTimeEngine:
+    """Tenants on one GPU + the three execution modes over the same kernel."""
+
+    def __init__(self, tenant_layers: Sequence[Sequence[Layer]], batches: Sequence[int], device_index: int = 0,
+                 seed: int = 42, slo_latency: float = 0.040, policy: Optional[BatchPolicy] = None,
+                 tenant_offset: int = 0, options: Optional[Dict[str, int]] = None):
+        self.device = torch.device("cuda", device_index)
+        torch.cuda.set_device(self.device)
+        self.ctx = Context(device_index, policy=policy or BatchPolicy(target_batch=0))
+        for name, value in (options or {}).items():
+            self.ctx.set_option(name, value)
+        self.models: List[TenantModel] = []
+        self.tenants: List[int] = []
+        for i, (layers, b) in enumerate(zip(tenant_layers, batches)):
+            m = TenantModel(layers, b, seed, tenant_offset + i, self.device)
+            self.models.append(m)
+            self.tenants.append(self.ctx.register_tenant(m.buffers, slo_latency=slo_latency,
+                                                         tenant_id=f"t{tenant_offset + i}"))
+        self._now = 0
+        self._graphs: Dict[Tuple[str, ...], Graph] = {}
+
+    # ------------------------------------------------------------ planning
+    def flops_per_round(self) -> int:
+        return sum(m.flops() for m in self.models)
+
+    def compulsory_bytes_per_round(self) -> int:
+        return sum(m.compulsory_bytes() for m in self.models)
+
+    def plan_round(self, policy: Optional[BatchPolicy] = None) -> Round:
+        """One space-time round on the virtual clock (advances it).
+
+        ``policy`` replaces the context's BatchPolicy from this round on
+        (e.g. ``max_waves=1`` for reference plan parity)."""
+        if policy is not None:
+            self.ctx.set_policy(policy)
+        r = self.ctx.plan_round(self.tenants, self._now)
+        if r.times:
+            self._now = max(e for _, e in r.times)
+        return r
+
+    # ------------------------------------------------------------ launch programs
+    def capture_packed(self, rnd: Round, timed: bool = False) -> Graph:
+        h = C.c_void_p()
+        check(lib().gm_graph_capture_plans(self.ctx.handle, rnd.handle, int(timed), C.byref(h)))
+        return Graph(h.value, timed)
+
+    def capture_round(self, rnd: Round, timed: bool = False) -> Graph:
+        """The round program: every plan of the round in one persistent launch."""
+        h = C.c_void_p()
+        check(lib().gm_graph_capture_round(self.ctx.handle, rnd.handle, int(timed), C.byref(h)))
+        return Graph(h.value, timed)
+
+    def capture_serial(self, mode: str, timed: bool = False) -> Graph:
+        m = {"time_only": N.GM_MODE_TIME_ONLY, "space_only": N.GM_MODE_SPACE_ONLY}[mode]
+        arr = (C.c_int32 * len(self.tenants))(*self.tenants)
+        h = C.c_void_p()
+        check(lib().gm_graph_capture_serial(self.ctx.handle, arr, len(self.tenants), m, int(timed), C.byref(h)))
+        return Graph(h.value, timed)
+
+    # ------------------------------------------------------------ public serving call
+    def serve_round(self, host_inputs: Sequence[torch.Tensor], host_outputs: Sequence[torch.Tensor],
+                    stream: torch.cuda.Stream) -> Round:
+        """End-to-end round through the public API with host buffers.
+
+        Copies each tenant's query batch host->device, plans the round with the
+        space-time scheduler, replays (or captures, on a new signature
+        sequence) the packed launch program, and copies each tenant's result
+        device->host.  Returns after the results are on the host.
+        """
+        with torch.cuda.stream(stream):
+            for m, h in zip(self.models, host_inputs):
+                m.query_input.copy_(h, non_blocking=True)
+            rnd = self.plan_round()
+            key = tuple(rnd.signatures)
+            g = self._graphs.get(key)
+            if g is None:
+                g = self._graphs[key] = self.capture_round(rnd)
+            g.launch(stream.cuda_stream)
+            for m, h in zip(self.models, host_outputs):
+                h.copy_(m.query_output, non_blocking=True)
+        stream.synchronize()
+        return rnd

@@ -63,6 +63,14 @@ class Context:
     def __del__(self):
         self.close()
 
+    def set_option(self, name: str, value: int) -> None:
+        """Runtime execution option (see gm_ctx_set_option in the header)."""
+        check(lib().gm_ctx_set_option(self.handle, name.encode(), int(value)))
+
+    def set_policy(self, policy: BatchPolicy) -> None:
+        check(lib().gm_ctx_set_policy(self.handle, C.byref(policy._c())))
+        self.policy = policy
+
     # ------------------------------------------------------------ tenants
     def register_tenant(self, layers: Sequence[LayerBuffers], slo_latency: float = 0.1, concurrency: int = 1,
                         tenant_id: str = "") -> int:
@@ -152,6 +160,13 @@ class Round:
         check(lib().gm_prepare_plans(self.ctx.handle, self.handle))
 
     def launch(self, stream: int = 0) -> int:
+        """One launch per formed super-kernel (the reference's dispatch unit)."""
         out = C.c_int32()
         check(lib().gm_dispatch_plans(self.ctx.handle, self.handle, int(stream), C.byref(out)))
+        return int(out.value)
+
+    def launch_round(self, stream: int = 0) -> int:
+        """The whole round as one persistent launch (round program)."""
+        out = C.c_int32()
+        check(lib().gm_dispatch_round(self.ctx.handle, self.handle, int(stream), C.byref(out)))
         return int(out.value)

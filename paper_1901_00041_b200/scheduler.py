@@ -204,10 +204,11 @@ class BatchPolicy:
     allow_variable_size: bool = False
     slo_safety_margin: float = 0.0
     variable_inefficiency: float = 1.10
+    max_waves: int = 1  # B200 extension; 1 = the reference's one-wave cap (plan parity)
 
     def _c(self) -> N.gm_batch_policy:
-        return N.gm_batch_policy(self.max_wait, self.target_batch, int(bool(self.allow_variable_size)), 0,
-                                 self.slo_safety_margin, self.variable_inefficiency)
+        return N.gm_batch_policy(self.max_wait, self.target_batch, int(bool(self.allow_variable_size)),
+                                 int(self.max_waves), self.slo_safety_margin, self.variable_inefficiency)
 
 
 @dataclass

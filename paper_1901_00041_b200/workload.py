@@ -1,0 +1,228 @@
+"""Tenant workloads: the reference presets and real-layer model graphs.
+
+* ``reference_presets()`` restates the reference's shipped presets
+  (proj/src/workload.cpp:15-95): ``rnn-matvec``, ``resnet18-conv2_2``,
+  ``square-256`` and the stylised ``resnet50`` / ``mobilenetv2`` GEMM lists.
+  They are plan-parity inputs (GemmShape lists), not executable graphs.
+* The model builders return executable operator lists with real
+  ConvSpecs (torchvision layer definitions), which the reference lacks
+  (SURVEY §8(d)): ResNet-18/50, VGG-16, MobileNet-v2 (depthwise layers are
+  tagged ``dwconv`` and are not yet executable on this path), BERT-base
+  projection/FFN GEMMs.  Convs are listed in forward order; a bottleneck's
+  downsample follows its conv3, a basic block's follows its conv2.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Optional
+
+from .scheduler import ConvSpec, GemmShape, batch_inputs, im2col_gemm_dims
+
+
+@dataclass(frozen=True)
+class WorkloadPreset:
+    """workload.hpp:24-29."""
+    name: str
+    layers: tuple
+    weights_bytes: float
+    slo_latency: float
+
+
+def reference_presets() -> List[WorkloadPreset]:
+    """The reference's preset table (workload.cpp:15-95), restated."""
+    out = [
+        WorkloadPreset("rnn-matvec", (GemmShape(512, 1, 512),), 512.0 * 512 * 4, 0.05),
+        WorkloadPreset("resnet18-conv2_2", (GemmShape(256, 128, 1152),), 1152.0 * 128 * 4, 0.05),
+        WorkloadPreset("square-256", (GemmShape(256, 256, 256),), 256.0 * 256 * 4, 0.05),
+    ]
+    l = [GemmShape(1024, 64, 147)]
+    for _ in range(3):
+        l += [GemmShape(256, 64, 64), GemmShape(256, 64, 576), GemmShape(256, 256, 64)]
+    l.append(GemmShape(256, 256, 64))
+    for _ in range(4):
+        l += [GemmShape(64, 128, 256), GemmShape(64, 128, 1152), GemmShape(64, 512, 128)]
+    l.append(GemmShape(64, 512, 256))
+    for _ in range(6):
+        l += [GemmShape(16, 256, 512), GemmShape(16, 256, 2304), GemmShape(16, 1024, 256)]
+    l.append(GemmShape(16, 1024, 512))
+    for _ in range(3):
+        l += [GemmShape(4, 512, 1024), GemmShape(4, 512, 4608), GemmShape(4, 2048, 512)]
+    l += [GemmShape(4, 2048, 1024), GemmShape(1, 1000, 2048)]
+    out.append(WorkloadPreset("resnet50", tuple(l), 102.4e6, 0.040))
+    m = [GemmShape(1024, 32, 27), GemmShape(256, 96, 16), GemmShape(256, 96, 9), GemmShape(256, 24, 96)]
+    for _ in range(2):
+        m += [GemmShape(64, 144, 24), GemmShape(64, 144, 9), GemmShape(64, 32, 144)]
+    for _ in range(3):
+        m += [GemmShape(16, 192, 32), GemmShape(16, 192, 9), GemmShape(16, 64, 192)]
+    for _ in range(2):
+        m += [GemmShape(4, 384, 64), GemmShape(4, 384, 9), GemmShape(4, 96, 384)]
+    for _ in range(2):
+        m += [GemmShape(4, 576, 96), GemmShape(4, 576, 9), GemmShape(4, 160, 576)]
+    m += [GemmShape(4, 960, 160), GemmShape(4, 960, 9), GemmShape(4, 320, 960), GemmShape(4, 1280, 320),
+          GemmShape(1, 1000, 1280)]
+    out.append(WorkloadPreset("mobilenetv2", tuple(m), 13.6e6, 0.020))
+    return out
+
+
+def find_preset(name: str) -> Optional[WorkloadPreset]:
+    for p in reference_presets():
+        if p.name == name:
+            return p
+    return None
+
+
+# ---------------------------------------------------------------- real graphs
+
+@dataclass(frozen=True)
+class Layer:
+    """One operator of a tenant graph.
+
+    conv/dwconv: ``conv`` holds the ConvSpec (per image).
+    gemm: ``rows`` rows per query (1 for a classifier, seq_len for BERT),
+          ``n`` outputs, ``k`` inner dimension.
+    """
+    name: str
+    kind: str
+    conv: Optional[ConvSpec] = None
+    rows: int = 0
+    n: int = 0
+    k: int = 0
+
+    def gemm_shape(self, batch: int = 1) -> GemmShape:
+        if self.kind in ("conv", "dwconv"):
+            return batch_inputs(im2col_gemm_dims(self.conv), batch)
+        return GemmShape(self.rows * batch, self.n, self.k)
+
+    def flops(self, batch: int = 1) -> int:
+        if self.kind == "dwconv":  # per-channel filter: K = R*S, not R*S*Cin
+            s = self.gemm_shape(batch)
+            return 2 * s.m * s.n * self.conv.kernel_h * self.conv.kernel_w
+        s = self.gemm_shape(batch)
+        return 2 * s.m * s.n * s.k
+
+    def compulsory_bytes(self, batch: int = 1, elem: int = 2) -> int:
+        """Implicit-GEMM bf16 traffic: input + weights + output."""
+        if self.kind in ("conv", "dwconv"):
+            c = self.conv
+            s = self.gemm_shape(batch)
+            w = c.out_channels * c.kernel_h * c.kernel_w * (1 if self.kind == "dwconv" else c.in_channels)
+            return elem * (batch * c.image_h * c.image_w * c.in_channels + w + s.m * s.n)
+        s = self.gemm_shape(batch)
+        return elem * (s.m * s.k + s.n * s.k + s.m * s.n)
+
+
+def _conv(name, hw, cin, cout, r, stride, pad):
+    return Layer(name, "conv", ConvSpec(hw, hw, r, r, cin, cout, stride, pad))
+
+
+def resnet50(image: int = 224, classifier: bool = True) -> List[Layer]:
+    """torchvision resnet50 (v1.5: stride on the 3x3), 53 convs + fc."""
+    L = [_conv("conv1", image, 3, 64, 7, 2, 3)]
+    hw = (image + 6 - 7) // 2 + 1
+    hw = (hw + 2 - 3) // 2 + 1  # maxpool 3x3 s2 p1
+    cin = 64
+    for stage, (width, blocks, stride) in enumerate([(64, 3, 1), (128, 4, 2), (256, 6, 2), (512, 3, 2)], start=1):
+        out = width * 4
+        for b in range(blocks):
+            s = stride if b == 0 else 1
+            p = f"layer{stage}.{b}"
+            L.append(_conv(p + ".conv1", hw, cin, width, 1, 1, 0))
+            L.append(_conv(p + ".conv2", hw, width, width, 3, s, 1))
+            ohw = (hw + 2 - 3) // s + 1
+            L.append(_conv(p + ".conv3", ohw, width, out, 1, 1, 0))
+            if b == 0:
+                L.append(_conv(p + ".downsample", hw, cin, out, 1, s, 0))
+            hw, cin = ohw, out
+    if classifier:
+        L.append(Layer("fc", "gemm", rows=1, n=1000, k=2048))
+    return L
+
+
+def resnet18(image: int = 224, classifier: bool = True) -> List[Layer]:
+    """torchvision resnet18; at image=128 layer2.* is the paper's conv2_2 (256,128,1152)."""
+    L = [_conv("conv1", image, 3, 64, 7, 2, 3)]
+    hw = (image + 6 - 7) // 2 + 1
+    hw = (hw + 2 - 3) // 2 + 1
+    cin = 64
+    for stage, (width, stride) in enumerate([(64, 1), (128, 2), (256, 2), (512, 2)], start=1):
+        for b in range(2):
+            s = stride if b == 0 else 1
+            p = f"layer{stage}.{b}"
+            L.append(_conv(p + ".conv1", hw, cin, width, 3, s, 1))
+            ohw = (hw + 2 - 3) // s + 1
+            L.append(_conv(p + ".conv2", ohw, width, width, 3, 1, 1))
+            if b == 0 and (s != 1 or cin != width):
+                L.append(_conv(p + ".downsample", hw, cin, width, 1, s, 0))
+            hw, cin = ohw, width
+    if classifier:
+        L.append(Layer("fc", "gemm", rows=1, n=1000, k=512))
+    return L
+
+
+def vgg16(image: int = 224, classifier: bool = True) -> List[Layer]:
+    """torchvision vgg16 (13 convs 3x3 p1 + 3 fc)."""
+    cfg = [64, 64, "M", 128, 128, "M", 256, 256, 256, "M", 512, 512, 512, "M", 512, 512, 512, "M"]
+    L, hw, cin, i = [], image, 3, 0
+    for v in cfg:
+        if v == "M":
+            hw //= 2
+            continue
+        L.append(_conv(f"features.{i}", hw, cin, v, 3, 1, 1))
+        cin, i = v, i + 1
+    if classifier:
+        L += [Layer("classifier.0", "gemm", rows=1, n=4096, k=512 * 7 * 7),
+              Layer("classifier.3", "gemm", rows=1, n=4096, k=4096),
+              Layer("classifier.6", "gemm", rows=1, n=1000, k=4096)]
+    return L
+
+
+def mobilenet_v2(image: int = 224, classifier: bool = True) -> List[Layer]:
+    """torchvision mobilenet_v2 (width 1.0); depthwise 3x3 convs are ``dwconv``."""
+    L = [_conv("features.0", image, 3, 32, 3, 2, 1)]
+    hw = (image + 2 - 3) // 2 + 1
+    cin = 32
+    settings = [(1, 16, 1, 1), (6, 24, 2, 2), (6, 32, 3, 2), (6, 64, 4, 2), (6, 96, 3, 1), (6, 160, 3, 2),
+                (6, 320, 1, 1)]
+    idx = 1
+    for t, c, n, s in settings:
+        for b in range(n):
+            stride = s if b == 0 else 1
+            hidden = cin * t
+            p = f"features.{idx}"
+            if t != 1:
+                L.append(_conv(p + ".expand", hw, cin, hidden, 1, 1, 0))
+            L.append(Layer(p + ".dw", "dwconv", ConvSpec(hw, hw, 3, 3, hidden, hidden, stride, 1)))
+            hw = (hw + 2 - 3) // stride + 1
+            L.append(_conv(p + ".project", hw, hidden, c, 1, 1, 0))
+            cin, idx = c, idx + 1
+    L.append(_conv("features.18", hw, cin, 1280, 1, 1, 0))
+    if classifier:
+        L.append(Layer("classifier.1", "gemm", rows=1, n=1000, k=1280))
+    return L
+
+
+def bert_base_gemms(seq_len: int = 128, layers: int = 1) -> List[Layer]:
+    """BERT-base projection/FFN GEMMs per encoder layer (hidden 768, FFN 3072)."""
+    out = []
+    for i in range(layers):
+        p = f"encoder.{i}"
+        out += [Layer(p + ".qkv", "gemm", rows=seq_len, n=2304, k=768),
+                Layer(p + ".attn_out", "gemm", rows=seq_len, n=768, k=768),
+                Layer(p + ".ffn1", "gemm", rows=seq_len, n=3072, k=768),
+                Layer(p + ".ffn2", "gemm", rows=seq_len, n=768, k=3072)]
+    return out
+
+
+def conv2_2() -> List[Layer]:
+    """The paper's microbenchmark layer: ResNet-18 conv2_2 at 16x16."""
+    return [_conv("conv2_2", 16, 128, 128, 3, 1, 1)]
+
+
+MODELS = {
+    "resnet50": resnet50,
+    "resnet18": resnet18,
+    "vgg16": vgg16,
+    "mobilenet_v2": mobilenet_v2,
+    "bert_base": bert_base_gemms,
+    "conv2_2": conv2_2,
+}

@@ -1,0 +1,22 @@
+import os
+import sys
+
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+for p in (HERE, ROOT):
+    if p not in sys.path:
+        sys.path.insert(0, p)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) GPU")
+
+
+@pytest.fixture(scope="session")
+def ref():
+    import refshim
+    if not refshim.have_ref():
+        pytest.skip("oracle/_ref not built (make -C oracle ref)")
+    return refshim.ref_call

@@ -1,0 +1,240 @@
+"""Super-kernel parity on the GPU: every output of the sm_100a path (through
+the C-ABI) against oracle/conv_oracle.c on the same bf16-rounded inputs.
+
+Tolerance (BASELINE north star): ||y - y_ref||_inf / ||y_ref||_inf <= 1e-2
+per operator output, bf16 in / fp32 accumulate / bf16 out.
+"""
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+from refshim import ROOT
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-2
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def oracle():
+    lib = ctypes.CDLL(os.path.join(ROOT, "oracle", "_build", "liboracle.so"))
+    f = ctypes.POINTER(ctypes.c_float)
+    i = ctypes.c_int64
+    lib.oracle_conv2d_nhwc.argtypes = [f, f, f] + [i] * 10 + [ctypes.c_int32]
+    lib.oracle_gemm_nt.argtypes = [f, f, f, i, i, i, i, i, ctypes.c_int32]
+    return lib
+
+
+def fp(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+
+
+def expect(oracle, L, relu=False):
+    """fp32 oracle output of one LayerBuffers (reads the device tensors' bf16 values)."""
+    x = np.ascontiguousarray(L.x.float().cpu().numpy())
+    w = np.ascontiguousarray(L.w.float().cpu().numpy())
+    if L.kind == "conv":
+        c = L.conv
+        P = (c.image_h + 2 * c.padding - c.kernel_h) // c.stride + 1
+        Q = (c.image_w + 2 * c.padding - c.kernel_w) // c.stride + 1
+        y = np.zeros((L.batch * P * Q, c.out_channels), np.float32)
+        oracle.oracle_conv2d_nhwc(fp(x), fp(w), fp(y), L.batch, c.image_h, c.image_w, c.in_channels,
+                                  c.out_channels, c.kernel_h, c.kernel_w, c.stride, c.padding, w.shape[1], int(relu))
+    else:
+        g = L.gemm
+        y = np.zeros((g.m, g.n), np.float32)
+        oracle.oracle_gemm_nt(fp(x), fp(w), fp(y), g.m, g.n, g.k, x.shape[1], w.shape[1], int(relu))
+    return y
+
+
+def rel_err(L, ref):
+    got = L.y.float().cpu().numpy().reshape(ref.shape)
+    assert np.isfinite(got).all()
+    return float(np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30))
+
+
+def conv_layer(b, hw, cin, cout, r, stride, pad, relu=False, seed=0):
+    from paper_1901_00041_b200.runtime import LayerBuffers
+    from paper_1901_00041_b200.scheduler import ConvSpec
+    g = torch.Generator().manual_seed(seed)
+    K = r * r * cin
+    ldw = (K + 7) // 8 * 8
+    x = (torch.rand(b, hw, hw, cin, generator=g) * 2 - 1).to(torch.bfloat16).cuda()
+    w = torch.zeros(cout, ldw, dtype=torch.bfloat16)
+    w[:, :K] = (torch.randn(cout, K, generator=g) * (2.0 / K) ** 0.5).to(torch.bfloat16)
+    P = (hw + 2 * pad - r) // stride + 1
+    y = torch.full((b * P * P, cout), float("nan"), dtype=torch.bfloat16, device="cuda")
+    return LayerBuffers("conv", x, w.cuda(), y, conv=ConvSpec(hw, hw, r, r, cin, cout, stride, pad), batch=b, relu=relu)
+
+
+def gemm_layer(m, n, k, relu=False, seed=0):
+    from paper_1901_00041_b200.runtime import LayerBuffers
+    from paper_1901_00041_b200.scheduler import GemmShape
+    g = torch.Generator().manual_seed(seed)
+    ld = (k + 7) // 8 * 8
+    x = torch.zeros(m, ld, dtype=torch.bfloat16)
+    x[:, :k] = (torch.rand(m, k, generator=g) * 2 - 1).to(torch.bfloat16)
+    w = torch.zeros(n, ld, dtype=torch.bfloat16)
+    w[:, :k] = (torch.randn(n, k, generator=g) / k ** 0.5).to(torch.bfloat16)
+    y = torch.full((m, n), float("nan"), dtype=torch.bfloat16, device="cuda")
+    return LayerBuffers("gemm", x.cuda(), w.cuda(), y, gemm=GemmShape(m, n, k), relu=relu)
+
+
+CASES = {
+    "gemm conv2_2 256x128x1152": lambda: gemm_layer(256, 128, 1152),
+    "gemm tails 200x72x100": lambda: gemm_layer(200, 72, 100),
+    "gemm 1000x1000x520": lambda: gemm_layer(1000, 1000, 520),
+    "gemm M=1 (fc b1)": lambda: gemm_layer(1, 1000, 2048),
+    "gemm bert qkv 128x2304x768": lambda: gemm_layer(128, 2304, 768),
+    "gemm relu": lambda: gemm_layer(130, 136, 200, relu=True),
+    "conv 3x3 s1 p1 16x16x128->128 b2 (im2col TMA)": lambda: conv_layer(2, 16, 128, 128, 3, 1, 1),
+    "conv 3x3 s2 p1 28x28x64->128": lambda: conv_layer(1, 28, 64, 128, 3, 2, 1),
+    "conv 1x1 s1 14x14x256->512 b3 (tiled GEMM)": lambda: conv_layer(3, 14, 256, 512, 1, 1, 0),
+    "conv 1x1 s2 28x28x256->512 (im2col stride)": lambda: conv_layer(1, 28, 256, 512, 1, 2, 0),
+    "conv 7x7 s2 p3 stem 64x64x3->64 b2 (pre-pass)": lambda: conv_layer(2, 64, 3, 64, 7, 2, 3),
+    "conv 3x3 s1 7x7x512->512 b1 (M=49)": lambda: conv_layer(1, 7, 512, 512, 3, 1, 1),
+    "conv 5x5 s1 p2 12x12x64->96": lambda: conv_layer(2, 12, 64, 96, 5, 1, 2),
+    "conv 3x3 Cin=32 (pre-pass) 10x10x32->64": lambda: conv_layer(1, 10, 32, 64, 3, 1, 1),
+    "conv 3x3 relu": lambda: conv_layer(1, 12, 64, 64, 3, 1, 1, relu=True),
+}
+
+
+@pytest.fixture(scope="module")
+def registered():
+    from paper_1901_00041_b200.runtime import Context
+    ctx = Context(0)
+    names = list(CASES)
+    layers = [CASES[n]() for n in names]
+    tenant = ctx.register_tenant(layers)
+    return ctx, tenant, names, layers
+
+
+@pytest.mark.parametrize("idx", range(len(CASES)))
+def test_single_member_matches_oracle(registered, oracle, idx):
+    ctx, tenant, names, layers = registered
+    L = layers[idx]
+    L.y.fill_(float("nan"))
+    assert ctx.launch_members([(tenant, idx)]) >= 1
+    torch.cuda.synchronize()
+    err = rel_err(L, expect(oracle, L, L.relu))
+    assert err <= TOL, f"{names[idx]}: {err:.3e}"
+
+
+def test_heterogeneous_members_in_one_launch(registered, oracle):
+    """Every case above as members of ONE super-kernel (variable-size packing)."""
+    ctx, tenant, names, layers = registered
+    for L in layers:
+        L.y.fill_(float("nan"))
+    ctx.launch_members([(tenant, i) for i in range(len(layers))])
+    torch.cuda.synchronize()
+    for n, L in zip(names, layers):
+        assert rel_err(L, expect(oracle, L, L.relu)) <= TOL, n
+
+
+def test_tile_table_matches_planner_blocks(registered):
+    """gm_build_tile_table == thread_blocks under the b200 profile (member, m, n order)."""
+    from paper_1901_00041_b200 import scheduler as S
+    ctx, tenant, _, layers = registered
+    q = S.RequestQueue()
+    shapes = [ctx.layer_shape(tenant, i) for i in range(4)]
+    for i, s in enumerate(shapes):
+        q.enqueue(S.KernelRequest(i + 1, tenant, s, 0, 10**9, i))
+    p = S.BatchPolicy(target_batch=1, allow_variable_size=True)
+    sks = S.form_batches(q, 10**8, p, ctx.device)
+    for sk in sks:
+        tt = sk.tile_table(ctx.device)
+        assert len(tt) == sk.planned_cost.blocks
+        expect_tt = [(j, a, b) for j, r in enumerate(sk.members)
+                     for a in range(-(-r.shape.m // ctx.device.tile_m)) for b in range(-(-r.shape.n // ctx.device.tile_n))]
+        assert tt == expect_tt
+
+
+def small_engine(tenants=3, batch=2, image=64, options=None):
+    from paper_1901_00041_b200 import workload as W
+    from paper_1901_00041_b200.engine import SpaceTimeEngine
+    return SpaceTimeEngine([W.resnet18(image)] * tenants, [batch] * tenants, options=options or {})
+
+
+def check_engine(eng, oracle):
+    for m in eng.models:
+        for L, buf in zip(m.layers, m.buffers):
+            err = rel_err(buf, expect(oracle, buf))
+            assert err <= TOL, f"{L.name}: {err:.3e}"
+
+
+def clear(eng):
+    for m in eng.models:
+        for buf in m.buffers:
+            buf.y.fill_(float("nan"))
+
+
+def test_round_program_matches_oracle(oracle):
+    """A whole 3-tenant ResNet-18 round as ONE persistent launch (device-side deps)."""
+    eng = small_engine()
+    rnd = eng.plan_round()
+    assert all(len(k.members) == 3 for k in rnd.kernels)
+    clear(eng)
+    s = torch.cuda.Stream()
+    rnd.launch_round(s.cuda_stream)
+    torch.cuda.synchronize()
+    check_engine(eng, oracle)
+
+
+def test_modes_compute_identical_bits(oracle):
+    """Packed (per plan), round program, time-only and space-only run the same
+    kernel code: outputs are bit-identical across modes."""
+    eng = small_engine(tenants=2)
+    rnd = eng.plan_round()
+    s = torch.cuda.Stream()
+    outs = []
+    for launch in (lambda: rnd.launch_round(s.cuda_stream), lambda: rnd.launch(s.cuda_stream),
+                   lambda: eng.capture_serial("time_only").launch(s.cuda_stream),
+                   lambda: eng.capture_serial("space_only").launch(s.cuda_stream),
+                   lambda: eng.capture_round(rnd).launch(s.cuda_stream)):
+        clear(eng)
+        launch()
+        torch.cuda.synchronize()
+        outs.append([b.y.clone() for m in eng.models for b in m.buffers])
+    for other in outs[1:]:
+        for a, b in zip(outs[0], other):
+            assert torch.equal(a, b)
+    check_engine(eng, oracle)
+
+
+@pytest.mark.parametrize("options", [{"split_k": 1}, {"narrow_min_tiles": 32}, {"pdl": 0},
+                                     {"split_k": 1, "max_splits": 8, "narrow_min_tiles": 64}])
+def test_execution_options_keep_results(oracle, options):
+    eng = small_engine(tenants=2, batch=4, options=options)
+    rnd = eng.plan_round()
+    clear(eng)
+    s = torch.cuda.Stream()
+    rnd.launch_round(s.cuda_stream)
+    torch.cuda.synchronize()
+    check_engine(eng, oracle)
+
+
+def test_serve_round_e2e_host_buffers(oracle):
+    eng = small_engine(tenants=2)
+    s = torch.cuda.Stream()
+    h_in = [m.query_input.cpu().pin_memory() for m in eng.models]
+    h_out = [torch.empty_like(m.query_output, device="cpu").pin_memory() for m in eng.models]
+    for _ in range(3):
+        rnd = eng.serve_round(h_in, h_out, s)
+    assert len(eng._graphs) == 1  # steady state: one cached launch program
+    for m, h in zip(eng.models, h_out):
+        assert torch.equal(h, m.query_output.cpu())
+    check_engine(eng, oracle)
+
+
+def test_no_silent_fallback_on_bad_registration():
+    from paper_1901_00041_b200.runtime import Context, LayerBuffers
+    from paper_1901_00041_b200.scheduler import GemmShape
+    ctx = Context(0)
+    x = torch.zeros(64, 100, dtype=torch.bfloat16, device="cuda")  # 200 B rows: not 16 B aligned strides
+    w = torch.zeros(64, 100, dtype=torch.bfloat16, device="cuda")
+    y = torch.zeros(64, 64, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError, match="multiple of 8"):
+        ctx.register_tenant([LayerBuffers("gemm", x, w, y, gemm=GemmShape(64, 64, 100))])

@@ -36,9 +36,16 @@ def gemm_case(M, N, K, dev):
 
 
 def main():
+    import argparse
+    from paper_1901_00041_b200.scheduler import b200_profile
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--tile-n", type=int, default=256)
+    a = ap.parse_args()
     dev = torch.device("cuda:0")
     torch.manual_seed(0)
-    ctx = Context(0)
+    spec = b200_profile()
+    spec.tile_n = a.tile_n
+    ctx = Context(0, device=spec)
     cases = {
         "gemm 256x128x1152": gemm_case(256, 128, 1152, dev),
         "gemm 200x72x100 (tails)": gemm_case(200, 72, 100, dev),
@@ -49,6 +56,9 @@ def main():
         "conv 1x1 s2 56x56x256->512 b1": conv_case(1, 56, 56, 256, 512, 1, 2, 0, dev),
         "conv 7x7 s2 stem 224->64 b2": conv_case(2, 224, 224, 3, 64, 7, 2, 3, dev),
         "conv 3x3 s1 7x7x512->512 b3": conv_case(3, 7, 7, 512, 512, 3, 1, 1, dev),
+        "conv 3x3 s1 7x7x512->512 b1 (M=49)": conv_case(1, 7, 7, 512, 512, 3, 1, 1, dev),
+        "gemm 8x1000x2048 (fc b8)": gemm_case(8, 1000, 2048, dev),
+        "gemm 384x2304x768 (bert qkv)": gemm_case(384, 2304, 768, dev),
     }
     names = list(cases)
     tenant = ctx.register_tenant([cases[n][0] for n in names])
@@ -75,6 +85,32 @@ def main():
         err = ((y - ref).abs().max() / ref.abs().max()).item()
         print(f"packed {n:29s} rel_err={err:.3e}", flush=True)
         ok &= err < 1e-2
+    # round program: a 3-tenant ResNet-18@64 round in one persistent launch
+    from paper_1901_00041_b200 import workload as W
+    from paper_1901_00041_b200.engine import SpaceTimeEngine
+    layers = W.resnet18(64)
+    eng = SpaceTimeEngine([layers] * 3, [2, 2, 2])
+    rnd = eng.plan_round()
+    refs = []
+    for m in eng.models:
+        for L, buf in zip(m.layers, m.buffers):
+            if L.kind == "conv":
+                c = L.conv
+                w = buf.w[:, : c.kernel_h * c.kernel_w * c.in_channels].reshape(
+                    c.out_channels, c.kernel_h, c.kernel_w, c.in_channels)
+                r = torch.nn.functional.conv2d(buf.x.float().permute(0, 3, 1, 2), w.float().permute(0, 3, 1, 2),
+                                               stride=c.stride, padding=c.padding).permute(0, 2, 3, 1).reshape(
+                    buf.y.shape)
+            else:
+                r = buf.x.float() @ buf.w.float().t()
+            refs.append((buf.y, r))
+            buf.y.fill_(float("nan"))
+    s = torch.cuda.Stream()
+    rnd.launch_round(s.cuda_stream)
+    torch.cuda.synchronize()
+    worst = max(((y.float() - r).abs().max() / r.abs().max()).item() for y, r in refs)
+    print(f"round program: {len(rnd.kernels)} plans in 1 launch, worst rel err {worst:.3e}")
+    ok &= worst < 1e-2
     print("ALL OK" if ok else "FAIL")
 
 
