@@ -193,6 +193,9 @@ size_t gm_plans_count(const gm_plans* p);
 int gm_plans_get(const gm_plans* p, size_t i, gm_plan_info* out);
 int gm_plans_members(const gm_plans* p, size_t i, gm_kernel_request* out, size_t cap, size_t* n);
 void gm_plans_destroy(gm_plans* p);
+/* 64-bit identity of a plan list (signatures + member tenant/layer ids): the
+ * key under which a captured launch program is cached and replayed. */
+int gm_plans_key(const gm_plans* p, uint64_t* key);
 /* Tile-dispatch table of plan i under device d. */
 int gm_build_tile_table(const gm_plans* p, size_t i, const gm_device_spec* d, gm_tile* out,
                         size_t cap, size_t* n);

@@ -137,6 +137,7 @@ _SIGS = {
     "gm_plans_get": (C.c_int, [C.c_void_p, C.c_size_t, P(gm_plan_info)]),
     "gm_plans_members": (C.c_int, [C.c_void_p, C.c_size_t, P(gm_kernel_request), C.c_size_t, P(C.c_size_t)]),
     "gm_plans_destroy": (None, [C.c_void_p]),
+    "gm_plans_key": (C.c_int, [C.c_void_p, P(C.c_uint64)]),
     "gm_build_tile_table": (C.c_int, [C.c_void_p, C.c_size_t, P(gm_device_spec), P(gm_tile), C.c_size_t,
                                       P(C.c_size_t)]),
     "gm_plan_super_kernel": (C.c_int, [P(gm_kernel_request), C.c_size_t, C.c_int, P(gm_batch_policy),

@@ -324,6 +324,30 @@ int gm_plans_members(const gm_plans* p, size_t i, gm_kernel_request* out, size_t
 
 void gm_plans_destroy(gm_plans* p) { delete p; }
 
+int gm_plans_key(const gm_plans* p, uint64_t* key) {
+  GM_API_BEGIN
+  need(p, "plans");
+  need(key, "key");
+  // FNV-1a over every plan's signature and member (tenant, layer) identities:
+  // equal keys <=> the same launch program (the CUDA-graph cache key).
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&h](const void* data, size_t n) {
+    const unsigned char* b = static_cast<const unsigned char*>(data);
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  };
+  for (const Plan& plan : p->plans) {
+    mix(plan.signature.data(), plan.signature.size());
+    for (const Request& r : plan.members) {
+      mix(&r.tenant, sizeof(r.tenant));
+      mix(&r.layer, sizeof(r.layer));
+    }
+    const char sep = '|';
+    mix(&sep, 1);
+  }
+  *key = h;
+  GM_API_END
+}
+
 int gm_build_tile_table(const gm_plans* p, size_t i, const gm_device_spec* d, gm_tile* out, size_t cap,
                         size_t* n) {
   GM_API_BEGIN

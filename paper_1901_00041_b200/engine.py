@@ -136,7 +136,7 @@ class SpaceTimeEngine:
             self.tenants.append(self.ctx.register_tenant(m.buffers, slo_latency=slo_latency,
                                                          tenant_id=f"t{tenant_offset + i}"))
         self._now = 0
-        self._graphs: Dict[Tuple[str, ...], Graph] = {}
+        self._graphs: Dict[int, Graph] = {}  # plan-list key -> captured round program
 
     # ------------------------------------------------------------ planning
     def flops_per_round(self) -> int:
@@ -153,8 +153,8 @@ class SpaceTimeEngine:
         if policy is not None:
             self.ctx.set_policy(policy)
         r = self.ctx.plan_round(self.tenants, self._now)
-        if r.times:
-            self._now = max(e for _, e in r.times)
+        if r.count:
+            self._now = r.end_time()  # dispatches are serial on the virtual device
         return r
 
     # ------------------------------------------------------------ launch programs
@@ -190,7 +190,7 @@ class SpaceTimeEngine:
             for m, h in zip(self.models, host_inputs):
                 m.query_input.copy_(h, non_blocking=True)
             rnd = self.plan_round()
-            key = tuple(rnd.signatures)
+            key = rnd.key
             g = self._graphs.get(key)
             if g is None:
                 g = self._graphs[key] = self.capture_round(rnd)

@@ -144,13 +144,38 @@ class Round:
     def __init__(self, ctx: Context, handle: int):
         self.ctx = ctx
         self._owner = _Plans(handle)
-        self.kernels: List[SuperKernel] = _unpack_plans(handle, self._owner)
         self.handle = handle
-        self.times = []
-        for i in range(len(self.kernels)):
-            s, e = C.c_int64(), C.c_int64()
-            check(lib().gm_plans_times(handle, i, C.byref(s), C.byref(e)))
-            self.times.append((int(s.value), int(e.value)))
+        self.count = int(lib().gm_plans_count(handle))
+        k = C.c_uint64()
+        check(lib().gm_plans_key(handle, C.byref(k)))
+        self.key = int(k.value)
+        self._kernels: Optional[List[SuperKernel]] = None
+        self._times: Optional[List[tuple]] = None
+
+    @property
+    def kernels(self) -> List[SuperKernel]:
+        """The formed super-kernels (unpacked on first use)."""
+        if self._kernels is None:
+            self._kernels = _unpack_plans(self.handle, self._owner)
+        return self._kernels
+
+    @property
+    def times(self) -> List[tuple]:
+        """Virtual [start, end) of every dispatch of the round."""
+        if self._times is None:
+            self._times = []
+            for i in range(self.count):
+                s, e = C.c_int64(), C.c_int64()
+                check(lib().gm_plans_times(self.handle, i, C.byref(s), C.byref(e)))
+                self._times.append((int(s.value), int(e.value)))
+        return self._times
+
+    def end_time(self) -> int:
+        if not self.count:
+            return 0
+        s, e = C.c_int64(), C.c_int64()
+        check(lib().gm_plans_times(self.handle, self.count - 1, C.byref(s), C.byref(e)))
+        return int(e.value)
 
     @property
     def signatures(self) -> List[str]:
