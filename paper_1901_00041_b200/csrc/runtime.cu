@@ -93,8 +93,13 @@ struct Prepared {
   uint32_t* split_ctr = nullptr;
   int n_ws = 0;
   std::vector<uint16_t> tile_plan;  // round programs: plan index of every tile (profiling)
+  // dynamic schedule: per-tenant work queues (heads live after the counters)
+  uint32_t* heads = nullptr;
+  int32_t* qinfo = nullptr;  // [nq] begins then [nq] lengths
+  int nq = 0;
 
   void release() {
+    cudaFree(qinfo);
     cudaFree(tiles);
     cudaFree(counters);
     cudaFree(targets);
@@ -123,6 +128,7 @@ struct Runtime {
   bool split_k = false;      // round programs split few-tile long-K members (opt-in)
   int64_t max_splits = 4;
   int64_t narrow_min_tiles = 0;  // >0: narrow a member's N tile until it has this many tiles
+  bool dynamic_schedule = false;  // round programs: per-tenant ready queues (else static round-robin)
   int bn = 256;     // N tile of the super-kernel (== DeviceSpec.tile_n)
   int smem_bytes = 0;
   const void* kernel = nullptr;
@@ -435,6 +441,30 @@ struct Runtime {
       }
       p.tile_plan.resize(table.size(), static_cast<uint16_t>(&pl - plans.data()));
     }
+    // Dynamic schedule: one work queue per tenant, its tiles in plan order.
+    std::vector<int32_t> qbeg, qlen;
+    if (dynamic_schedule && !table.empty()) {
+      std::vector<size_t> idx(table.size());
+      for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
+      auto tenant_of = [&](size_t i) { return flat[table[i].member].tenant; };
+      std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return tenant_of(a) < tenant_of(b); });
+      std::vector<dev::TileEntry> sorted(table.size());
+      std::vector<uint16_t> sorted_plan(table.size());
+      for (size_t i = 0; i < idx.size(); ++i) {
+        sorted[i] = table[idx[i]];
+        sorted_plan[i] = p.tile_plan[idx[i]];
+      }
+      table.swap(sorted);
+      p.tile_plan.swap(sorted_plan);
+      for (size_t i = 0; i < table.size(); ++i) {
+        if (i == 0 || flat[table[i].member].tenant != flat[table[i - 1].member].tenant) {
+          qbeg.push_back(static_cast<int32_t>(i));
+          qlen.push_back(0);
+        }
+        ++qlen.back();
+      }
+    }
+    p.nq = static_cast<int>(qbeg.size());
     p.n_tiles = static_cast<int>(table.size());
     p.n_counters = static_cast<int>(targets.size());
     p.n_ws = n_ws;
@@ -459,7 +489,17 @@ struct Runtime {
     cuda_check(cudaMalloc(&p.tiles, std::max<size_t>(1, table.size()) * sizeof(dev::TileEntry)), "cudaMalloc(tiles)");
     cuda_check(cudaMemcpy(p.tiles, table.data(), table.size() * sizeof(dev::TileEntry), cudaMemcpyHostToDevice),
                "upload round tiles");
-    cuda_check(cudaMalloc(&p.counters, std::max<size_t>(1, targets.size()) * sizeof(uint32_t)), "cudaMalloc(counters)");
+    // counters and queue heads share one allocation: one memset per launch resets both
+    cuda_check(cudaMalloc(&p.counters, std::max<size_t>(1, targets.size() + p.nq) * sizeof(uint32_t)),
+               "cudaMalloc(counters)");
+    if (p.nq > 0) {
+      p.heads = p.counters + targets.size();
+      std::vector<int32_t> qinfo(qbeg);
+      qinfo.insert(qinfo.end(), qlen.begin(), qlen.end());
+      cuda_check(cudaMalloc(&p.qinfo, qinfo.size() * sizeof(int32_t)), "cudaMalloc(queues)");
+      cuda_check(cudaMemcpy(p.qinfo, qinfo.data(), qinfo.size() * sizeof(int32_t), cudaMemcpyHostToDevice),
+                 "upload queues");
+    }
     cuda_check(cudaMalloc(&p.targets, std::max<size_t>(1, targets.size()) * sizeof(uint32_t)), "cudaMalloc(targets)");
     cuda_check(cudaMemcpy(p.targets, targets.data(), targets.size() * sizeof(uint32_t), cudaMemcpyHostToDevice),
                "upload round targets");
@@ -490,7 +530,7 @@ struct Runtime {
       if (count) ++n_prepasses;
     }
     if (p.counters)
-      cuda_check(cudaMemsetAsync(p.counters, 0, static_cast<size_t>(p.n_counters) * sizeof(uint32_t), stream),
+      cuda_check(cudaMemsetAsync(p.counters, 0, static_cast<size_t>(p.n_counters + p.nq) * sizeof(uint32_t), stream),
                  "reset round counters");
     if (ev_begin) cuda_check(cudaEventRecordWithFlags(ev_begin, stream, cudaEventRecordExternal), "event record");
     const int grid = std::max(1, std::min(p.n_tiles, sms));
@@ -509,7 +549,8 @@ struct Runtime {
     int n = p.n_tiles;
     uint32_t* counters = p.counters;
     const uint32_t* targets = p.targets;
-    dev::RoundArgs ra{counters, targets, p.ws_map, p.ws, p.split_ctr, trace};
+    dev::RoundArgs ra{counters, targets, p.ws_map, p.ws, p.split_ctr, trace,
+                      p.heads, p.qinfo, p.qinfo ? p.qinfo + p.nq : nullptr, p.nq};
     void* args[4] = {&slots, &tiles, &n, &ra};
     cuda_check(cudaLaunchKernelExC(&cfg, kernel, args), "launch superkernel");
     if (ev_end) cuda_check(cudaEventRecordWithFlags(ev_end, stream, cudaEventRecordExternal), "event record");
@@ -680,6 +721,8 @@ int gm_ctx_set_option(gm_ctx* ctx, const char* name, int64_t value) {
   } else if (n == "max_splits") {
     if (value < 2 || value > 64) throw std::invalid_argument("max_splits must be in [2, 64]");
     rt.max_splits = value;
+  } else if (n == "dynamic_schedule") {
+    rt.dynamic_schedule = value != 0;  // applies to round programs prepared afterwards
   } else if (n == "narrow_min_tiles") {
     rt.narrow_min_tiles = value;  // applies to tenants registered afterwards
   } else {

@@ -46,7 +46,7 @@ struct Cfg {
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;
-  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 512 /*barriers, tile ring*/;
 };
 
 enum : int32_t { kATiled = 0, kAIm2col = 1 };
@@ -87,14 +87,29 @@ struct TileEntry {
 };
 
 // Round-program side state (all null for a plain super-kernel launch).
+//
+// Dynamic scheduling (round programs): the tiles are grouped into one work
+// queue per tenant (tiles [qbeg[q], qbeg[q] + qlen[q]) in that tenant's plan
+// order).  A CTA claims the head of any queue whose head tile's dependency is
+// already satisfied (atomicCAS on heads[q]), so a tenant blocked at a layer
+// boundary never idles SMs another tenant could use and tenants desynchronise
+// instead of running in lock-step.  Claimed tiles never wait, so the claim
+// order cannot deadlock.  heads == nullptr selects the static schedule.
 struct RoundArgs {
   uint32_t* counters;         // per member instance: tile-quarters stored
   const uint32_t* targets;
-  const CUtensorMap* ws_map;  // fp32 [n_ws * 128, BN], 16 x 32 reduce boxes
-  float* ws;
+  const CUtensorMap* ws_map;  // (unused; kept for ABI stability of the struct)
+  float* ws;                  // split-K workspace, lane-major fp32
   uint32_t* split_ctr;        // per workspace tile and quarter: splits arrived
   uint64_t* trace;            // 6 %globaltimer stamps per tile (profiling)
+  uint32_t* heads;            // per queue: next unclaimed position
+  const int32_t* qbeg;
+  const int32_t* qlen;
+  int32_t nq;
 };
+
+constexpr int kTileQ = 8;   // claimed-tile ring between producer and consumers
+constexpr int kSchedQ = 2;  // scheduler look-ahead: tiles claimed before the producer needs them
 
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
@@ -243,7 +258,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + kStages;
   uint64_t* acc_full = empty + kStages;
   uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* tq_full = acc_empty + 2;     // claimed-tile ring: producer -> consumers
+  uint64_t* tq_empty = tq_full + kTileQ;
+  uint64_t* sq_full = tq_empty + kTileQ;  // scheduler -> producer (claim look-ahead)
+  uint64_t* sq_empty = sq_full + kSchedQ;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sq_empty + kSchedQ);
+  volatile int32_t* tq = reinterpret_cast<volatile int32_t*>(tmem_slot + 1);
+  volatile int32_t* sq = tq + kTileQ;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -256,6 +277,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], 128);
+    }
+    for (int q = 0; q < kTileQ; ++q) {
+      mbar_init(&tq_full[q], 1);
+      mbar_init(&tq_empty[q], 1 + 8);  // the MMA thread + one lane per epilogue warp
+    }
+    for (int q = 0; q < kSchedQ; ++q) {
+      mbar_init(&sq_full[q], 1);
+      mbar_init(&sq_empty[q], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -278,7 +307,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ------------------------------------------------ TMA producer
       uint32_t stage = 0, phase = 0;
       bool first = true;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      uint32_t qslot = 0, qphase = 0, sslot = 0, sphase = 0;
+      for (;;) {
+        mbar_wait(&sq_full[sslot], sphase);  // next tile from the scheduler warp
+        const int t = sq[sslot];
+        mbar_arrive(&sq_empty[sslot]);
+        if (++sslot == kSchedQ) {
+          sslot = 0;
+          sphase ^= 1;
+        }
+        mbar_wait(&tq_empty[qslot], qphase ^ 1);
+        tq[qslot] = t;
+        mbar_arrive(&tq_full[qslot]);
+        if (++qslot == kTileQ) {
+          qslot = 0;
+          qphase ^= 1;
+        }
+        if (t < 0) break;
         const TileEntry te = tiles[t];
         const MemberDesc* md = slots + te.member;
         prefetch_tmap(&md->a);
@@ -372,7 +417,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       // ------------------------------------------------ MMA issuer
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      uint32_t qslot = 0, qphase = 0;
+      for (;;) {
+        mbar_wait(&tq_full[qslot], qphase);
+        const int t = tq[qslot];
+        mbar_arrive(&tq_empty[qslot]);
+        if (++qslot == kTileQ) {
+          qslot = 0;
+          qphase ^= 1;
+        }
+        if (t < 0) break;
         const TileEntry te = tiles[t];
         const MemberDesc* md = slots + te.member;
         const int kb_lo = te.kb_end ? te.kb_begin : 0;
@@ -405,6 +459,57 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (acc == 0) acc_phase ^= 1;
       }
     }
+  } else if (warp == 3) {
+    if (lane == 0) {
+      // ------------------------------------------------ tile scheduler
+      // Claims this CTA's next tile (static round-robin, or the head of a
+      // ready per-tenant queue) up to kSchedQ tiles ahead of the producer, so
+      // the claim's atomic round trip overlaps the producer's loads.
+      uint32_t sslot = 0, sphase = 0;
+      int static_next = blockIdx.x;
+      int rr = ra.nq > 0 ? static_cast<int>(blockIdx.x) % ra.nq : 0;
+      auto claim = [&]() -> int {
+        if (!ra.heads) {
+          const int t = static_next < n_tiles ? static_next : -1;
+          static_next += gridDim.x;
+          return t;
+        }
+        for (;;) {
+          bool pending = false;
+          for (int i = 0; i < ra.nq; ++i) {
+            const int q = rr + i < ra.nq ? rr + i : rr + i - ra.nq;
+            const uint32_t len = static_cast<uint32_t>(ra.qlen[q]);
+            const uint32_t h = *reinterpret_cast<volatile uint32_t*>(ra.heads + q);
+            if (h >= len) continue;
+            pending = true;
+            // peek (no contention): skip a queue whose head is still blocked
+            const int dep = tiles[ra.qbeg[q] + static_cast<int>(h)].dep;
+            if (dep >= 0 && ld_acquire(counters + dep) < targets[dep]) continue;
+            // claim with one fetch-and-add; a claim that overtook the peeked
+            // head may land on a not-yet-ready tile, which the gate waits for
+            // (queue order is a topological order, so this cannot deadlock)
+            const uint32_t got = atomicAdd(ra.heads + q, 1u);
+            if (got < len) {
+              rr = q;
+              return ra.qbeg[q] + static_cast<int>(got);
+            }
+          }
+          if (!pending) return -1;
+          __nanosleep(100);
+        }
+      };
+      for (;;) {
+        const int t = claim();
+        mbar_wait(&sq_empty[sslot], sphase ^ 1);
+        sq[sslot] = t;
+        mbar_arrive(&sq_full[sslot]);
+        if (++sslot == kSchedQ) {
+          sslot = 0;
+          sphase ^= 1;
+        }
+        if (t < 0) break;
+      }
+    }
   } else if (warp >= 4) {
     // -------------------------------------------------- epilogue: 2 warpgroups
     // Warpgroup g drains accumulator buffer g, i.e. every other tile, so one
@@ -414,8 +519,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t acc = static_cast<uint32_t>((warp - 4) >> 2);
     uint8_t* stage_buf = epi + (warp - 4) * 2 * kEpiBufBytes;
     uint32_t acc_phase = 0, buf = 0;
-    int issued = 0, local = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++local) {
+    int issued = 0;
+    uint32_t qslot = 0, qphase = 0;
+    for (int local = 0;; ++local) {
+      int t = 0;
+      if (lane == 0) {
+        mbar_wait(&tq_full[qslot], qphase);
+        t = tq[qslot];
+        mbar_arrive(&tq_empty[qslot]);
+      }
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (++qslot == kTileQ) {
+        qslot = 0;
+        qphase ^= 1;
+      }
+      if (t < 0) break;
       if ((local & 1) != static_cast<int>(acc)) continue;
       const TileEntry te = tiles[t];
       const MemberDesc* md = slots + te.member;
@@ -462,64 +580,55 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
       bool publish = te.done >= 0;
       if (te.splits > 1) {
-        // ---- split-K partial: reduce-add fp32 into the workspace tile
-        const int ws_row = te.ws * kBM + quarter * 32;
-        for (int c = 0; c < cols; c += kEpiChunk) {
-          uint32_t v[32];
-          tmem_ld32(taddr + c, v);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            if (c + 16 * h < cols) {
-              uint8_t* sbuf = claim();
-              uint8_t* row = sbuf + lane * 64;
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                *reinterpret_cast<uint4*>(row + ((j ^ sw) << 4)) =
-                    make_uint4(v[16 * h + 4 * j], v[16 * h + 4 * j + 1], v[16 * h + 4 * j + 2], v[16 * h + 4 * j + 3]);
-              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-              __syncwarp();
-              if (lane == 0) {
-                asm volatile(
-                    "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                        reinterpret_cast<uint64_t>(ra.ws_map)),
-                    "r"(smem_u32(sbuf)), "r"(c + 16 * h), "r"(ws_row)
-                    : "memory");
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-              }
-              issue();
-            }
-          }
-        }
-        tc_fence_before();
-        mbar_arrive(&acc_empty[acc]);  // TMEM is free; the rest works from the workspace
-        uint32_t prev = 0;
-        if (lane == 0) {
-          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-          __threadfence();
-          prev = atomicAdd(ra.split_ctr + te.ws * 4 + quarter, 1u);
-        }
-        prev = __shfl_sync(0xffffffffu, prev, 0);
-        publish = publish && prev + 1 == te.splits;
-        if (prev + 1 == te.splits) {
-          // ---- last split: sum is complete; convert, store, clear the workspace
-          __threadfence();
-          float* wrow = ra.ws + static_cast<int64_t>(ws_row + lane) * BN;
+        // ---- split-K partial: coalesced fp32 red.add into the workspace tile.
+        // Lane-major layout: the 32 lanes' float4 of (chunk c, j) are 512
+        // contiguous bytes, so each warp-wide REDG.F32x4 is fully coalesced.
+        constexpr int kChunks = BN / kEpiChunk;
+        float* wq = ra.ws + (static_cast<int64_t>(te.ws) * 4 + quarter) * (kChunks * 8 * 128);
+        uint32_t* ctr = ra.split_ctr + te.ws * 4 + quarter;
+        const bool finisher = te.kb_end == md->k_blocks;  // the split holding the K tail
+        if (!finisher) {
+          // fire and forget: reduce-add the partial, then a release arrival
+          // per lane (orders this lane's reductions before it); no waiting
           for (int c = 0; c < cols; c += kEpiChunk) {
             uint32_t v[32];
-            float4* src = reinterpret_cast<float4*>(wrow + c);
+            tmem_ld32(taddr + c, v);
+            float* wc = wq + (c / kEpiChunk) * (8 * 128) + lane * 4;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(wc + j * 128),
+                           "f"(__uint_as_float(v[4 * j])), "f"(__uint_as_float(v[4 * j + 1])),
+                           "f"(__uint_as_float(v[4 * j + 2])), "f"(__uint_as_float(v[4 * j + 3]))
+                           : "memory");
+          }
+          tc_fence_before();
+          mbar_arrive(&acc_empty[acc]);
+          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+          publish = false;
+        } else {
+          // finisher: wait for the other splits' lanes, add its own TMEM
+          // partial to their sum, store bf16, clear the workspace
+          const uint32_t want = static_cast<uint32_t>(te.splits - 1) * 32u;
+          while (ld_acquire(ctr) < want) __nanosleep(40);
+          for (int c = 0; c < cols; c += kEpiChunk) {
+            uint32_t v[32];
+            tmem_ld32(taddr + c, v);
+            float4* src = reinterpret_cast<float4*>(wq + (c / kEpiChunk) * (8 * 128) + lane * 4);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              const float4 f = __ldcg(src + j);
-              v[4 * j] = __float_as_uint(f.x);
-              v[4 * j + 1] = __float_as_uint(f.y);
-              v[4 * j + 2] = __float_as_uint(f.z);
-              v[4 * j + 3] = __float_as_uint(f.w);
-              __stcg(src + j, make_float4(0.f, 0.f, 0.f, 0.f));
+              const float4 f = __ldcg(src + j * 32);
+              v[4 * j] = __float_as_uint(__uint_as_float(v[4 * j]) + f.x);
+              v[4 * j + 1] = __float_as_uint(__uint_as_float(v[4 * j + 1]) + f.y);
+              v[4 * j + 2] = __float_as_uint(__uint_as_float(v[4 * j + 2]) + f.z);
+              v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + f.w);
+              __stcg(src + j * 32, make_float4(0.f, 0.f, 0.f, 0.f));
             }
             if (m0 < md->m) store_bf16(v, c);
           }
-          if (lane == 0) ra.split_ctr[te.ws * 4 + quarter] = 0;
+          tc_fence_before();
+          mbar_arrive(&acc_empty[acc]);
+          __syncwarp();
+          if (lane == 0) *ctr = 0;  // next round (kernel boundary orders it)
         }
       } else {
         if (m0 < md->m) {  // warp-uniform: this quarter holds at least one real row
