@@ -77,6 +77,8 @@ struct Operator {
   const void* x = nullptr;
   void* scratch = nullptr;  // explicit-im2col rows [M, ldk]
   int64_t ldk = 0;
+  void* wpad = nullptr;     // narrow-channel conv: weights repacked to 8 channels per tap
+  int64_t kernel_k = 0;     // K the kernel iterates (0 = shape.k)
 };
 
 struct Prepared {
@@ -139,7 +141,10 @@ struct Runtime {
     cudaDeviceSynchronize();
     for (auto& [k, p] : prepared) p.release();
     for (auto& [k, p] : rounds) p.release();
-    for (Operator& op : flat) cudaFree(op.scratch);
+    for (Operator& op : flat) {
+      cudaFree(op.scratch);
+      cudaFree(op.wpad);
+    }
     cudaFree(d_desc);
   }
 
@@ -203,25 +208,29 @@ struct Runtime {
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled(store) failed (" + std::to_string(int(r)) + ")");
   }
 
-  void im2col_map(CUtensorMap* map, const void* x, const Conv& c, int batch, int pixels) {
+  // `pitch` = channels per stored pixel (>= C_in); `box_c` channels per box
+  // pixel: 64 (one SW128 row) for the regular mode, 8 (16 B, no swizzle) for
+  // the narrow-channel mode.
+  void im2col_map(CUtensorMap* map, const void* x, const Conv& c, int batch, int pixels, int64_t pitch = 0,
+                  int box_c = dev::kBK, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     if (!aligned16(x)) throw std::invalid_argument("conv input must be 16-byte aligned");
-    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(c.in_channels), static_cast<cuuint64_t>(c.image_w),
+    if (pitch <= 0) pitch = c.in_channels;
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(pitch), static_cast<cuuint64_t>(c.image_w),
                                 static_cast<cuuint64_t>(c.image_h), static_cast<cuuint64_t>(batch)};
-    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(c.in_channels * 2),
-                                   static_cast<cuuint64_t>(c.image_w * c.in_channels * 2),
-                                   static_cast<cuuint64_t>(c.image_h * c.image_w * c.in_channels * 2)};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(pitch * 2),
+                                   static_cast<cuuint64_t>(c.image_w * pitch * 2),
+                                   static_cast<cuuint64_t>(c.image_h * c.image_w * pitch * 2)};
     const int lower[2] = {static_cast<int>(-c.padding), static_cast<int>(-c.padding)};
     const int upper[2] = {static_cast<int>(c.padding - (c.kernel_w - 1)), static_cast<int>(c.padding - (c.kernel_h - 1))};
     const cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(c.stride), static_cast<cuuint32_t>(c.stride), 1};
     const CUresult r = encode_im2col(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides,
-                                     lower, upper, dev::kBK, static_cast<cuuint32_t>(pixels), estr,
-                                     CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                     lower, upper, static_cast<cuuint32_t>(box_c), static_cast<cuuint32_t>(pixels),
+                                     estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeIm2col failed (" + std::to_string(int(r)) + ")");
     // Driver <= 13.1 mis-encodes im2col maps of tensors under 128 KiB; clear
     // the offending bit exactly as CUTLASS does (copy_traits_sm90_im2col.hpp).
-    const int64_t bytes = static_cast<int64_t>(batch) * c.image_h * c.image_w * c.in_channels * 2;
+    const int64_t bytes = static_cast<int64_t>(batch) * c.image_h * c.image_w * pitch * 2;
     if (driver_version <= 13010 && bytes < 131072) reinterpret_cast<uint64_t*>(map)[1] &= ~(1ull << 21);
   }
 
@@ -267,6 +276,32 @@ struct Runtime {
           md.pad = static_cast<int32_t>(c.padding);
           md.s_taps = static_cast<int32_t>(c.kernel_w);
           md.c_blocks = static_cast<int32_t>(c.in_channels / dev::kBK);
+        } else if (c.in_channels <= dev::kNarrowC && L.ldx == dev::kNarrowC && c.kernel_h == c.kernel_w &&
+                   c.stride <= 8 && c.padding <= 127) {
+          // narrow-channel implicit GEMM: the input stores 8 channels per
+          // pixel; one 16 B TMA im2col column per filter tap, 8 taps per
+          // k-block; weights repacked once to the same (tap, 8-channel) K order
+          md.a_mode = dev::kAIm2colNarrow;
+          im2col_map(&md.a, L.x, c, op.batch, a_box_rows(op.shape.m), dev::kNarrowC, dev::kNarrowC,
+                     CU_TENSOR_MAP_SWIZZLE_NONE);
+          const int taps = static_cast<int>(c.kernel_h * c.kernel_w);
+          md.pq = static_cast<int32_t>(P * Q);
+          md.q = static_cast<int32_t>(Q);
+          md.stride = static_cast<int32_t>(c.stride);
+          md.pad = static_cast<int32_t>(c.padding);
+          md.s_taps = static_cast<int32_t>(c.kernel_w);
+          md.taps = taps;
+          md.images = op.batch;
+          op.kernel_k = static_cast<int64_t>(taps) * dev::kNarrowC;
+          const size_t wbytes = static_cast<size_t>(op.shape.n * op.kernel_k * 2);
+          cuda_check(cudaMalloc(&op.wpad, wbytes), "cudaMalloc(narrow weights)");
+          dev::pad_narrow_weights<<<static_cast<int>(std::min<int64_t>((op.shape.n * op.kernel_k + 255) / 256, 4096)),
+                                    256>>>(static_cast<const __nv_bfloat16*>(L.w), ldw,
+                                           static_cast<__nv_bfloat16*>(op.wpad), static_cast<int>(op.shape.n), taps,
+                                           static_cast<int>(c.in_channels));
+          cuda_check(cudaGetLastError(), "launch pad_narrow_weights");
+          cuda_check(cudaDeviceSynchronize(), "pad_narrow_weights");
+          tiled_map(&md.b, op.wpad, op.shape.n, op.kernel_k, op.kernel_k, b_box_rows(op.shape.n, op.n_tile));
         } else {
           md.a_mode = dev::kATiled;  // explicit im2col pre-pass, then GEMM
           op.prepass = true;
@@ -292,8 +327,11 @@ struct Runtime {
       store_map(&md.c, L.y, op.shape.m, op.shape.n);
       md.m = static_cast<int32_t>(op.shape.m);
       md.n = static_cast<int32_t>(op.shape.n);
-      md.k_blocks = static_cast<int32_t>((op.shape.k + dev::kBK - 1) / dev::kBK);
+      if (op.kernel_k == 0) op.kernel_k = op.shape.k;
+      md.k_blocks = static_cast<int32_t>((op.kernel_k + dev::kBK - 1) / dev::kBK);
       md.idesc = make_idesc(b_box_rows(op.shape.n, op.n_tile));
+      // one k-block moves an A box (rows x 64 channels, or 8 tap columns of
+      // rows x 8 channels: the same bytes) plus a B box
       md.tx_bytes = static_cast<uint32_t>((a_box_rows(op.shape.m) + b_box_rows(op.shape.n, op.n_tile)) * dev::kBK * 2);
       md.relu = L.relu ? 1 : 0;
       md.n_tile = op.n_tile;

@@ -49,7 +49,13 @@ struct Cfg {
   static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 512 /*barriers, tile ring*/;
 };
 
-enum : int32_t { kATiled = 0, kAIm2col = 1 };
+// A-operand modes: 2-D tiled box; TMA im2col (C_in % 64 == 0: one 128 B
+// channel block per k-block, SW128); narrow-channel TMA im2col (input pixel
+// pitch of 8 channels: eight 16 B tap columns per k-block, SWIZZLE_NONE).
+enum : int32_t { kATiled = 0, kAIm2col = 1, kAIm2colNarrow = 2 };
+constexpr int kNarrowC = 8;                     // channels per pixel of a narrow-im2col input
+constexpr int kNarrowTaps = kBK / kNarrowC;     // filter taps per k-block
+constexpr int kNarrowTapBytes = kBM * kNarrowC * 2;  // one tap column: 128 pixels x 16 B
 
 // Device-resident descriptor of one registered (tenant, layer) operator.
 struct alignas(128) MemberDesc {
@@ -67,6 +73,8 @@ struct alignas(128) MemberDesc {
   int32_t c_blocks;     // Cin / kBK
   int32_t relu;
   int32_t n_tile;       // output columns per tile (<= BN): narrower for few-tile members
+  int32_t taps;         // narrow im2col: R*S filter taps
+  int32_t images;       // narrow im2col: batch (an out-of-range image zero-fills a box)
 };
 
 // Device tile-table entry; `member` is the registered slot index.
@@ -198,6 +206,18 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr) {
   d |= static_cast<uint64_t>(1024u >> 4) << 32;
   d |= static_cast<uint64_t>(1u) << 46;
   d |= static_cast<uint64_t>(2u) << 61;
+  return d;
+}
+
+// SWIZZLE_NONE K-major descriptor: 8-row x 16 B core matrices contiguous,
+// SBO = 128 B to the next 8 rows, LBO = one narrow tap column to the next 8
+// K elements.
+__device__ __forceinline__ uint64_t interleave_desc(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(kNarrowTapBytes >> 4) << 16;
+  d |= static_cast<uint64_t>(128u >> 4) << 32;
+  d |= static_cast<uint64_t>(1u) << 46;
   return d;
 }
 
@@ -333,7 +353,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t tx = md->tx_bytes;
         const int m0 = te.m_tile * kBM;
         const int n0 = te.n_tile * md->n_tile;
-        const bool im2col = md->a_mode == kAIm2col;
+        const bool narrow = md->a_mode == kAIm2colNarrow;
+        const bool im2col = md->a_mode == kAIm2col || narrow;
         int img = 0, h0 = 0, w0 = 0, c_blocks = 1, s_taps = 1;
         if (im2col) {
           img = m0 / md->pq;
@@ -347,7 +368,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         auto load_a = [&](int kb, uint32_t st) {
           uint8_t* a_dst = ring + st * C::kStageBytes;
-          if (im2col) {
+          if (narrow) {
+            // eight 16 B tap columns; taps past R*S load an out-of-range image
+            // so TMA zero-fills them (the weights there are zero too)
+#pragma unroll 1
+            for (int j = 0; j < kNarrowTaps; ++j) {
+              const int tap = kb * kNarrowTaps + j;
+              const bool real = tap < md->taps;
+              const int r = real ? tap / s_taps : 0;
+              const int s = real ? tap - r * s_taps : 0;
+              tma_load_im2col(a_dst + j * kNarrowTapBytes, &md->a, &full[st], 0, w0, h0, real ? img : md->images,
+                              static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+            }
+          } else if (im2col) {
             const int tap = kb / c_blocks;
             const int c0 = (kb - tap * c_blocks) * kBK;
             const int r = tap / s_taps;
@@ -432,6 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kb_lo = te.kb_end ? te.kb_begin : 0;
         const int k_blocks = te.kb_end ? te.kb_end : md->k_blocks;
         const uint32_t idesc = md->idesc;
+        const bool a_narrow = md->a_mode == kAIm2colNarrow;
         mbar_wait(&acc_empty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -443,9 +477,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t b_addr = a_addr + kABytes;
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
-            // advance 16 bf16 (32 B) along K inside the 128 B swizzle atom
-            umma_bf16(d_tmem, sw128_desc(a_addr + k * 32), sw128_desc(b_addr + k * 32), idesc,
-                      (kb != kb_lo || k != 0) ? 1u : 0u);
+            // advance 16 bf16 along K: 32 B inside the 128 B swizzle atom, or
+            // two narrow tap columns
+            const uint64_t a_desc =
+                a_narrow ? interleave_desc(a_addr + k * 2 * kNarrowTapBytes) : sw128_desc(a_addr + k * 32);
+            umma_bf16(d_tmem, a_desc, sw128_desc(b_addr + k * 32), idesc, (kb != kb_lo || k != 0) ? 1u : 0u);
           }
           umma_commit(&empty[stage]);  // frees the smem stage once these MMAs retire
           if (++stage == kStages) {
@@ -660,6 +696,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::kTmemCols)
                  : "memory");
+  }
+}
+
+// Registration-time repack of narrow-channel conv weights: KRSC rows with
+// C_in channels per tap -> kNarrowC channels per tap (zero padded), the K order
+// of the narrow im2col A operand.
+__global__ void pad_narrow_weights(const __nv_bfloat16* __restrict__ src, int64_t ldw, __nv_bfloat16* __restrict__ dst,
+                                   int cout, int taps, int cin) {
+  const int row = taps * kNarrowC;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cout * row; i += gridDim.x * blockDim.x) {
+    const int o = i / row;
+    const int rem = i - o * row;
+    const int tap = rem / kNarrowC;
+    const int c = rem - tap * kNarrowC;
+    dst[i] = c < cin ? src[static_cast<int64_t>(o) * ldw + tap * cin + c] : __float2bfloat16(0.f);
   }
 }
 

@@ -23,7 +23,7 @@ import torch
 from . import _native as N
 from ._native import check, lib
 from .runtime import Context, LayerBuffers, Round
-from .scheduler import BatchPolicy
+from .scheduler import BatchPolicy, DeviceSpec
 from .workload import Layer
 
 _MASK = (1 << 64) - 1
@@ -42,6 +42,7 @@ def mix64(*parts: int) -> int:
 
 
 KIND_INPUT, KIND_WEIGHT = 1, 2
+NARROW_C = 8  # pixel pitch of narrow-channel conv inputs (superkernel.cuh kNarrowC)
 
 
 class Graph:
@@ -77,7 +78,8 @@ class TenantModel:
     rows are padded to a multiple of 8 elements (16-byte TMA strides).
     """
 
-    def __init__(self, layers: Sequence[Layer], batch: int, seed: int, tenant: int, device: torch.device):
+    def __init__(self, layers: Sequence[Layer], batch: int, seed: int, tenant: int, device: torch.device,
+                 narrow_inputs: bool = False):
         self.layers = list(layers)
         self.batch = batch
         self.buffers: List[LayerBuffers] = []
@@ -94,6 +96,14 @@ class TenantModel:
                 c = L.conv
                 x = (torch.rand(batch, c.image_h, c.image_w, c.in_channels, device=device, generator=g_in) * 2 - 1)
                 x = x.to(torch.bfloat16)
+                if narrow_inputs and c.in_channels < NARROW_C and c.kernel_h > 1:
+                    # narrow-channel input (RGB stem): stored with an 8-channel
+                    # pixel pitch, zero padded, for the narrow TMA im2col path
+                    # (opt-in: one 16 B TMA request per pixel and tap is slower
+                    # than the explicit pre-pass on B200)
+                    xp = torch.zeros(batch, c.image_h, c.image_w, NARROW_C, device=device, dtype=torch.bfloat16)
+                    xp[..., : c.in_channels] = x
+                    x = xp
                 y = torch.empty(s.m, s.n, device=device, dtype=torch.bfloat16)
                 self.buffers.append(LayerBuffers("conv", x, w, y, conv=c, batch=batch))
             else:
@@ -122,10 +132,11 @@ class SpaceTimeEngine:
 
     def __init__(self, tenant_layers: Sequence[Sequence[Layer]], batches: Sequence[int], device_index: int = 0,
                  seed: int = 42, slo_latency: float = 0.040, policy: Optional[BatchPolicy] = None,
-                 tenant_offset: int = 0, options: Optional[Dict[str, int]] = None):
+                 tenant_offset: int = 0, options: Optional[Dict[str, int]] = None,
+                 device_spec: Optional[DeviceSpec] = None):
         self.device = torch.device("cuda", device_index)
         torch.cuda.set_device(self.device)
-        self.ctx = Context(device_index, policy=policy or BatchPolicy(target_batch=0))
+        self.ctx = Context(device_index, device=device_spec, policy=policy or BatchPolicy(target_batch=0))
         for name, value in (options or {}).items():
             self.ctx.set_option(name, value)
         self.models: List[TenantModel] = []

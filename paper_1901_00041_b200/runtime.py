@@ -84,6 +84,7 @@ class Context:
                 d.batch = L.batch
                 d.conv = L.conv._c()
                 d.ldw = L.w.stride(0)
+                d.ldx = L.x.stride(2)  # NHWC pixel pitch in channels (8 selects the narrow im2col path)
             elif L.kind == "gemm":
                 d.kind = N.GM_LAYER_GEMM
                 d.gemm = L.gemm._c()

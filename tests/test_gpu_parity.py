@@ -38,6 +38,7 @@ def expect(oracle, L, relu=False):
     w = np.ascontiguousarray(L.w.float().cpu().numpy())
     if L.kind == "conv":
         c = L.conv
+        x = np.ascontiguousarray(x[..., :c.in_channels])  # narrow inputs carry zero pad channels
         P = (c.image_h + 2 * c.padding - c.kernel_h) // c.stride + 1
         Q = (c.image_w + 2 * c.padding - c.kernel_w) // c.stride + 1
         y = np.zeros((L.batch * P * Q, c.out_channels), np.float32)
@@ -56,13 +57,18 @@ def rel_err(L, ref):
     return float(np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30))
 
 
-def conv_layer(b, hw, cin, cout, r, stride, pad, relu=False, seed=0):
+def conv_layer(b, hw, cin, cout, r, stride, pad, relu=False, seed=0, pitch=0):
     from paper_1901_00041_b200.runtime import LayerBuffers
     from paper_1901_00041_b200.scheduler import ConvSpec
     g = torch.Generator().manual_seed(seed)
     K = r * r * cin
     ldw = (K + 7) // 8 * 8
-    x = (torch.rand(b, hw, hw, cin, generator=g) * 2 - 1).to(torch.bfloat16).cuda()
+    x = (torch.rand(b, hw, hw, cin, generator=g) * 2 - 1).to(torch.bfloat16)
+    if pitch:
+        xp = torch.zeros(b, hw, hw, pitch, dtype=torch.bfloat16)
+        xp[..., :cin] = x
+        x = xp
+    x = x.cuda()
     w = torch.zeros(cout, ldw, dtype=torch.bfloat16)
     w[:, :K] = (torch.randn(cout, K, generator=g) * (2.0 / K) ** 0.5).to(torch.bfloat16)
     P = (hw + 2 * pad - r) // stride + 1
@@ -95,6 +101,9 @@ CASES = {
     "conv 1x1 s1 14x14x256->512 b3 (tiled GEMM)": lambda: conv_layer(3, 14, 256, 512, 1, 1, 0),
     "conv 1x1 s2 28x28x256->512 (im2col stride)": lambda: conv_layer(1, 28, 256, 512, 1, 2, 0),
     "conv 7x7 s2 p3 stem 64x64x3->64 b2 (pre-pass)": lambda: conv_layer(2, 64, 3, 64, 7, 2, 3),
+    "conv 7x7 s2 p3 stem 64x64x3->64 b2 (narrow im2col)": lambda: conv_layer(2, 64, 3, 64, 7, 2, 3, pitch=8),
+    "conv 3x3 s2 p1 narrow 33x33x3->32": lambda: conv_layer(3, 33, 3, 32, 3, 2, 1, pitch=8),
+    "conv 3x3 s1 p1 narrow Cin=8 9x9->16 (M<128)": lambda: conv_layer(1, 9, 8, 16, 3, 1, 1, pitch=8),
     "conv 3x3 s1 7x7x512->512 b1 (M=49)": lambda: conv_layer(1, 7, 512, 512, 3, 1, 1),
     "conv 5x5 s1 p2 12x12x64->96": lambda: conv_layer(2, 12, 64, 96, 5, 1, 2),
     "conv 3x3 Cin=32 (pre-pass) 10x10x32->64": lambda: conv_layer(1, 10, 32, 64, 3, 1, 1),

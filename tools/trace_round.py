@@ -28,12 +28,16 @@ def main():
     ap.add_argument("--max-waves", type=int, default=1)
     ap.add_argument("--out", default="")
     ap.add_argument("--opt", action="append", default=[], help="runtime option name=value")
+    ap.add_argument("--tile-n", type=int, default=256)
     a = ap.parse_args()
     peaks = json.load(open("MEASURED_PEAKS.json"))
     P, BW = peaks["bf16_tflops"] * 1e12, peaks["hbm_gbs"] * 1e9
     layers = W.resnet50(224) if a.model == "resnet50" else W.MODELS[a.model]()
     opts = {kv.split("=")[0]: int(kv.split("=")[1]) for kv in a.opt}
-    eng = SpaceTimeEngine([layers] * a.tenants, [a.batch] * a.tenants, options=opts)
+    from paper_1901_00041_b200.scheduler import b200_profile
+    spec = b200_profile()
+    spec.tile_n = a.tile_n
+    eng = SpaceTimeEngine([layers] * a.tenants, [a.batch] * a.tenants, options=opts, device_spec=spec)
     rnd = eng.plan_round(BatchPolicy(target_batch=0, max_waves=a.max_waves))
     s = torch.cuda.Stream()
     for _ in range(3):
