@@ -74,8 +74,9 @@ struct Operator {
   int tenant = -1, layer = -1;
   int n_tile = 256;  // output columns per tile (<= the kernel's BN)
   bool prepass = false;
+  bool fold = false;        // the pre-pass is the row fold (kAIm2colFold)
   const void* x = nullptr;
-  void* scratch = nullptr;  // explicit-im2col rows [M, ldk]
+  void* scratch = nullptr;  // explicit-im2col rows [M, ldk], or the folded input [b, H, Q, 32]
   int64_t ldk = 0;
   void* wpad = nullptr;     // narrow-channel conv: weights repacked to 8 channels per tap
   int64_t kernel_k = 0;     // K the kernel iterates (0 = shape.k)
@@ -130,6 +131,7 @@ struct Runtime {
   bool split_k = false;      // round programs split few-tile long-K members (opt-in)
   int64_t max_splits = 4;
   int64_t narrow_min_tiles = 0;  // >0: narrow a member's N tile until it has this many tiles
+  bool row_fold = true;          // S*Cin <= 32 convs (RGB stems) use the row-folded im2col path
   bool dynamic_schedule = false;  // round programs: per-tenant ready queues (else static round-robin)
   int bn = 256;     // N tile of the super-kernel (== DeviceSpec.tile_n)
   int smem_bytes = 0;
@@ -234,6 +236,27 @@ struct Runtime {
     if (driver_version <= 13010 && bytes < 131072) reinterpret_cast<uint64_t*>(map)[1] &= ~(1ull << 21);
   }
 
+  // Folded input X' [b, H, Q, 32] as an R x 1 im2col source: vertical stride
+  // and padding from the conv, horizontal already applied by the fold.
+  void fold_map(CUtensorMap* map, const void* xf, const Conv& c, int64_t Q, int batch, int pixels) {
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(dev::kFoldC), static_cast<cuuint64_t>(Q),
+                                static_cast<cuuint64_t>(c.image_h), static_cast<cuuint64_t>(batch)};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(dev::kFoldC * 2),
+                                   static_cast<cuuint64_t>(Q * dev::kFoldC * 2),
+                                   static_cast<cuuint64_t>(c.image_h * Q * dev::kFoldC * 2)};
+    const int lower[2] = {0, static_cast<int>(-c.padding)};
+    const int upper[2] = {0, static_cast<int>(c.padding - (c.kernel_h - 1))};
+    const cuuint32_t estr[4] = {1, 1, static_cast<cuuint32_t>(c.stride), 1};
+    const CUresult r = encode_im2col(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(xf), dims, strides,
+                                     lower, upper, static_cast<cuuint32_t>(dev::kFoldC),
+                                     static_cast<cuuint32_t>(pixels), estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                     CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeIm2col(fold) failed (" + std::to_string(int(r)) + ")");
+    const int64_t bytes = static_cast<int64_t>(batch) * c.image_h * Q * dev::kFoldC * 2;
+    if (driver_version <= 13010 && bytes < 131072) reinterpret_cast<uint64_t*>(map)[1] &= ~(1ull << 21);
+  }
+
   int register_tenant(const gm_tenant_desc& t) {
     if (!t.layers || t.n_layers == 0) throw std::invalid_argument("register_tenant: tenant has no layers");
     std::vector<int> ops;
@@ -301,6 +324,32 @@ struct Runtime {
                                            static_cast<int>(c.in_channels));
           cuda_check(cudaGetLastError(), "launch pad_narrow_weights");
           cuda_check(cudaDeviceSynchronize(), "pad_narrow_weights");
+          tiled_map(&md.b, op.wpad, op.shape.n, op.kernel_k, op.kernel_k, b_box_rows(op.shape.n, op.n_tile));
+        } else if (row_fold && c.kernel_w * c.in_channels <= dev::kFoldC &&
+                   (L.ldx <= 0 || L.ldx == c.in_channels) && c.stride <= 8 && c.padding <= 127 &&
+                   c.kernel_h - 1 - c.padding <= 128) {
+          // row-folded implicit GEMM: a pre-pass folds each output column's
+          // horizontal window into a 32-channel pixel; R x 1 TMA im2col over it
+          md.a_mode = dev::kAIm2colFold;
+          op.prepass = op.fold = true;
+          const size_t xbytes = static_cast<size_t>(op.batch * c.image_h * Q * dev::kFoldC * 2);
+          cuda_check(cudaMalloc(&op.scratch, xbytes), "cudaMalloc(folded input)");
+          fold_map(&md.a, op.scratch, c, Q, op.batch, a_box_rows(op.shape.m));
+          md.pq = static_cast<int32_t>(P * Q);
+          md.q = static_cast<int32_t>(Q);
+          md.stride = static_cast<int32_t>(c.stride);
+          md.pad = static_cast<int32_t>(c.padding);
+          md.taps = static_cast<int32_t>(c.kernel_h);
+          const int rpad = static_cast<int>((c.kernel_h + dev::kFoldTaps - 1) / dev::kFoldTaps * dev::kFoldTaps);
+          op.kernel_k = static_cast<int64_t>(rpad) * dev::kFoldC;
+          cuda_check(cudaMalloc(&op.wpad, static_cast<size_t>(op.shape.n * op.kernel_k * 2)),
+                     "cudaMalloc(folded weights)");
+          dev::fold_weights<<<static_cast<int>(std::min<int64_t>((op.shape.n * op.kernel_k + 255) / 256, 4096)), 256>>>(
+              static_cast<const __nv_bfloat16*>(L.w), ldw, static_cast<__nv_bfloat16*>(op.wpad),
+              static_cast<int>(op.shape.n), static_cast<int>(c.kernel_h),
+              static_cast<int>(c.kernel_w * c.in_channels), rpad);
+          cuda_check(cudaGetLastError(), "launch fold_weights");
+          cuda_check(cudaDeviceSynchronize(), "fold_weights");
           tiled_map(&md.b, op.wpad, op.shape.n, op.kernel_k, op.kernel_k, b_box_rows(op.shape.n, op.n_tile));
         } else {
           md.a_mode = dev::kATiled;  // explicit im2col pre-pass, then GEMM
@@ -544,6 +593,56 @@ struct Runtime {
     return rounds.emplace(key, std::move(p)).first->second;
   }
 
+  // The plan's pre-passes: row folds are batched (up to 16 jobs per launch,
+  // blockIdx.y = job); explicit im2col runs one launch per operator.
+  static constexpr int kFoldJobs = 16;
+  int prepass_launches(const std::vector<int>& ops) const {
+    int folds = 0, other = 0;
+    for (int f : ops) (flat[f].fold ? folds : other) += 1;
+    return (folds + kFoldJobs - 1) / kFoldJobs + other;
+  }
+  int launch_prepasses(const Prepared& p, cudaStream_t stream, bool count) {
+    int launches = 0;
+    dev::FoldBatch fb{};
+    int nj = 0, max_pixels = 0;
+    auto flush = [&]() {
+      if (!nj) return;
+      const int gx = std::min((max_pixels + 255) / 256, sms * 8);
+      dev::fold_rows<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(nj)), 256, 0, stream>>>(fb);
+      cuda_check(cudaGetLastError(), "launch fold_rows");
+      ++launches;
+      if (count) ++n_prepasses;
+      nj = 0;
+      max_pixels = 0;
+    };
+    for (int f : p.prepass_ops) {
+      const Operator& op = flat[f];
+      const Conv& c = op.conv;
+      const int H = static_cast<int>(c.image_h), W = static_cast<int>(c.image_w), Cin = static_cast<int>(c.in_channels);
+      const int R = static_cast<int>(c.kernel_h), S = static_cast<int>(c.kernel_w);
+      const int st = static_cast<int>(c.stride), pad = static_cast<int>(c.padding), ldk = static_cast<int>(op.ldk);
+      const int P = static_cast<int>((c.image_h + 2 * c.padding - c.kernel_h) / c.stride + 1);
+      const int Q = static_cast<int>((c.image_w + 2 * c.padding - c.kernel_w) / c.stride + 1);
+      if (op.fold) {
+        fb.job[nj] = dev::FoldJob{static_cast<const __nv_bfloat16*>(op.x), static_cast<__nv_bfloat16*>(op.scratch),
+                                  op.batch, H, W, Cin, S, st, pad, Q};
+        max_pixels = std::max(max_pixels, op.batch * H * Q);
+        if (++nj == kFoldJobs) flush();
+        continue;
+      }
+      const int64_t total = op.shape.m * (op.ldk / 8);
+      const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, int64_t(sms) * 16));
+      dev::im2col_prepass<<<grid, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(op.x),
+                                                     static_cast<__nv_bfloat16*>(op.scratch), op.batch, H, W, Cin, R,
+                                                     S, st, pad, P, Q, ldk);
+      cuda_check(cudaGetLastError(), "launch im2col_prepass");
+      ++launches;
+      if (count) ++n_prepasses;
+    }
+    flush();
+    return launches;
+  }
+
   // Enqueue one plan: explicit-im2col pre-passes (if any), then the
   // super-kernel.  `ev` (optional) brackets the super-kernel with external
   // event records so a captured graph can time it.  `count` is false while
@@ -551,26 +650,12 @@ struct Runtime {
   int launch(Prepared& p, cudaStream_t stream, bool count = true, cudaEvent_t ev_begin = nullptr,
              cudaEvent_t ev_end = nullptr, uint64_t* trace = nullptr) {
     int launches = 0;
-    for (int f : p.prepass_ops) {
-      const Operator& op = flat[f];
-      const Conv& c = op.conv;
-      const int P = static_cast<int>((c.image_h + 2 * c.padding - c.kernel_h) / c.stride + 1);
-      const int Q = static_cast<int>((c.image_w + 2 * c.padding - c.kernel_w) / c.stride + 1);
-      const int64_t total = op.shape.m * (op.ldk / 8);
-      const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, int64_t(sms) * 16));
-      dev::im2col_prepass<<<grid, 256, 0, stream>>>(
-          static_cast<const __nv_bfloat16*>(op.x), static_cast<__nv_bfloat16*>(op.scratch), op.batch,
-          static_cast<int>(c.image_h), static_cast<int>(c.image_w), static_cast<int>(c.in_channels),
-          static_cast<int>(c.kernel_h), static_cast<int>(c.kernel_w), static_cast<int>(c.stride),
-          static_cast<int>(c.padding), P, Q, static_cast<int>(op.ldk));
-      cuda_check(cudaGetLastError(), "launch im2col_prepass");
-      ++launches;
-      if (count) ++n_prepasses;
-    }
+    // counters first: the pre-pass -> super-kernel edge stays kernel-to-kernel (PDL)
     if (p.counters)
       cuda_check(cudaMemsetAsync(p.counters, 0, static_cast<size_t>(p.n_counters + p.nq) * sizeof(uint32_t), stream),
                  "reset round counters");
     if (ev_begin) cuda_check(cudaEventRecordWithFlags(ev_begin, stream, cudaEventRecordExternal), "event record");
+    launches += launch_prepasses(p, stream, count);
     const int grid = std::max(1, std::min(p.n_tiles, sms));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
@@ -763,6 +848,8 @@ int gm_ctx_set_option(gm_ctx* ctx, const char* name, int64_t value) {
     rt.dynamic_schedule = value != 0;  // applies to round programs prepared afterwards
   } else if (n == "narrow_min_tiles") {
     rt.narrow_min_tiles = value;  // applies to tenants registered afterwards
+  } else if (n == "row_fold") {
+    rt.row_fold = value != 0;  // applies to tenants registered afterwards
   } else {
     throw std::invalid_argument("unknown option " + n);
   }
@@ -843,9 +930,10 @@ int gm_members_launch_count(gm_ctx* ctx, const int32_t* tenants, const int32_t* 
   GM_API_BEGIN
   if (n == 0 || !tenants || !layers || !launches) throw std::invalid_argument("empty dispatch");
   Runtime& rt = runtime_of(ctx);
-  int l = 1;
-  for (size_t j = 0; j < n; ++j) l += rt.op_of(tenants[j], layers[j]).prepass ? 1 : 0;
-  *launches = l;
+  std::vector<int> ops;
+  for (size_t j = 0; j < n; ++j)
+    if (rt.op_of(tenants[j], layers[j]).prepass) ops.push_back(rt.flat_index(tenants[j], layers[j]));
+  *launches = 1 + rt.prepass_launches(ops);
   GM_API_END
 }
 

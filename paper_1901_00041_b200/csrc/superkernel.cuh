@@ -52,10 +52,17 @@ struct Cfg {
 // A-operand modes: 2-D tiled box; TMA im2col (C_in % 64 == 0: one 128 B
 // channel block per k-block, SW128); narrow-channel TMA im2col (input pixel
 // pitch of 8 channels: eight 16 B tap columns per k-block, SWIZZLE_NONE).
-enum : int32_t { kATiled = 0, kAIm2col = 1, kAIm2colNarrow = 2 };
+// Row-folded mode (S * C_in <= 32, e.g. the 7x7 RGB stem): a pre-pass folds
+// each output column's horizontal window into one 32-channel "pixel"
+// (X'[b, h, q, s*C_in + c]); the conv becomes R x 1 with vertical stride,
+// two 64 B (SW64) TMA im2col columns per k-block.
+enum : int32_t { kATiled = 0, kAIm2col = 1, kAIm2colNarrow = 2, kAIm2colFold = 3 };
 constexpr int kNarrowC = 8;                     // channels per pixel of a narrow-im2col input
 constexpr int kNarrowTaps = kBK / kNarrowC;     // filter taps per k-block
 constexpr int kNarrowTapBytes = kBM * kNarrowC * 2;  // one tap column: 128 pixels x 16 B
+constexpr int kFoldC = 32;                      // channels per folded pixel (64 B)
+constexpr int kFoldTaps = kBK / kFoldC;         // filter rows per k-block
+constexpr int kFoldTapBytes = kBM * kFoldC * 2;  // one filter-row column: 128 pixels x 64 B
 
 // Device-resident descriptor of one registered (tenant, layer) operator.
 struct alignas(128) MemberDesc {
@@ -209,6 +216,17 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr) {
   return d;
 }
 
+// SWIZZLE_64B K-major descriptor: 64 B rows, SBO = 512 B between 8-row groups.
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1u) << 16;
+  d |= static_cast<uint64_t>(512u >> 4) << 32;
+  d |= static_cast<uint64_t>(1u) << 46;
+  d |= static_cast<uint64_t>(4u) << 61;
+  return d;
+}
+
 // SWIZZLE_NONE K-major descriptor: 8-row x 16 B core matrices contiguous,
 // SBO = 128 B to the next 8 rows, LBO = one narrow tap column to the next 8
 // K elements.
@@ -354,7 +372,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m0 = te.m_tile * kBM;
         const int n0 = te.n_tile * md->n_tile;
         const bool narrow = md->a_mode == kAIm2colNarrow;
-        const bool im2col = md->a_mode == kAIm2col || narrow;
+        const bool fold = md->a_mode == kAIm2colFold;
+        const bool im2col = md->a_mode != kATiled;
         int img = 0, h0 = 0, w0 = 0, c_blocks = 1, s_taps = 1;
         if (im2col) {
           img = m0 / md->pq;
@@ -362,13 +381,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int p0 = rem / md->q;
           const int q0 = rem - p0 * md->q;
           h0 = p0 * md->stride - md->pad;
-          w0 = q0 * md->stride - md->pad;
+          w0 = fold ? q0 : q0 * md->stride - md->pad;  // folded columns are already strided
           c_blocks = md->c_blocks;
           s_taps = md->s_taps;
         }
         auto load_a = [&](int kb, uint32_t st) {
           uint8_t* a_dst = ring + st * C::kStageBytes;
-          if (narrow) {
+          if (fold) {
+            // two filter rows; a row past R re-reads row 0 (its weights are zero)
+#pragma unroll
+            for (int j = 0; j < kFoldTaps; ++j) {
+              const int r = kb * kFoldTaps + j;
+              tma_load_im2col(a_dst + j * kFoldTapBytes, &md->a, &full[st], 0, w0, h0, img, 0,
+                              static_cast<uint16_t>(r < md->taps ? r : 0));
+            }
+          } else if (narrow) {
             // eight 16 B tap columns; taps past R*S load an out-of-range image
             // so TMA zero-fills them (the weights there are zero too)
 #pragma unroll 1
@@ -466,6 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int k_blocks = te.kb_end ? te.kb_end : md->k_blocks;
         const uint32_t idesc = md->idesc;
         const bool a_narrow = md->a_mode == kAIm2colNarrow;
+        const bool a_fold = md->a_mode == kAIm2colFold;
         mbar_wait(&acc_empty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -478,9 +506,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             // advance 16 bf16 along K: 32 B inside the 128 B swizzle atom, or
-            // two narrow tap columns
+            // two narrow tap columns, or 32 B inside a folded 64 B row
             const uint64_t a_desc =
-                a_narrow ? interleave_desc(a_addr + k * 2 * kNarrowTapBytes) : sw128_desc(a_addr + k * 32);
+                a_fold     ? sw64_desc(a_addr + (k >> 1) * kFoldTapBytes + (k & 1) * 32)
+                : a_narrow ? interleave_desc(a_addr + k * 2 * kNarrowTapBytes)
+                           : sw128_desc(a_addr + k * 32);
             umma_bf16(d_tmem, a_desc, sw128_desc(b_addr + k * 32), idesc, (kb != kb_lo || k != 0) ? 1u : 0u);
           }
           umma_commit(&empty[stage]);  // frees the smem stage once these MMAs retire
@@ -711,6 +741,67 @@ __global__ void pad_narrow_weights(const __nv_bfloat16* __restrict__ src, int64_
     const int tap = rem / kNarrowC;
     const int c = rem - tap * kNarrowC;
     dst[i] = c < cin ? src[static_cast<int64_t>(o) * ldw + tap * cin + c] : __float2bfloat16(0.f);
+  }
+}
+
+// Row-folded weights: dst[o, r*kFoldC + j] = src[o, r*S*Cin + j] for
+// j < S*Cin and r < R, zero elsewhere (rows r in [R, rpad) pad K to whole k-blocks).
+__global__ void fold_weights(const __nv_bfloat16* __restrict__ src, int64_t ldw, __nv_bfloat16* __restrict__ dst,
+                             int cout, int R, int sc, int rpad) {
+  const int row = rpad * kFoldC;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cout * row; i += gridDim.x * blockDim.x) {
+    const int o = i / row;
+    const int rem = i - o * row;
+    const int r = rem / kFoldC, j = rem - r * kFoldC;
+    dst[i] = (r < R && j < sc) ? src[static_cast<int64_t>(o) * ldw + r * sc + j] : __float2bfloat16(0.f);
+  }
+}
+
+// Row-fold pre-pass: X'[b, h, q, j] = X[b, h, q*stride - pad + j / Cin, j % Cin]
+// for j < S*Cin (zero outside the image and for j >= S*Cin).  One thread per
+// folded pixel (64 B: four 16 B stores); blockIdx.y selects the job.
+struct FoldJob {
+  const __nv_bfloat16* x;
+  __nv_bfloat16* out;
+  int batch, H, W, Cin, S, stride, pad, Q;
+};
+struct FoldBatch {
+  FoldJob job[16];
+};
+
+__global__ void __launch_bounds__(256) fold_rows(const __grid_constant__ FoldBatch fb) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const FoldJob& j = fb.job[blockIdx.y];
+  const unsigned short* xs = reinterpret_cast<const unsigned short*>(j.x);
+  const int sc = j.S * j.Cin;
+  const int total = j.batch * j.H * j.Q;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int q = i % j.Q;
+    const int bh = i / j.Q;  // b * H + h
+    const int iw0 = q * j.stride - j.pad;
+    const unsigned short* row = xs + static_cast<int64_t>(bh) * j.W * j.Cin;
+    uint32_t packed[kFoldC / 2];
+    int s = 0, c = 0;
+#pragma unroll
+    for (int e = 0; e < kFoldC; ++e) {
+      uint32_t v = 0;
+      if (e < sc) {
+        const int iw = iw0 + s;
+        if (iw >= 0 && iw < j.W) v = __ldg(row + iw * j.Cin + c);
+        if (++c == j.Cin) {
+          c = 0;
+          ++s;
+        }
+      }
+      if (e & 1)
+        packed[e >> 1] |= v << 16;
+      else
+        packed[e >> 1] = v;
+    }
+    uint4* dst = reinterpret_cast<uint4*>(j.out + static_cast<int64_t>(i) * kFoldC);
+#pragma unroll
+    for (int u = 0; u < kFoldC / 8; ++u)
+      dst[u] = make_uint4(packed[4 * u], packed[4 * u + 1], packed[4 * u + 2], packed[4 * u + 3]);
   }
 }
 

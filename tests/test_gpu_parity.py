@@ -100,7 +100,10 @@ CASES = {
     "conv 3x3 s2 p1 28x28x64->128": lambda: conv_layer(1, 28, 64, 128, 3, 2, 1),
     "conv 1x1 s1 14x14x256->512 b3 (tiled GEMM)": lambda: conv_layer(3, 14, 256, 512, 1, 1, 0),
     "conv 1x1 s2 28x28x256->512 (im2col stride)": lambda: conv_layer(1, 28, 256, 512, 1, 2, 0),
-    "conv 7x7 s2 p3 stem 64x64x3->64 b2 (pre-pass)": lambda: conv_layer(2, 64, 3, 64, 7, 2, 3),
+    "conv 7x7 s2 p3 stem 64x64x3->64 b2 (row fold)": lambda: conv_layer(2, 64, 3, 64, 7, 2, 3),
+    "conv 7x7 s2 p3 row fold odd 37x37x3->64": lambda: conv_layer(1, 37, 3, 64, 7, 2, 3),
+    "conv 3x3 s2 p1 row fold 33x33x3->32 b3": lambda: conv_layer(3, 33, 3, 32, 3, 2, 1),
+    "conv 3x3 s1 p1 row fold Cin=8 9x9->16 (M<128)": lambda: conv_layer(1, 9, 8, 16, 3, 1, 1),
     "conv 7x7 s2 p3 stem 64x64x3->64 b2 (narrow im2col)": lambda: conv_layer(2, 64, 3, 64, 7, 2, 3, pitch=8),
     "conv 3x3 s2 p1 narrow 33x33x3->32": lambda: conv_layer(3, 33, 3, 32, 3, 2, 1, pitch=8),
     "conv 3x3 s1 p1 narrow Cin=8 9x9->16 (M<128)": lambda: conv_layer(1, 9, 8, 16, 3, 1, 1, pitch=8),
@@ -213,7 +216,7 @@ def test_modes_compute_identical_bits(oracle):
     check_engine(eng, oracle)
 
 
-@pytest.mark.parametrize("options", [{"split_k": 1}, {"narrow_min_tiles": 32}, {"pdl": 0},
+@pytest.mark.parametrize("options", [{"split_k": 1}, {"narrow_min_tiles": 32}, {"pdl": 0}, {"row_fold": 0},
                                      {"split_k": 1, "max_splits": 8, "narrow_min_tiles": 64}])
 def test_execution_options_keep_results(oracle, options):
     eng = small_engine(tenants=2, batch=4, options=options)
