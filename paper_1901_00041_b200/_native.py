@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libgpumux_b200.so")
+LIB_PATH = os.environ.get("GM_LIB_PATH") or os.path.join(_HERE, "_lib", "libgpumux_b200.so")
 
 GM_OK, GM_EINVAL, GM_ECONFIG, GM_EOOM, GM_EINTERNAL, GM_ECUDA, GM_ERANGE, GM_ENODEV = range(8)
 GM_LAYER_GEMM, GM_LAYER_CONV = 0, 1
