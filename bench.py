@@ -40,6 +40,9 @@ def parse_args():
     ap.add_argument("--table1", default="2,4,8,10,16,20,32,40,64,80,100,120",
                     help="R values of the conv2_2 microbench sweep ('' to skip)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--serve-seconds", type=float, default=1.5,
+                    help="real-clock serving run per load point (0 = skip the serving section)")
+    ap.add_argument("--slo", type=float, default=0.040, help="query SLO (s) of the serving run")
     ap.add_argument("--max-waves", type=int, default=1,
                     help="planner wave cap per super-kernel (1 = reference plan parity; >1 = b200 extension)")
     return ap.parse_args()
@@ -360,6 +363,11 @@ def run_ours(args):
     h2d = sum(t.numel() * t.element_size() for t in h_in)
     d2h = sum(t.numel() * t.element_size() for t in h_out)
 
+    # Real-clock serving (dynamic batcher + round programs + CUDA-event completions)
+    serving = None
+    if args.serve_seconds > 0:
+        serving = run_serving(args, layers, local, rank, world, dist if world > 1 else None)
+
     # Table-1 analogue: R tenants x conv2_2 (256,128,1152) b1, L2 flushed between steps
     table1 = None
     if args.table1 and rank == 0 and world == 1:
@@ -433,7 +441,9 @@ def run_ours(args):
         },
         "packed_over_space_only": results["space_only"]["ms_per_step"] / packed["ms_per_step"],
         "packed_over_time_only": results["time_only"]["ms_per_step"] / packed["ms_per_step"],
-        "p99_query_latency_ms": p99,
+        "p99_query_latency_ms": serving["poisson_50pct"]["p99_ms"] if serving else p99,
+        "p99_note": ("real-clock serving, Poisson arrivals at 50% of saturated load, SLO-bound dynamic batching "
+                     "(see serving)") if serving else "round-program step time",
         "roofline": {
             "bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s", "frac": achieved_gbs / hbm,
             "traffic": traffic, "algorithmic_bytes_per_launch": bytes_round,
@@ -457,10 +467,62 @@ def run_ours(args):
         line["cpu_baseline"] = cpu
     if table1 is not None:
         line["table1"] = table1
+    if serving is not None:
+        line["serving"] = serving
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def run_serving(args, layers, local, rank, world, dist):
+    """Real-clock serving of the same tenants through gm_serve (the B200 form of
+    run_space_time): closed loop at saturation, then Poisson arrivals at 50% and
+    80% of the saturated query rate.  Query latency = completion - arrival
+    (queueing + batching wait + execution); p99 by nearest rank over every
+    rank's samples (one all-gather after the run, off the hot path)."""
+    from paper_1901_00041_b200.engine import ServeTenant, ServingEngine
+    T = args.tenants
+
+    def session(rate, conc):
+        specs = [ServeTenant(layers, max_batch=args.batch, rate_qps=rate, concurrency=conc, slo_latency=args.slo)
+                 for _ in range(T)]
+        eng = ServingEngine(specs, device_index=local, tenant_offset=rank * T)
+        eng.serve(duration=0.3, warmup=0.1, seed=1)  # prewarm plans + device tables, JIT of the path
+        if dist is not None:
+            dist.barrier()
+        r = eng.serve(duration=args.serve_seconds, warmup=min(0.2, args.serve_seconds / 4), seed=42 + rank)
+        lat = r.latencies_ms
+        if dist is not None:
+            gathered = [None] * world
+            dist.all_gather_object(gathered, lat)
+            lat = [x for g in gathered for x in g]
+            tot = [None] * world
+            dist.all_gather_object(tot, (r.stats["tflops"], r.stats["qps"], r.stats["slo_violation_frac"],
+                                         r.stats["queries"]))
+        else:
+            tot = [(r.stats["tflops"], r.stats["qps"], r.stats["slo_violation_frac"], r.stats["queries"])]
+        q = sum(t[3] for t in tot)
+        out = {"tflops": sum(t[0] for t in tot), "qps": sum(t[1] for t in tot),
+               "p50_ms": nearest_rank(lat, 50.0) if lat else None, "p99_ms": nearest_rank(lat, 99.0) if lat else None,
+               "max_ms": max(lat) if lat else None,
+               "slo_violation_frac": sum(t[2] * t[3] for t in tot) / q if q else None,
+               "queries": q, "rounds_per_gpu": r.stats["rounds"],
+               "mean_queries_per_round": r.stats["mean_queries_per_round"],
+               "mean_round_ms": r.stats["mean_round_ms"], "plan_misses_on_clock": r.stats["plan_misses"],
+               "evicted": r.stats["evicted"]}
+        del eng
+        return out
+
+    sat = session(0.0, args.batch)
+    per_tenant_qps = sat["qps"] / (T * world)
+    res = {"api": "ServingEngine.serve -> gm_serve (C++ real-clock loop, round-program dispatch)",
+           "slo_ms": args.slo * 1e3, "max_batch": args.batch, "seconds_per_point": args.serve_seconds,
+           "closed_loop": sat}
+    for frac in (0.5, 0.8):
+        res[f"poisson_{int(frac * 100)}pct"] = dict(session(frac * per_tenant_qps, 1),
+                                                   rate_qps_per_tenant=frac * per_tenant_qps)
+    return res
 
 
 def run_table1(torch, rs, dev, stream):

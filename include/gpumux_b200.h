@@ -403,6 +403,52 @@ void gm_graph_destroy(gm_graph* g);
 int gm_ctx_launch_stats(const gm_ctx* ctx, int64_t* superkernels, int64_t* prepasses,
                         int64_t* tiles);
 
+/* ---------------------------------------------------------------- serving
+ * Real-clock space-time serving on one GPU: the B200 form of the reference's
+ * run_space_time loop (proj/src/sim.cpp:398-581) with query arrivals, the
+ * dynamic batcher's size/age/SLO triggers (form_batches, scheduler.cpp:166-197),
+ * one round program per dispatch, CUDA-event completions feeding
+ * record_latency / detect_stragglers / evict (scheduler.cpp:214-271).
+ * A logical tenant registers one runtime tenant per batch variant (same
+ * buffers, sized for the largest batch); a dispatch serves up to the largest
+ * batch of its pending queries with the smallest variant that holds them. */
+typedef struct gm_serve_tenant {
+  int32_t n_variants;
+  const int32_t* variant_tenant;  /* runtime tenant index per variant */
+  const int32_t* variant_batch;   /* queries (images / sequences) per variant */
+  double rate_qps;                /* Poisson arrivals per second; 0 = closed loop */
+  int32_t concurrency;            /* closed loop: queries outstanding */
+  int32_t reserved0;
+  double slo_latency;             /* seconds; a query meets its SLO if latency <= slo */
+  int64_t flops_per_query;        /* algorithmic FLOPs of one query (credited at completion) */
+} gm_serve_tenant;
+
+typedef struct gm_serve_config {
+  double duration;   /* seconds of real time (arrivals stop at the end) */
+  double warmup;     /* seconds excluded from the statistics */
+  double max_wait;   /* batcher age trigger in seconds; < 0 = the ctx policy's max_wait */
+  uint64_t seed;     /* Poisson streams: per tenant, hashed from the seed */
+  int32_t depth;     /* rounds in flight (1 = the reference's single dispatch in flight) */
+  int32_t prewarm;   /* > 0: plan + upload every formable member set before the clock starts
+                        (fails if there are more than this many); 0 = plan on first use */
+  uint64_t stream;   /* cudaStream_t */
+} gm_serve_config;
+
+typedef struct gm_serve_stats {
+  int64_t queries;             /* completed inside (warmup, duration] */
+  int64_t rounds;              /* dispatches (round-program launches) */
+  int64_t dispatched_queries;
+  double window_s, tflops, qps;
+  double p50_ms, p99_ms, max_ms, mean_ms;  /* query latency: completion - arrival, nearest rank */
+  double slo_violation_frac;
+  double mean_queries_per_round, mean_round_ms;
+  int64_t plan_hits, plan_misses;          /* member-set plan / device-table cache */
+  int32_t evicted, reserved0;
+} gm_serve_stats;
+
+int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, const gm_serve_config* cfg,
+             gm_serve_stats* out, double* latencies_ms, size_t cap, size_t* n_lat);
+
 #ifdef __cplusplus
 }  /* extern "C" */
 #endif

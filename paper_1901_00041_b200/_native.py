@@ -106,6 +106,26 @@ class gm_tenant_desc(C.Structure):
 
 
 P = C.POINTER
+class gm_serve_tenant(C.Structure):
+    _fields_ = [("n_variants", C.c_int32), ("variant_tenant", C.POINTER(C.c_int32)),
+                ("variant_batch", C.POINTER(C.c_int32)), ("rate_qps", C.c_double), ("concurrency", C.c_int32),
+                ("reserved0", C.c_int32), ("slo_latency", C.c_double), ("flops_per_query", C.c_int64)]
+
+
+class gm_serve_config(C.Structure):
+    _fields_ = [("duration", C.c_double), ("warmup", C.c_double), ("max_wait", C.c_double), ("seed", C.c_uint64),
+                ("depth", C.c_int32), ("prewarm", C.c_int32), ("stream", C.c_uint64)]
+
+
+class gm_serve_stats(C.Structure):
+    _fields_ = [("queries", C.c_int64), ("rounds", C.c_int64), ("dispatched_queries", C.c_int64),
+                ("window_s", C.c_double), ("tflops", C.c_double), ("qps", C.c_double), ("p50_ms", C.c_double),
+                ("p99_ms", C.c_double), ("max_ms", C.c_double), ("mean_ms", C.c_double),
+                ("slo_violation_frac", C.c_double), ("mean_queries_per_round", C.c_double),
+                ("mean_round_ms", C.c_double), ("plan_hits", C.c_int64), ("plan_misses", C.c_int64),
+                ("evicted", C.c_int32), ("reserved0", C.c_int32)]
+
+
 _SIGS = {
     "gm_last_error": (C.c_char_p, []),
     "gm_abi_version": (C.c_int, []),
@@ -194,6 +214,8 @@ _SIGS = {
     "gm_graph_kernel_times": (C.c_int, [C.c_void_p, P(C.c_float), C.c_size_t, P(C.c_size_t)]),
     "gm_graph_destroy": (None, [C.c_void_p]),
     "gm_ctx_launch_stats": (C.c_int, [C.c_void_p, P(C.c_int64), P(C.c_int64), P(C.c_int64)]),
+    "gm_serve": (C.c_int, [C.c_void_p, P(gm_serve_tenant), C.c_size_t, P(gm_serve_config), P(gm_serve_stats),
+                           P(C.c_double), C.c_size_t, P(C.c_size_t)]),
 }
 
 _lib = None

@@ -5,8 +5,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cmath>
 #include <cstring>
+#include <deque>
+#include <map>
+#include <random>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -1170,3 +1176,296 @@ int gm_ctx_launch_stats(const gm_ctx* ctx, int64_t* superkernels, int64_t* prepa
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Real-clock serving: the B200 form of run_space_time (proj/src/sim.cpp:398-581).
+//
+// Queries arrive per logical tenant (Poisson, or closed loop: a query re-arrives
+// when the previous one completes).  The batcher keeps per-tenant pending
+// queues and triggers a dispatch on the reference's three conditions
+// (form_batches, scheduler.cpp:166-197): size (pending queries >= target,
+// auto = live tenants as in sim.cpp:516-523), age (oldest >= max_wait) or SLO
+// (some pending query's deadline minus the predicted round time has passed).
+// A dispatch takes up to one max-batch of queries per tenant (the tenant's
+// dynamic batch: the smallest registered batch variant that holds them) and
+// runs them as one round program: the reference planner orders and packs every
+// layer of every member (plan_round), one persistent super-kernel launch
+// executes it with device-side layer dependencies.  Plans and device tables are
+// cached per member set (the SuperKernelCache meaning on B200).  Completions
+// come from CUDA events; each member tenant's monitor is fed the round's device
+// time (execution time, sim.cpp:475-476), then stragglers are detected and
+// evicted (terminal, scheduler.cpp:225-271).
+namespace gmb {
+namespace {
+
+struct ServeRound {
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<std::pair<int, std::vector<int64_t>>> members;  // (logical tenant, arrival ns of its queries)
+  int64_t dispatch_ns = 0;
+};
+
+int64_t since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace
+}  // namespace gmb
+
+extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, const gm_serve_config* cfg,
+                        gm_serve_stats* out, double* latencies_ms, size_t cap, size_t* n_lat) {
+  GM_API_BEGIN
+  if (!tenants || n == 0 || !cfg || !out) throw std::invalid_argument("null argument");
+  Runtime& rt = runtime_of(ctx);
+  cuda_check(cudaSetDevice(rt.device), "cudaSetDevice");
+  if (cfg->prewarm < 0) throw std::invalid_argument("serve: prewarm cap must be >= 0");
+  if (cfg->duration <= 0 || cfg->warmup < 0 || cfg->warmup >= cfg->duration)
+    throw std::invalid_argument("serve: need 0 <= warmup < duration");
+  const int depth = std::max(1, cfg->depth);
+  const int64_t duration_ns = to_ns(cfg->duration), warmup_ns = to_ns(cfg->warmup);
+  const int64_t max_wait_ns = to_ns(cfg->max_wait >= 0 ? cfg->max_wait : ctx->pol.max_wait);
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(cfg->stream);
+
+  struct T {
+    std::vector<std::pair<int, int>> variants;  // (batch, runtime tenant), ascending batch
+    double rate = 0, slo = 0.1;
+    int conc = 0;
+    int64_t flops = 0;
+    std::deque<int64_t> pending;
+    int64_t next_arrival = 0;
+    std::mt19937_64 rng;
+    bool live = true;
+  };
+  std::vector<T> ts(n);
+  std::vector<Health> health(n);
+  for (size_t i = 0; i < n; ++i) {
+    const gm_serve_tenant& st = tenants[i];
+    if (st.n_variants < 1 || !st.variant_tenant || !st.variant_batch)
+      throw std::invalid_argument("serve: tenant needs at least one batch variant");
+    for (int v = 0; v < st.n_variants; ++v) {
+      rt.op_of(st.variant_tenant[v], 0);
+      if (st.variant_batch[v] < 1) throw std::invalid_argument("serve: variant batch must be >= 1");
+      ts[i].variants.emplace_back(st.variant_batch[v], st.variant_tenant[v]);
+    }
+    std::sort(ts[i].variants.begin(), ts[i].variants.end());
+    if (st.rate_qps < 0 || (st.rate_qps == 0 && st.concurrency < 1))
+      throw std::invalid_argument("serve: tenant needs a Poisson rate > 0 or a closed-loop concurrency >= 1");
+    ts[i].rate = st.rate_qps;
+    ts[i].conc = st.concurrency;
+    ts[i].slo = st.slo_latency > 0 ? st.slo_latency : 0.1;
+    ts[i].flops = st.flops_per_query;
+    // per-tenant stream: splitmix-chained seed (hash, never XOR)
+    uint64_t h = cfg->seed + 0x9E3779B97F4A7C15ull * (i + 1);
+    h = (h ^ (h >> 30)) * 0xBF58476D1CE4E5B9ull;
+    h = (h ^ (h >> 27)) * 0x94D049BB133111EBull;
+    ts[i].rng.seed(h ^ (h >> 31));
+    health[i].tenant = static_cast<int>(i);
+    health[i].alpha = ctx->det.ewma_alpha;
+  }
+  auto draw = [](T& t) {
+    std::exponential_distribution<double> e(t.rate);
+    return static_cast<int64_t>(std::llround(e(t.rng) * 1e9));
+  };
+  for (T& t : ts) {
+    if (t.rate > 0)
+      t.next_arrival = draw(t);
+    else
+      for (int c = 0; c < t.conc; ++c) t.pending.push_back(0);
+  }
+
+  // plan + device-table cache per member set
+  struct Cached {
+    Prepared* prep;
+    double planned_s;
+  };
+  std::map<std::vector<int>, Cached> cache;
+  int64_t plan_hits = 0, plan_misses = 0;
+  auto plan_members = [&](const std::vector<int>& key) {
+    std::vector<RoundTenant> round;
+    for (int id : key) {
+      RoundTenant rtn;
+      rtn.tenant = id;
+      for (int f : rt.tenant_ops[id]) rtn.layers.push_back(rt.flat[f].shape);
+      rtn.slo_ns = to_ns(rt.tenant_slo[id]);
+      round.push_back(std::move(rtn));
+    }
+    RoundResult res = plan_round(round, 0, ctx->pol, ctx->dev, ctx->cache.c, ctx->next_request_id);
+    std::vector<std::vector<int>> plans;
+    TimeNs end = 0;
+    for (RoundDispatch& d : res.dispatches) {
+      plans.push_back(members_of(rt, d.plan));
+      end = std::max(end, d.end);
+    }
+    return cache.emplace(key, Cached{&rt.prepare_round(plans), to_seconds(end)}).first;
+  };
+  // Pre-warm: plan and upload every member set the batcher can form (one
+  // variant or none per tenant), so no dispatch pays the miss path on the
+  // clock -- the steady state the reference's cache converges to
+  // ("cache super-kernels as workloads stabilize").
+  if (cfg->prewarm) {
+    size_t combos = 1;
+    for (const T& t : ts) combos = std::min<size_t>(combos * (t.variants.size() + 1), 1u << 20);
+    if (combos - 1 > static_cast<size_t>(cfg->prewarm))
+      throw std::invalid_argument("serve: " + std::to_string(combos - 1) + " member sets exceed the prewarm cap");
+    std::vector<size_t> pick(n, 0);
+    for (size_t c = 1; c < combos; ++c) {
+      size_t x = c;
+      std::vector<int> key;
+      for (size_t i = 0; i < n; ++i) {
+        const size_t k = x % (ts[i].variants.size() + 1);
+        x /= ts[i].variants.size() + 1;
+        if (k) key.push_back(ts[i].variants[k - 1].second);
+      }
+      if (!cache.count(key)) plan_members(key);
+    }
+  }
+  std::vector<cudaEvent_t> pool;
+  auto get_event = [&]() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+  };
+  std::deque<ServeRound> inflight;
+  std::vector<double> lat_ms;
+  int64_t queries = 0, rounds = 0, dispatched_queries = 0, slo_miss = 0, flops_done = 0;
+  double round_ms_sum = 0;
+  double predicted_s = 0;  // EWMA of measured round device time (SLO trigger)
+  int evicted = 0;
+  const auto t0 = std::chrono::steady_clock::now();
+
+  for (;;) {
+    int64_t now = since(t0);
+    // arrivals (stop admitting at the end of the window)
+    for (T& t : ts) {
+      if (!t.live || t.rate <= 0) continue;
+      while (t.next_arrival <= now && t.next_arrival < duration_ns) {
+        t.pending.push_back(t.next_arrival);
+        t.next_arrival += draw(t);
+      }
+    }
+    // completions, in dispatch order
+    while (!inflight.empty() && cudaEventQuery(inflight.front().ev1) == cudaSuccess) {
+      ServeRound r = std::move(inflight.front());
+      inflight.pop_front();
+      const int64_t done = since(t0);
+      float ms = 0;
+      cuda_check(cudaEventElapsedTime(&ms, r.ev0, r.ev1), "cudaEventElapsedTime");
+      pool.push_back(r.ev0);
+      pool.push_back(r.ev1);
+      round_ms_sum += ms;
+      predicted_s = rounds == 1 && predicted_s == 0 ? ms * 1e-3 : 0.8 * predicted_s + 0.2 * ms * 1e-3;
+      for (auto& [ti, arr] : r.members) {
+        T& t = ts[ti];
+        for (int64_t a : arr) {
+          const double l = (done - a) * 1e-6;
+          if (a >= warmup_ns && done <= duration_ns) {
+            lat_ms.push_back(l);
+            ++queries;
+            flops_done += t.flops;
+            if (l * 1e-3 > t.slo) ++slo_miss;
+          }
+          if (t.rate <= 0 && t.live && done < duration_ns) t.pending.push_back(done);  // closed loop
+        }
+        if (!health[ti].evicted) observe(health[ti], ms * 1e-3);
+      }
+      if (ctx->det.evict_stragglers) {
+        for (int s : stragglers(health, ctx->det.threshold_ratio, ctx->det.min_observations)) {
+          health[s].evicted = true;  // terminal (scheduler.cpp:225-244): pending queries are cancelled
+          ts[s].live = false;
+          ts[s].pending.clear();
+          ++evicted;
+        }
+      }
+      now = since(t0);
+    }
+    size_t pending = 0, live = 0;
+    int64_t oldest = INT64_MAX;
+    bool slo_due = false;
+    const int64_t pred_ns = to_ns(predicted_s * (1.0 + ctx->pol.slo_safety_margin));
+    for (T& t : ts) {
+      if (!t.live) continue;
+      ++live;
+      pending += t.pending.size();
+      if (!t.pending.empty()) {
+        oldest = std::min(oldest, t.pending.front());
+        if (t.pending.front() + to_ns(t.slo) - pred_ns <= now) slo_due = true;
+      }
+    }
+    if (now >= duration_ns && inflight.empty() && (pending == 0 || now >= duration_ns + to_ns(1.0))) break;
+    if (static_cast<int>(inflight.size()) < depth && pending > 0) {
+      const size_t target = ctx->pol.target_batch > 0 ? static_cast<size_t>(ctx->pol.target_batch) : live;
+      if (pending >= target || now - oldest >= max_wait_ns || slo_due || now >= duration_ns) {
+        // dynamic batch per tenant: up to its largest variant, the smallest variant that holds them
+        std::vector<int> key;
+        ServeRound r;
+        for (size_t i = 0; i < n; ++i) {
+          T& t = ts[i];
+          if (!t.live || t.pending.empty()) continue;
+          const int bmax = t.variants.back().first;
+          const int q = static_cast<int>(std::min<size_t>(t.pending.size(), static_cast<size_t>(bmax)));
+          int rtid = t.variants.back().second;
+          for (auto& [b, id] : t.variants)
+            if (b >= q) {
+              rtid = id;
+              break;
+            }
+          key.push_back(rtid);
+          std::vector<int64_t> arr(t.pending.begin(), t.pending.begin() + q);
+          t.pending.erase(t.pending.begin(), t.pending.begin() + q);
+          dispatched_queries += q;
+          r.members.emplace_back(static_cast<int>(i), std::move(arr));
+        }
+        auto it = cache.find(key);
+        if (it == cache.end()) {
+          ++plan_misses;
+          it = plan_members(key);
+        } else {
+          ++plan_hits;
+        }
+        if (predicted_s == 0) predicted_s = it->second.planned_s;
+        r.ev0 = get_event();
+        r.ev1 = get_event();
+        r.dispatch_ns = now;
+        cuda_check(cudaEventRecord(r.ev0, stream), "cudaEventRecord");
+        rt.launch(*it->second.prep, stream);
+        cuda_check(cudaEventRecord(r.ev1, stream), "cudaEventRecord");
+        inflight.push_back(std::move(r));
+        ++rounds;
+        continue;
+      }
+    }
+    // nothing to do right now: yield briefly (completion polling granularity)
+    std::this_thread::yield();
+  }
+  cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+  for (cudaEvent_t e : pool) cudaEventDestroy(e);
+
+  std::memset(out, 0, sizeof(*out));
+  out->queries = queries;
+  out->rounds = rounds;
+  out->dispatched_queries = dispatched_queries;
+  out->window_s = cfg->duration - cfg->warmup;
+  out->tflops = static_cast<double>(flops_done) / out->window_s / 1e12;
+  out->qps = static_cast<double>(queries) / out->window_s;
+  if (!lat_ms.empty()) {
+    out->p50_ms = nearest_rank(lat_ms, 50.0);
+    out->p99_ms = nearest_rank(lat_ms, 99.0);
+    out->max_ms = *std::max_element(lat_ms.begin(), lat_ms.end());
+    double sum = 0;
+    for (double l : lat_ms) sum += l;
+    out->mean_ms = sum / static_cast<double>(lat_ms.size());
+    out->slo_violation_frac = static_cast<double>(slo_miss) / static_cast<double>(lat_ms.size());
+  }
+  out->mean_queries_per_round = rounds ? static_cast<double>(dispatched_queries) / rounds : 0;
+  out->mean_round_ms = rounds ? round_ms_sum / rounds : 0;
+  out->plan_hits = plan_hits;
+  out->plan_misses = plan_misses;
+  out->evicted = evicted;
+  if (n_lat) *n_lat = lat_ms.size();
+  if (latencies_ms && cap) std::copy(lat_ms.begin(), lat_ms.begin() + std::min(cap, lat_ms.size()), latencies_ms);
+  GM_API_END
+}

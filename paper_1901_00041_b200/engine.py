@@ -16,6 +16,7 @@ and replays the cached graph while the sequence is unchanged.
 from __future__ import annotations
 
 import ctypes as C
+from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence, Tuple
 
 import torch
@@ -23,7 +24,7 @@ import torch
 from . import _native as N
 from ._native import check, lib
 from .runtime import Context, LayerBuffers, Round
-from .scheduler import BatchPolicy, DeviceSpec
+from .scheduler import BatchPolicy, DeviceSpec, GemmShape
 from .workload import Layer
 
 _MASK = (1 << 64) - 1
@@ -210,3 +211,94 @@ class SpaceTimeEngine:
                 h.copy_(m.query_output, non_blocking=True)
         stream.synchronize()
         return rnd
+
+
+# --------------------------------------------------------------------------- serving
+@dataclass
+class ServeTenant:
+    """One logical tenant of a serving session (gm_serve_tenant).
+
+    ``rate_qps`` > 0: Poisson arrivals; 0: closed loop with ``concurrency``
+    queries outstanding.  The dynamic batcher serves up to ``max_batch``
+    queries per dispatch with the smallest registered variant in ``batches``
+    that holds them (default: powers of two up to ``max_batch``)."""
+    layers: Sequence[Layer]
+    max_batch: int = 8
+    rate_qps: float = 0.0
+    concurrency: int = 1
+    slo_latency: float = 0.040
+    batches: Optional[Sequence[int]] = None
+
+
+@dataclass
+class ServeResult:
+    stats: Dict[str, float]
+    latencies_ms: List[float] = field(default_factory=list)
+
+
+def _variant(buf: LayerBuffers, max_batch: int, b: int) -> LayerBuffers:
+    """The same device buffers viewed as a batch-b operator (the first b queries)."""
+    if buf.kind == "conv":
+        return LayerBuffers("conv", buf.x, buf.w, buf.y, conv=buf.conv, batch=b, relu=buf.relu)
+    g = buf.gemm
+    return LayerBuffers("gemm", buf.x, buf.w, buf.y, gemm=GemmShape(g.m // max_batch * b, g.n, g.k), relu=buf.relu)
+
+
+class ServingEngine:
+    """Real-clock space-time serving on one GPU (gm_serve).
+
+    Each logical tenant owns device buffers for its largest batch and one
+    registered runtime tenant per batch variant sharing them; ``serve`` runs
+    the native serving loop (arrivals, dynamic batcher, round-program
+    dispatch, CUDA-event completions, straggler monitor) for ``duration``
+    seconds and returns throughput and query-latency percentiles."""
+
+    def __init__(self, tenants: Sequence[ServeTenant], device_index: int = 0, seed: int = 42,
+                 policy: Optional[BatchPolicy] = None, options: Optional[Dict[str, int]] = None,
+                 device_spec: Optional[DeviceSpec] = None, tenant_offset: int = 0):
+        self.device = torch.device("cuda", device_index)
+        torch.cuda.set_device(self.device)
+        self.ctx = Context(device_index, device=device_spec, policy=policy or BatchPolicy(target_batch=0))
+        for name, value in (options or {}).items():
+            self.ctx.set_option(name, value)
+        self.specs = list(tenants)
+        self.models: List[TenantModel] = []
+        self._variants: List[List[Tuple[int, int]]] = []
+        for i, spec in enumerate(self.specs):
+            bmax = spec.max_batch
+            batches = sorted(set(spec.batches or [b for b in (1, 2, 4, 8, 16, 32, 64) if b < bmax] + [bmax]))
+            if batches[-1] != bmax or batches[0] < 1:
+                raise ValueError("batch variants must be >= 1 and end at max_batch")
+            m = TenantModel(spec.layers, bmax, seed, tenant_offset + i, self.device)
+            self.models.append(m)
+            vs = []
+            for b in batches:
+                bufs = [_variant(buf, bmax, b) for buf in m.buffers]
+                vs.append((b, self.ctx.register_tenant(bufs, slo_latency=spec.slo_latency,
+                                                       tenant_id=f"t{tenant_offset + i}/b{b}")))
+            self._variants.append(vs)
+
+    def flops_per_query(self, i: int) -> int:
+        return sum(L.flops(1) for L in self.specs[i].layers)
+
+    def serve(self, duration: float, warmup: float = 0.1, max_wait: float = -1.0, depth: int = 1,
+              seed: int = 42, stream: Optional[torch.cuda.Stream] = None, prewarm: int = 4096) -> ServeResult:
+        n = len(self.specs)
+        arr = (N.gm_serve_tenant * n)()
+        keep = []
+        for i, (spec, vs) in enumerate(zip(self.specs, self._variants)):
+            tid = (C.c_int32 * len(vs))(*[t for _, t in vs])
+            bat = (C.c_int32 * len(vs))(*[b for b, _ in vs])
+            keep += [tid, bat]
+            arr[i] = N.gm_serve_tenant(len(vs), tid, bat, float(spec.rate_qps), int(spec.concurrency), 0,
+                                       float(spec.slo_latency), self.flops_per_query(i))
+        s = stream or torch.cuda.Stream(self.device)
+        cfg = N.gm_serve_config(float(duration), float(warmup), float(max_wait), int(seed), int(depth),
+                                int(prewarm), int(s.cuda_stream))
+        out = N.gm_serve_stats()
+        cap = 1 << 20
+        lat = (C.c_double * cap)()
+        nl = C.c_size_t()
+        check(lib().gm_serve(self.ctx.handle, arr, n, C.byref(cfg), C.byref(out), lat, cap, C.byref(nl)))
+        stats = {f: getattr(out, f) for f, _ in N.gm_serve_stats._fields_ if not f.startswith("reserved")}
+        return ServeResult(stats, [lat[i] for i in range(min(nl.value, cap))])
