@@ -194,7 +194,11 @@ class CpuPort:
         self.tensors = []
         for L in layers:
             s = L.gemm_shape(batch)
-            if L.kind == "conv":
+            if L.kind == "dwconv":
+                c = L.conv
+                x = rng.uniform(-1, 1, (batch, c.image_h, c.image_w, c.in_channels)).astype(np.float32)
+                w = rng.uniform(-1, 1, (c.out_channels, c.kernel_h, c.kernel_w)).astype(np.float32)
+            elif L.kind == "conv":
                 c = L.conv
                 x = rng.uniform(-1, 1, (batch, c.image_h, c.image_w, c.in_channels)).astype(np.float32)
                 w = rng.uniform(-1, 1, (c.out_channels, c.kernel_h, c.kernel_w, c.in_channels)).astype(np.float32)
@@ -207,7 +211,9 @@ class CpuPort:
 
     def run_pass(self):
         for L, x, w in self.tensors:
-            if L.kind == "conv":
+            if L.kind == "dwconv":
+                self.cpu_conv.dwconv2d_nhwc(x, w, L.conv.stride, L.conv.padding)
+            elif L.kind == "conv":
                 self.cpu_conv.conv2d_nhwc(x, w, L.conv.stride, L.conv.padding)
             else:
                 self.cpu_conv.gemm_nt(x, w)

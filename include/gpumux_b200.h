@@ -277,7 +277,10 @@ void gm_sim_trace_destroy(gm_sim_trace* t);
 
 /* ---- B200 runtime: tenants, super-kernel dispatch ------------------------ */
 
-enum gm_layer_kind { GM_LAYER_GEMM = 0, GM_LAYER_CONV = 1 };
+/* DWCONV: depthwise conv (groups = channels; MobileNet-v2).  The planner sees
+ * the reference's model of it, a K = R*S GEMM (proj/src/workload.cpp:66):
+ * (b*P*Q, C, R*S); w is [C, ldw] with R*S taps per row; R*S <= 9, C % 4 == 0. */
+enum gm_layer_kind { GM_LAYER_GEMM = 0, GM_LAYER_CONV = 1, GM_LAYER_DWCONV = 2 };
 
 /* One operator of a tenant's graph, with its device buffers (bf16).
  *   CONV: x = NHWC [batch, H, W, Cin]; w = KRSC [Cout, R, S, Cin] with a row

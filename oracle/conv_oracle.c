@@ -104,3 +104,35 @@ void oracle_im2col_nhwc(const float* x, float* out, int64_t batch, int64_t H, in
     (void)K;
   }
 }
+
+/* Depthwise conv (groups = C): y[b, p, q, c] = sum_{r,s} x[b, p*st - pad + r, q*st - pad + s, c] * w[c*ldw + r*S + s].
+ * The reference models it only as a K = R*S GEMM (proj/src/workload.cpp:66: (M, C, 9)); the
+ * semantics restated here are torchvision's MobileNet-v2 depthwise 3x3 (conv2d, groups = C). */
+void oracle_dwconv2d_nhwc(const float* x, const float* w, float* y, int64_t batch, int64_t H, int64_t W, int64_t C,
+                          int64_t R, int64_t S, int64_t stride, int64_t pad, int64_t ldw, int32_t relu) {
+  const int64_t P = (H + 2 * pad - R) / stride + 1;
+  const int64_t Q = (W + 2 * pad - S) / stride + 1;
+  if (ldw <= 0) ldw = R * S;
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int64_t b = 0; b < batch; ++b) {
+    for (int64_t p = 0; p < P; ++p) {
+      for (int64_t q = 0; q < Q; ++q) {
+        float* out = y + ((b * P + p) * Q + q) * C;
+        for (int64_t c = 0; c < C; ++c) {
+          double acc = 0.0;
+          for (int64_t r = 0; r < R; ++r) {
+            const int64_t ih = p * stride - pad + r;
+            if (ih < 0 || ih >= H) continue;
+            for (int64_t s = 0; s < S; ++s) {
+              const int64_t iw = q * stride - pad + s;
+              if (iw < 0 || iw >= W) continue;
+              acc += (double)x[((b * H + ih) * W + iw) * C + c] * (double)w[c * ldw + r * S + s];
+            }
+          }
+          float v = (float)acc;
+          out[c] = (relu && v < 0.0f) ? 0.0f : v;
+        }
+      }
+    }
+  }
+}

@@ -32,6 +32,21 @@ def conv2d_nhwc(x: np.ndarray, w: np.ndarray, stride: int, pad: int) -> np.ndarr
     return (a @ w.reshape(O, R * S * Cin).T).reshape(b, P, Q, O)
 
 
+def dwconv2d_nhwc(x: np.ndarray, w: np.ndarray, stride: int, pad: int) -> np.ndarray:
+    """Depthwise (groups = C): x [b, H, W, C], w [C, R, S] -> y [b, P, Q, C] (torchvision MobileNet-v2)."""
+    b, H, W, C = x.shape
+    _, R, S = w.shape
+    if pad:
+        x = np.pad(x, ((0, 0), (pad, pad), (pad, pad), (0, 0)))
+    P = (H + 2 * pad - R) // stride + 1
+    Q = (W + 2 * pad - S) // stride + 1
+    y = np.zeros((b, P, Q, C), np.float32)
+    for r in range(R):
+        for s in range(S):
+            y += x[:, r:r + stride * P:stride, s:s + stride * Q:stride, :] * w[:, r, s]
+    return y
+
+
 def gemm_nt(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     return a @ b.T
 

@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GM_LIB_PATH") or os.path.join(_HERE, "_lib", "libgpumux_b200.so")
 
 GM_OK, GM_EINVAL, GM_ECONFIG, GM_EOOM, GM_EINTERNAL, GM_ECUDA, GM_ERANGE, GM_ENODEV = range(8)
-GM_LAYER_GEMM, GM_LAYER_CONV = 0, 1
+GM_LAYER_GEMM, GM_LAYER_CONV, GM_LAYER_DWCONV = 0, 1, 2
 GM_MODE_PACKED, GM_MODE_TIME_ONLY, GM_MODE_SPACE_ONLY = 0, 1, 2
 
 

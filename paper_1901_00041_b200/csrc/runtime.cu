@@ -364,6 +364,41 @@ struct Runtime {
           cuda_check(cudaMalloc(&op.scratch, static_cast<size_t>(op.shape.m * op.ldk * 2)), "cudaMalloc(im2col)");
           tiled_map(&md.a, op.scratch, op.shape.m, K, op.ldk, a_box_rows(op.shape.m));
         }
+      } else if (L.kind == GM_LAYER_DWCONV) {
+        // depthwise conv: the reference models it as a K = R*S GEMM
+        // (proj/src/workload.cpp:66); executed as the super-kernel's CUDA-core
+        // tile type (one filter per channel, no tensor-core path)
+        op.conv = to_conv(L.conv);
+        op.batch = L.batch < 1 ? 1 : L.batch;
+        const Conv& c = op.conv;
+        if (c.in_channels != c.out_channels) throw std::invalid_argument("register_tenant: depthwise needs Cin == Cout");
+        if (c.kernel_h * c.kernel_w > dev::kDwMaxTaps)
+          throw std::invalid_argument("register_tenant: depthwise filter larger than 3x3");
+        if (c.in_channels % 4 != 0) throw std::invalid_argument("register_tenant: depthwise channels must be a multiple of 4");
+        const int64_t taps = c.kernel_h * c.kernel_w;
+        const int64_t ldw = L.ldw > 0 ? L.ldw : taps;
+        if (ldw < taps) throw std::invalid_argument("register_tenant: ldw < R*S");
+        if (!aligned16(L.x)) throw std::invalid_argument("conv input must be 16-byte aligned");
+        const int64_t P = (c.image_h + 2 * c.padding - c.kernel_h) / c.stride + 1;
+        const int64_t Q = (c.image_w + 2 * c.padding - c.kernel_w) / c.stride + 1;
+        if (P < 1 || Q < 1) throw std::invalid_argument("conv output dims must be positive");
+        op.shape = Shape{op.batch * P * Q, c.out_channels, taps};
+        op.n_tile = dev::kDwTileC;
+        md.a_mode = dev::kDepthwise;
+        md.dx = static_cast<const __nv_bfloat16*>(L.x);
+        md.dw = static_cast<const __nv_bfloat16*>(L.w);
+        md.dy = static_cast<__nv_bfloat16*>(L.y);
+        md.h_in = static_cast<int32_t>(c.image_h);
+        md.w_in = static_cast<int32_t>(c.image_w);
+        md.ch = static_cast<int32_t>(c.in_channels);
+        md.r_taps = static_cast<int32_t>(taps);
+        md.ldw = static_cast<int32_t>(ldw);
+        md.s_taps = static_cast<int32_t>(c.kernel_w);
+        md.stride = static_cast<int32_t>(c.stride);
+        md.pad = static_cast<int32_t>(c.padding);
+        md.pq = static_cast<int32_t>(P * Q);
+        md.q = static_cast<int32_t>(Q);
+        md.images = op.batch;
       } else if (L.kind == GM_LAYER_GEMM) {
         op.shape = to_shape(L.gemm);
         op.n_tile = pick_n_tile(op.shape, bn, narrow_min_tiles);
@@ -514,7 +549,8 @@ struct Runtime {
           const int chunk = (kb + splits - 1) / splits;
           splits = (kb + chunk - 1) / chunk;
         }
-        targets.push_back(static_cast<uint32_t>(mt * nt * 4));  // 4 epilogue warps arrive per output tile
+        // 4 epilogue warps arrive per output tile (8 for a depthwise tile: all of them compute it)
+        targets.push_back(static_cast<uint32_t>(mt * nt * (op.kind == GM_LAYER_DWCONV ? 8 : 4)));
         for (int64_t a = 0; a < mt; ++a)
           for (int64_t b = 0; b < nt; ++b) {
             if (splits == 1) {

@@ -56,7 +56,13 @@ struct Cfg {
 // each output column's horizontal window into one 32-channel "pixel"
 // (X'[b, h, q, s*C_in + c]); the conv becomes R x 1 with vertical stride,
 // two 64 B (SW64) TMA im2col columns per k-block.
-enum : int32_t { kATiled = 0, kAIm2col = 1, kAIm2colNarrow = 2, kAIm2colFold = 3 };
+enum : int32_t { kATiled = 0, kAIm2col = 1, kAIm2colNarrow = 2, kAIm2colFold = 3, kDepthwise = 4 };
+// Depthwise conv (MobileNet-v2) is a CUDA-core tile type inside the same
+// persistent kernel (tensor cores do not apply: one filter per channel).  Its
+// tiles skip the TMA/MMA pipeline; the eight epilogue warps compute them
+// directly (16 output pixels each x kDwTileC channels, 4 channels per lane).
+constexpr int kDwTileC = 128;
+constexpr int kDwMaxTaps = 9;
 constexpr int kNarrowC = 8;                     // channels per pixel of a narrow-im2col input
 constexpr int kNarrowTaps = kBK / kNarrowC;     // filter taps per k-block
 constexpr int kNarrowTapBytes = kBM * kNarrowC * 2;  // one tap column: 128 pixels x 16 B
@@ -82,6 +88,12 @@ struct alignas(128) MemberDesc {
   int32_t n_tile;       // output columns per tile (<= BN): narrower for few-tile members
   int32_t taps;         // narrow im2col: R*S filter taps
   int32_t images;       // narrow im2col: batch (an out-of-range image zero-fills a box)
+  // depthwise members: raw operands and geometry (x NHWC [b, H, W, C],
+  // w [C, ldw] with R*S taps per row, y [b*P*Q, C])
+  const __nv_bfloat16* dx;
+  const __nv_bfloat16* dw;
+  __nv_bfloat16* dy;
+  int32_t h_in, w_in, ch, r_taps, ldw;
 };
 
 // Device tile-table entry; `member` is the registered slot index.
@@ -277,6 +289,53 @@ __device__ __forceinline__ uint32_t pack_bf16(uint32_t lo_bits, uint32_t hi_bits
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Depthwise tile (CUDA cores): epilogue warp `ew` (0..7) computes output
+// pixels [m_tile*128 + ew*16, +16) x channels [n_tile*kDwTileC + 4*lane, +4)
+// in fp32 from bf16 NHWC input and [C, R*S] filters; one 8-byte load per tap
+// and pixel per lane (a warp reads 256 contiguous bytes of channels).
+__device__ __forceinline__ void depthwise_tile(const MemberDesc* __restrict__ md, const TileEntry& te, int ew, int lane) {
+  const int M = md->m, C = md->ch, H = md->h_in, W = md->w_in;
+  const int c = te.n_tile * kDwTileC + lane * 4;
+  if (c >= C) return;
+  const int taps = md->r_taps, S = md->s_taps, st = md->stride, pad = md->pad, PQ = md->pq, Q = md->q;
+  const int R = taps / S;
+  float wv[4][kDwMaxTaps];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int k = 0; k < kDwMaxTaps; ++k)
+      wv[j][k] = k < taps ? __bfloat162float(md->dw[static_cast<int64_t>(c + j) * md->ldw + k]) : 0.f;
+  const int m_base = te.m_tile * kBM + ew * 16;
+  for (int i = 0; i < 16; ++i) {
+    const int m = m_base + i;
+    if (m >= M) break;
+    const int b = m / PQ;
+    const int rem = m - b * PQ;
+    const int p = rem / Q;
+    const int q = rem - p * Q;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < kDwMaxTaps; ++k) {
+      if (k >= taps) break;
+      const int r = k / S, s = k - r * S;
+      const int ih = p * st - pad + r, iw = q * st - pad + s;
+      if (ih < 0 || ih >= H || iw < 0 || iw >= W) continue;
+      const uint2 raw = __ldcg(reinterpret_cast<const uint2*>(md->dx + ((static_cast<int64_t>(b) * H + ih) * W + iw) * C + c));
+      const __nv_bfloat162 x01 = *reinterpret_cast<const __nv_bfloat162*>(&raw.x);
+      const __nv_bfloat162 x23 = *reinterpret_cast<const __nv_bfloat162*>(&raw.y);
+      acc[0] = fmaf(__low2float(x01), wv[0][k], acc[0]);
+      acc[1] = fmaf(__high2float(x01), wv[1][k], acc[1]);
+      acc[2] = fmaf(__low2float(x23), wv[2][k], acc[2]);
+      acc[3] = fmaf(__high2float(x23), wv[3][k], acc[3]);
+    }
+    (void)R;
+    uint2 o;
+    o.x = pack_bf16(__float_as_uint(acc[0]), __float_as_uint(acc[1]), md->relu);
+    o.y = pack_bf16(__float_as_uint(acc[2]), __float_as_uint(acc[3]), md->relu);
+    *reinterpret_cast<uint2*>(md->dy + static_cast<int64_t>(m) * C + c) = o;
+  }
+}
+
 // ---------------------------------------------------------------- kernel
 
 template <int BN>
@@ -364,6 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (t < 0) break;
         const TileEntry te = tiles[t];
         const MemberDesc* md = slots + te.member;
+        if (md->a_mode == kDepthwise) continue;  // computed by the epilogue warps
         prefetch_tmap(&md->a);
         prefetch_tmap(&md->b);
         const int kb_lo = te.kb_end ? te.kb_begin : 0;
@@ -489,6 +549,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (t < 0) break;
         const TileEntry te = tiles[t];
         const MemberDesc* md = slots + te.member;
+        if (md->a_mode == kDepthwise) continue;  // no accumulator: the epilogue warps compute it
         const int kb_lo = te.kb_end ? te.kb_begin : 0;
         const int k_blocks = te.kb_end ? te.kb_end : md->k_blocks;
         const uint32_t idesc = md->idesc;
@@ -587,7 +648,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0, buf = 0;
     int issued = 0;
     uint32_t qslot = 0, qphase = 0;
-    for (int local = 0;; ++local) {
+    int mma_local = 0;     // accumulator tiles seen (depthwise tiles have none)
+    bool dw_gated = false;  // PDL wait done before this warp's first depthwise tile
+    for (;;) {
       int t = 0;
       if (lane == 0) {
         mbar_wait(&tq_full[qslot], qphase);
@@ -600,9 +663,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         qphase ^= 1;
       }
       if (t < 0) break;
-      if ((local & 1) != static_cast<int>(acc)) continue;
       const TileEntry te = tiles[t];
       const MemberDesc* md = slots + te.member;
+      if (md->a_mode == kDepthwise) {
+        // all eight epilogue warps share the tile; gate on the PDL
+        // prerequisite and the tenant's previous layer like the A producer
+        if (!dw_gated) {
+          asm volatile("griddepcontrol.wait;" ::: "memory");
+          dw_gated = true;
+        }
+        if (te.dep >= 0) {
+          if (lane == 0)
+            while (ld_acquire(counters + te.dep) < targets[te.dep]) __nanosleep(32);
+          __syncwarp();
+        }
+        if (trace && warp == 4 && lane == 0) {
+          const uint64_t now = globaltimer();
+          for (int j = 0; j < 5; ++j) trace[6 * t + j] = now;  // no load / MMA phases
+        }
+        depthwise_tile(md, te, warp - 4, lane);
+        __syncwarp();
+        if (trace && warp == 4 && lane == 0) trace[6 * t + 5] = globaltimer();
+        if (te.done >= 0 && lane == 0) {
+          __threadfence();
+          atomicAdd(counters + te.done, 1u);
+        }
+        continue;
+      }
+      const bool mine = (mma_local & 1) == static_cast<int>(acc);
+      ++mma_local;
+      if (!mine) continue;
       const int m0 = te.m_tile * kBM + quarter * 32;
       const int n0 = te.n_tile * md->n_tile;
       const int cols = min(md->n_tile, md->n - n0);

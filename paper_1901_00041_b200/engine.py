@@ -85,14 +85,19 @@ class TenantModel:
         self.batch = batch
         self.buffers: List[LayerBuffers] = []
         for li, L in enumerate(self.layers):
-            if L.kind == "dwconv":
-                raise NotImplementedError(f"{L.name}: depthwise conv has no tensor-core tile type yet")
             s = L.gemm_shape(batch)
             g_in = torch.Generator(device=device).manual_seed(mix64(seed, tenant, li, KIND_INPUT))
             g_w = torch.Generator(device=device).manual_seed(mix64(seed, tenant, li, KIND_WEIGHT))
             kpad = (s.k + 7) // 8 * 8
             w = torch.zeros(s.n, kpad, device=device, dtype=torch.bfloat16)
             w[:, : s.k] = (torch.randn(s.n, s.k, device=device, generator=g_w) * (2.0 / s.k) ** 0.5).to(torch.bfloat16)
+            if L.kind == "dwconv":
+                c = L.conv
+                x = (torch.rand(batch, c.image_h, c.image_w, c.in_channels, device=device, generator=g_in) * 2 - 1)
+                w = (torch.randn(s.n, s.k, device=device, generator=g_w) * (2.0 / s.k) ** 0.5).to(torch.bfloat16)
+                y = torch.empty(s.m, s.n, device=device, dtype=torch.bfloat16)
+                self.buffers.append(LayerBuffers("dwconv", x.to(torch.bfloat16), w, y, conv=c, batch=batch))
+                continue
             if L.kind == "conv":
                 c = L.conv
                 x = (torch.rand(batch, c.image_h, c.image_w, c.in_channels, device=device, generator=g_in) * 2 - 1)
@@ -238,8 +243,8 @@ class ServeResult:
 
 def _variant(buf: LayerBuffers, max_batch: int, b: int) -> LayerBuffers:
     """The same device buffers viewed as a batch-b operator (the first b queries)."""
-    if buf.kind == "conv":
-        return LayerBuffers("conv", buf.x, buf.w, buf.y, conv=buf.conv, batch=b, relu=buf.relu)
+    if buf.kind in ("conv", "dwconv"):
+        return LayerBuffers(buf.kind, buf.x, buf.w, buf.y, conv=buf.conv, batch=b, relu=buf.relu)
     g = buf.gemm
     return LayerBuffers("gemm", buf.x, buf.w, buf.y, gemm=GemmShape(g.m // max_batch * b, g.n, g.k), relu=buf.relu)
 

@@ -23,6 +23,7 @@ class LayerBuffers:
     """One operator of a tenant graph with its device tensors (bf16).
 
     conv: x NHWC [b, H, W, Cin], w [Cout, ldw] (KRSC rows), y NHWC [b, P, Q, Cout]
+    dwconv: x NHWC [b, H, W, C], w [C, ldw] (R*S taps per row), y NHWC [b, P, Q, C]
     gemm: x [M, ldx], w [N, ldw], y [M, N]
     """
     kind: str
@@ -85,6 +86,11 @@ class Context:
                 d.conv = L.conv._c()
                 d.ldw = L.w.stride(0)
                 d.ldx = L.x.stride(2)  # NHWC pixel pitch in channels (8 selects the narrow im2col path)
+            elif L.kind == "dwconv":
+                d.kind = N.GM_LAYER_DWCONV
+                d.batch = L.batch
+                d.conv = L.conv._c()
+                d.ldw = L.w.stride(0)
             elif L.kind == "gemm":
                 d.kind = N.GM_LAYER_GEMM
                 d.gemm = L.gemm._c()

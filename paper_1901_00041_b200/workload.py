@@ -7,7 +7,7 @@
 * The model builders return executable operator lists with real
   ConvSpecs (torchvision layer definitions), which the reference lacks
   (SURVEY §8(d)): ResNet-18/50, VGG-16, MobileNet-v2 (depthwise layers are
-  tagged ``dwconv`` and are not yet executable on this path), BERT-base
+  tagged ``dwconv``: the super-kernel's CUDA-core depthwise tile type), BERT-base
   projection/FFN GEMMs.  Convs are listed in forward order; a bottleneck's
   downsample follows its conv3, a basic block's follows its conv2.
 """
@@ -89,15 +89,15 @@ class Layer:
     k: int = 0
 
     def gemm_shape(self, batch: int = 1) -> GemmShape:
-        if self.kind in ("conv", "dwconv"):
+        if self.kind == "dwconv":  # the reference's model of a depthwise conv: K = R*S (workload.cpp:66)
+            s = batch_inputs(im2col_gemm_dims(self.conv), batch)
+            return GemmShape(s.m, s.n, self.conv.kernel_h * self.conv.kernel_w)
+        if self.kind == "conv":
             return batch_inputs(im2col_gemm_dims(self.conv), batch)
         return GemmShape(self.rows * batch, self.n, self.k)
 
     def flops(self, batch: int = 1) -> int:
-        if self.kind == "dwconv":  # per-channel filter: K = R*S, not R*S*Cin
-            s = self.gemm_shape(batch)
-            return 2 * s.m * s.n * self.conv.kernel_h * self.conv.kernel_w
-        s = self.gemm_shape(batch)
+        s = self.gemm_shape(batch)  # dwconv: per-channel filter, K = R*S
         return 2 * s.m * s.n * s.k
 
     def compulsory_bytes(self, batch: int = 1, elem: int = 2) -> int:

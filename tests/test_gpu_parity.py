@@ -25,6 +25,7 @@ def oracle():
     i = ctypes.c_int64
     lib.oracle_conv2d_nhwc.argtypes = [f, f, f] + [i] * 10 + [ctypes.c_int32]
     lib.oracle_gemm_nt.argtypes = [f, f, f, i, i, i, i, i, ctypes.c_int32]
+    lib.oracle_dwconv2d_nhwc.argtypes = [f, f, f] + [i] * 9 + [ctypes.c_int32]
     return lib
 
 
@@ -36,7 +37,14 @@ def expect(oracle, L, relu=False):
     """fp32 oracle output of one LayerBuffers (reads the device tensors' bf16 values)."""
     x = np.ascontiguousarray(L.x.float().cpu().numpy())
     w = np.ascontiguousarray(L.w.float().cpu().numpy())
-    if L.kind == "conv":
+    if L.kind == "dwconv":
+        c = L.conv
+        P = (c.image_h + 2 * c.padding - c.kernel_h) // c.stride + 1
+        Q = (c.image_w + 2 * c.padding - c.kernel_w) // c.stride + 1
+        y = np.zeros((L.batch * P * Q, c.out_channels), np.float32)
+        oracle.oracle_dwconv2d_nhwc(fp(x), fp(w), fp(y), L.batch, c.image_h, c.image_w, c.in_channels, c.kernel_h,
+                                    c.kernel_w, c.stride, c.padding, w.shape[1], int(relu))
+    elif L.kind == "conv":
         c = L.conv
         x = np.ascontiguousarray(x[..., :c.in_channels])  # narrow inputs carry zero pad channels
         P = (c.image_h + 2 * c.padding - c.kernel_h) // c.stride + 1
@@ -76,6 +84,18 @@ def conv_layer(b, hw, cin, cout, r, stride, pad, relu=False, seed=0, pitch=0):
     return LayerBuffers("conv", x, w.cuda(), y, conv=ConvSpec(hw, hw, r, r, cin, cout, stride, pad), batch=b, relu=relu)
 
 
+def dw_layer(b, hw, c, stride, relu=False, seed=0):
+    """Depthwise 3x3 pad 1 (MobileNet-v2): the super-kernel's CUDA-core tile type."""
+    from paper_1901_00041_b200.runtime import LayerBuffers
+    from paper_1901_00041_b200.scheduler import ConvSpec
+    g = torch.Generator().manual_seed(seed)
+    x = (torch.rand(b, hw, hw, c, generator=g) * 2 - 1).to(torch.bfloat16).cuda()
+    w = (torch.randn(c, 9, generator=g) * (2.0 / 9) ** 0.5).to(torch.bfloat16).cuda()
+    P = (hw + 2 - 3) // stride + 1
+    y = torch.full((b * P * P, c), float("nan"), dtype=torch.bfloat16, device="cuda")
+    return LayerBuffers("dwconv", x, w, y, conv=ConvSpec(hw, hw, 3, 3, c, c, stride, 1), batch=b, relu=relu)
+
+
 def gemm_layer(m, n, k, relu=False, seed=0):
     from paper_1901_00041_b200.runtime import LayerBuffers
     from paper_1901_00041_b200.scheduler import GemmShape
@@ -111,6 +131,10 @@ CASES = {
     "conv 5x5 s1 p2 12x12x64->96": lambda: conv_layer(2, 12, 64, 96, 5, 1, 2),
     "conv 3x3 Cin=32 (pre-pass) 10x10x32->64": lambda: conv_layer(1, 10, 32, 64, 3, 1, 1),
     "conv 3x3 relu": lambda: conv_layer(1, 12, 64, 64, 3, 1, 1, relu=True),
+    "dwconv 3x3 s1 14x14x96 b2": lambda: dw_layer(2, 14, 96, 1),
+    "dwconv 3x3 s2 15x15x144 (odd, stride 2)": lambda: dw_layer(1, 15, 144, 2),
+    "dwconv 3x3 s1 56x56x32 b3 (many tiles)": lambda: dw_layer(3, 56, 32, 1),
+    "dwconv 3x3 s1 7x7x200 relu (partial channel tile)": lambda: dw_layer(1, 7, 200, 1, relu=True),
 }
 
 
@@ -213,6 +237,27 @@ def test_modes_compute_identical_bits(oracle):
     for other in outs[1:]:
         for a, b in zip(outs[0], other):
             assert torch.equal(a, b)
+    check_engine(eng, oracle)
+
+
+def test_heterogeneous_models_round_program(oracle):
+    """BASELINE configs[2]'s model mix in one round program: MobileNet-v2
+    (depthwise CUDA-core tiles + 1x1 tensor-core tiles), ResNet-18 and VGG-16
+    tenants with different layer lists, per-tenant device-side layer deps."""
+    from paper_1901_00041_b200 import workload as W
+    from paper_1901_00041_b200.engine import SpaceTimeEngine
+    eng = SpaceTimeEngine([W.mobilenet_v2(64, classifier=False), W.resnet18(64), W.vgg16(32, classifier=False)],
+                          [2, 2, 1])
+    rnd = eng.plan_round()
+    clear(eng)
+    s = torch.cuda.Stream()
+    rnd.launch_round(s.cuda_stream)
+    torch.cuda.synchronize()
+    check_engine(eng, oracle)
+    # and the same members one launch per formed super-kernel
+    clear(eng)
+    rnd.launch(s.cuda_stream)
+    torch.cuda.synchronize()
     check_engine(eng, oracle)
 
 

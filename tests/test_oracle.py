@@ -34,6 +34,7 @@ def oracle():
     lib.oracle_gemm_nt.argtypes = [f, f, f, i, i, i, i, i, ctypes.c_int32]
     lib.oracle_round_bf16.argtypes = [f, i]
     lib.oracle_im2col_nhwc.argtypes = [f, f] + [i] * 9
+    lib.oracle_dwconv2d_nhwc.argtypes = [f, f, f] + [i] * 9 + [ctypes.c_int32]
     return lib
 
 
@@ -77,6 +78,21 @@ def test_conv_oracle_relu_and_im2col(oracle):
     y = cols[:, :K] @ w.reshape(8, K).T
     np.testing.assert_allclose(y.reshape(2, 10, 10, 8), run_conv(oracle, x, w, 1, 1), rtol=1e-5, atol=1e-5)
     assert not cols[:, K:].any()
+
+
+@pytest.mark.parametrize("b,hw,c,stride", [(1, 14, 96, 1), (2, 15, 144, 2), (3, 7, 32, 1), (1, 112, 32, 1)])
+def test_dwconv_oracle_matches_torch_groups(oracle, b, hw, c, stride):
+    rng = np.random.default_rng(b * 100 + hw + c)
+    x = rng.uniform(-1, 1, (b, hw, hw, c)).astype(np.float32)
+    w = rng.standard_normal((c, 3, 3)).astype(np.float32)
+    P = (hw + 2 - 3) // stride + 1
+    y = np.zeros((b, P, P, c), np.float32)
+    oracle.oracle_dwconv2d_nhwc(fp(x), fp(np.ascontiguousarray(w.reshape(c, 9))), fp(y), b, hw, hw, c, 3, 3, stride,
+                                1, 9, 0)
+    t = torch.nn.functional.conv2d(torch.from_numpy(x).permute(0, 3, 1, 2).double(),
+                                   torch.from_numpy(w).unsqueeze(1).double(), stride=stride, padding=1,
+                                   groups=c).permute(0, 2, 3, 1).float().numpy()
+    np.testing.assert_allclose(y, t, rtol=1e-5, atol=1e-5)
 
 
 def test_gemm_oracle_matches_numpy(oracle):
