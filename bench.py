@@ -40,6 +40,8 @@ def parse_args():
     ap.add_argument("--table1", default="2,4,8,10,16,20,32,40,64,80,100,120",
                     help="R values of the conv2_2 microbench sweep ('' to skip)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--extra", default="mix,bert",
+                    help="extra BASELINE configs at N=1: mix (configs[2]) and bert (configs[3]); '' to skip")
     ap.add_argument("--serve-seconds", type=float, default=1.5,
                     help="real-clock serving run per load point (0 = skip the serving section)")
     ap.add_argument("--slo", type=float, default=0.040, help="query SLO (s) of the serving run")
@@ -369,10 +371,18 @@ def run_ours(args):
     h2d = sum(t.numel() * t.element_size() for t in h_in)
     d2h = sum(t.numel() * t.element_size() for t in h_out)
 
+    bytes_round = eng.compulsory_bytes_per_round()
     # Real-clock serving (dynamic batcher + round programs + CUDA-event completions)
     serving = None
     if args.serve_seconds > 0:
         serving = run_serving(args, layers, local, rank, world, dist if world > 1 else None)
+
+    extra = {}
+    if args.extra and rank == 0 and world == 1:
+        del eng
+        torch.cuda.empty_cache()
+        for name in args.extra.split(","):
+            extra[name] = {"mix": run_mix, "bert": run_bert}[name](torch, args, dev, stream)
 
     # Table-1 analogue: R tenants x conv2_2 (256,128,1152) b1, L2 flushed between steps
     table1 = None
@@ -395,7 +405,6 @@ def run_ours(args):
     # intensity (FLOPs/bytes) is below the ridge point, so HBM is the binding
     # roof; the tensor view is reported beside it.
     round_s = sk_avg[0] / 1e3
-    bytes_round = eng.compulsory_bytes_per_round()
     achieved_gbs = bytes_round / round_s / 1e9
     achieved = flops_round / round_s / 1e12
     traffic = None
@@ -438,7 +447,7 @@ def run_ours(args):
                        f"per formed super-kernel",
             "superkernels_per_round": len(rnd.kernels), "tiles_per_round": sum(k.planned_cost.blocks
                                                                              for k in rnd.kernels),
-            "l2": f"inputs larger than L2 ({eng.compulsory_bytes_per_round() / 1e6:.0f} MB compulsory/round)",
+            "l2": f"inputs larger than L2 ({bytes_round / 1e6:.0f} MB compulsory/round)",
         },
         "modes": {
             name: {"tflops": tf(r["ms_per_step"]), "ms_per_step": r["ms_per_step"], "launches_per_step": r["launches"],
@@ -475,6 +484,8 @@ def run_ours(args):
         line["table1"] = table1
     if serving is not None:
         line["serving"] = serving
+    for name, sec in extra.items():
+        line["config_" + name] = sec
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -529,6 +540,84 @@ def run_serving(args, layers, local, rank, world, dist):
         res[f"poisson_{int(frac * 100)}pct"] = dict(session(frac * per_tenant_qps, 1),
                                                    rate_qps_per_tenant=frac * per_tenant_qps)
     return res
+
+
+def round_modes(torch, eng, stream, steps, warmup=3):
+    """Packed round program vs time-only vs space-only over one engine's tenants."""
+    rnd = eng.plan_round()
+    gs = {"packed": eng.capture_round(rnd), "time_only": eng.capture_serial("time_only"),
+          "space_only": eng.capture_serial("space_only")}
+    out = {"superkernels_per_round": len(rnd.kernels), "tiles_per_round": sum(k.planned_cost.blocks for k in rnd.kernels),
+           "gflop_per_round": eng.flops_per_round() / 1e9}
+    for name, g in gs.items():
+        for _ in range(warmup):
+            g.launch(stream.cuda_stream)
+        per, span = time_graph(torch, g, stream, steps)
+        ms = span / steps
+        out[name] = {"tflops": eng.flops_per_round() / (ms / 1e3) / 1e12, "ms_per_step": ms,
+                     "p99_ms": nearest_rank(per, 99.0), "launches_per_step": g.kernels}
+    out["packed_over_space_only"] = out["space_only"]["ms_per_step"] / out["packed"]["ms_per_step"]
+    out["packed_over_time_only"] = out["time_only"]["ms_per_step"] / out["packed"]["ms_per_step"]
+    return out
+
+
+def serve_points(eng_factory, seconds, fracs=(0.5, 0.8)):
+    """Closed-loop saturation, then Poisson at fractions of the saturated rate."""
+    eng = eng_factory(None)
+    eng.serve(duration=0.3, warmup=0.1, seed=1)
+    sat = eng.serve(duration=seconds, warmup=min(0.2, seconds / 4), seed=42).stats
+    del eng
+    pts = {"closed_loop": sat}
+    for f in fracs:
+        eng = eng_factory(f * sat["qps"])
+        eng.serve(duration=0.3, warmup=0.1, seed=1)
+        pts[f"poisson_{int(f * 100)}pct"] = eng.serve(duration=seconds, warmup=min(0.2, seconds / 4), seed=42).stats
+        del eng
+    keep = ("tflops", "qps", "p50_ms", "p99_ms", "max_ms", "slo_violation_frac", "queries", "rounds",
+            "mean_queries_per_round", "mean_round_ms", "plan_misses", "evicted")
+    return {k: {f: v[f] for f in keep} for k, v in pts.items()}
+
+
+def run_mix(torch, args, dev, stream):
+    """BASELINE configs[2]: ResNet-50 + VGG-16 + MobileNet-v2 tenants (two each)
+    at 224, different layer lists in one round program (MobileNet's depthwise
+    layers are the super-kernel's CUDA-core tile type); round modes at batch
+    4, then real-clock serving with Poisson arrivals and dynamic batching
+    (max batch 8 in variants 2 and 8, SLOs 40/60/20 ms)."""
+    from paper_1901_00041_b200 import workload as W
+    from paper_1901_00041_b200.engine import ServeTenant, ServingEngine, SpaceTimeEngine
+    models = [("resnet50", W.resnet50(224), 0.040), ("vgg16", W.vgg16(224), 0.060),
+              ("mobilenet_v2", W.mobilenet_v2(224), 0.020)] * 2
+    eng = SpaceTimeEngine([m[1] for m in models], [4] * len(models), device_index=dev.index)
+    rm = round_modes(torch, eng, stream, max(5, args.steps // 2))
+    del eng
+
+    def factory(total_qps):
+        specs = []
+        for _, layers, slo in models:
+            rate = 0.0 if total_qps is None else total_qps / len(models)
+            specs.append(ServeTenant(layers, max_batch=8, rate_qps=rate, concurrency=8, slo_latency=slo,
+                                     batches=[2, 8]))
+        return ServingEngine(specs, device_index=dev.index)
+
+    sv = serve_points(factory, max(0.5, args.serve_seconds))
+    return {"workload": "2x resnet50 + 2x vgg16 + 2x mobilenet_v2 @224 (BASELINE configs[2]); round modes at "
+                        "batch 4; serving: max batch 8 (variants 2/8), SLO 40/60/20 ms, Poisson at 50%/80% of "
+                        "closed-loop saturation (equal per-tenant rates)",
+            "round_b4": rm, "serving": sv}
+
+
+def run_bert(torch, args, dev, stream):
+    """BASELINE configs[3]: 16 tenants x BERT-base projection/FFN GEMMs (12
+    encoder layers: qkv, attn-out, ffn1, ffn2), seq 128, batch 1 and 4."""
+    from paper_1901_00041_b200 import workload as W
+    from paper_1901_00041_b200.engine import SpaceTimeEngine
+    out = {"workload": "16 tenants x BERT-base 12-layer projection/FFN GEMMs, seq 128 (BASELINE configs[3])"}
+    for b in (1, 4):
+        eng = SpaceTimeEngine([W.bert_base_gemms(128, layers=12)] * 16, [b] * 16, device_index=dev.index)
+        out[f"batch{b}"] = round_modes(torch, eng, stream, max(5, args.steps // 2))
+        del eng
+    return out
 
 
 def run_table1(torch, rs, dev, stream):

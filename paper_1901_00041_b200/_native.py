@@ -241,6 +241,8 @@ def lib() -> C.CDLL:
             raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() (no fallback path exists)")
         handle = C.CDLL(LIB_PATH)
         for name, (res, args) in _SIGS.items():
+            if os.environ.get("GM_LIB_PATH") and not hasattr(handle, name):
+                continue  # an older build loaded for A/B comparisons (debug)
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args

@@ -106,6 +106,7 @@ struct Prepared {
   uint32_t* heads = nullptr;
   int32_t* qinfo = nullptr;  // [nq] begins then [nq] lengths
   int nq = 0;
+  bool greedy = false;  // greedy in-order claiming (one claim counter after the counters and queue heads)
 
   void release() {
     cudaFree(qinfo);
@@ -139,6 +140,7 @@ struct Runtime {
   int64_t narrow_min_tiles = 0;  // >0: narrow a member's N tile until it has this many tiles
   bool row_fold = true;          // S*Cin <= 32 convs (RGB stems) use the row-folded im2col path
   bool dynamic_schedule = false;  // round programs: per-tenant ready queues (else static round-robin)
+  bool greedy_schedule = false;   // round programs: greedy in-order tile claiming (else static round-robin)
   int bn = 256;     // N tile of the super-kernel (== DeviceSpec.tile_n)
   int smem_bytes = 0;
   const void* kernel = nullptr;
@@ -619,8 +621,8 @@ struct Runtime {
     cuda_check(cudaMemcpy(p.tiles, table.data(), table.size() * sizeof(dev::TileEntry), cudaMemcpyHostToDevice),
                "upload round tiles");
     // counters and queue heads share one allocation: one memset per launch resets both
-    cuda_check(cudaMalloc(&p.counters, std::max<size_t>(1, targets.size() + p.nq) * sizeof(uint32_t)),
-               "cudaMalloc(counters)");
+    p.greedy = greedy_schedule && !dynamic_schedule;
+    cuda_check(cudaMalloc(&p.counters, (targets.size() + p.nq + 1) * sizeof(uint32_t)), "cudaMalloc(counters)");
     if (p.nq > 0) {
       p.heads = p.counters + targets.size();
       std::vector<int32_t> qinfo(qbeg);
@@ -694,7 +696,7 @@ struct Runtime {
     int launches = 0;
     // counters first: the pre-pass -> super-kernel edge stays kernel-to-kernel (PDL)
     if (p.counters)
-      cuda_check(cudaMemsetAsync(p.counters, 0, static_cast<size_t>(p.n_counters + p.nq) * sizeof(uint32_t), stream),
+      cuda_check(cudaMemsetAsync(p.counters, 0, static_cast<size_t>(p.n_counters + p.nq + 1) * sizeof(uint32_t), stream),
                  "reset round counters");
     if (ev_begin) cuda_check(cudaEventRecordWithFlags(ev_begin, stream, cudaEventRecordExternal), "event record");
     launches += launch_prepasses(p, stream, count);
@@ -715,7 +717,8 @@ struct Runtime {
     uint32_t* counters = p.counters;
     const uint32_t* targets = p.targets;
     dev::RoundArgs ra{counters, targets, p.ws_map, p.ws, p.split_ctr, trace,
-                      p.heads, p.qinfo, p.qinfo ? p.qinfo + p.nq : nullptr, p.nq};
+                      p.heads, p.qinfo, p.qinfo ? p.qinfo + p.nq : nullptr, p.nq,
+                      p.greedy ? p.counters + p.n_counters + p.nq : nullptr};
     void* args[4] = {&slots, &tiles, &n, &ra};
     cuda_check(cudaLaunchKernelExC(&cfg, kernel, args), "launch superkernel");
     if (ev_end) cuda_check(cudaEventRecordWithFlags(ev_end, stream, cudaEventRecordExternal), "event record");
@@ -888,6 +891,8 @@ int gm_ctx_set_option(gm_ctx* ctx, const char* name, int64_t value) {
     rt.max_splits = value;
   } else if (n == "dynamic_schedule") {
     rt.dynamic_schedule = value != 0;  // applies to round programs prepared afterwards
+  } else if (n == "greedy_schedule") {
+    rt.greedy_schedule = value != 0;  // applies to round programs prepared afterwards
   } else if (n == "narrow_min_tiles") {
     rt.narrow_min_tiles = value;  // applies to tenants registered afterwards
   } else if (n == "row_fold") {

@@ -133,9 +133,11 @@ struct RoundArgs {
   const int32_t* qbeg;
   const int32_t* qlen;
   int32_t nq;
+  uint32_t* next_tile;        // greedy schedule: one global in-order claim counter (null = static / queues)
 };
 
 constexpr int kTileQ = 8;   // claimed-tile ring between producer and consumers
+constexpr int kDwTag = 1 << 30;  // tile-ring tag: a depthwise tile (no TMA / MMA work)
 constexpr int kSchedQ = 2;  // scheduler look-ahead: tiles claimed before the producer needs them
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -405,25 +407,50 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t stage = 0, phase = 0;
       bool first = true;
       uint32_t qslot = 0, qphase = 0, sslot = 0, sphase = 0;
+      // Greedy schedule: the producer claims its own tiles in table order
+      // from one global counter, the next one as it starts a tile's loads (a
+      // one-tile look-ahead instead of the static round-robin assignment).
+      const bool greedy = ra.next_tile != nullptr;
+      int next = greedy ? static_cast<int>(atomicAdd(ra.next_tile, 1u)) : 0;
       for (;;) {
-        mbar_wait(&sq_full[sslot], sphase);  // next tile from the scheduler warp
-        const int t = sq[sslot];
-        mbar_arrive(&sq_empty[sslot]);
-        if (++sslot == kSchedQ) {
-          sslot = 0;
-          sphase ^= 1;
+        int t;
+        if (greedy) {
+          t = next < n_tiles ? next : -1;
+        } else {
+          mbar_wait(&sq_full[sslot], sphase);  // next tile from the scheduler warp
+          t = sq[sslot];
+          mbar_arrive(&sq_empty[sslot]);
+          if (++sslot == kSchedQ) {
+            sslot = 0;
+            sphase ^= 1;
+          }
+        }
+        TileEntry te{};
+        const MemberDesc* md = slots;
+        bool dw = false;
+        if (t >= 0) {
+          te = tiles[t];
+          md = slots + te.member;
+          dw = md->a_mode == kDepthwise;
         }
         mbar_wait(&tq_empty[qslot], qphase ^ 1);
-        tq[qslot] = t;
+        tq[qslot] = dw ? (t | kDwTag) : t;  // consumers skip / route a depthwise tile without loading it
         mbar_arrive(&tq_full[qslot]);
+        const uint32_t wslot = qslot, wphase = qphase;
         if (++qslot == kTileQ) {
           qslot = 0;
           qphase ^= 1;
         }
         if (t < 0) break;
-        const TileEntry te = tiles[t];
-        const MemberDesc* md = slots + te.member;
-        if (md->a_mode == kDepthwise) continue;  // computed by the epilogue warps
+        if (dw) {  // computed by the epilogue warps
+          if (greedy) {
+            // claim the next tile only once every epilogue warp has taken this
+            // one, so a CTA never hoards depthwise tiles other SMs could run
+            mbar_wait(&tq_empty[wslot], wphase);
+            next = static_cast<int>(atomicAdd(ra.next_tile, 1u));
+          }
+          continue;
+        }
         prefetch_tmap(&md->a);
         prefetch_tmap(&md->b);
         const int kb_lo = te.kb_end ? te.kb_begin : 0;
@@ -520,6 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             phase ^= 1;
           }
         }
+        if (greedy) next = static_cast<int>(atomicAdd(ra.next_tile, 1u));  // latency hides under the loads
         for (; kb < k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], tx);
@@ -547,9 +575,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           qphase ^= 1;
         }
         if (t < 0) break;
+        if (t & kDwTag) continue;  // depthwise: no accumulator, the epilogue warps compute it
         const TileEntry te = tiles[t];
         const MemberDesc* md = slots + te.member;
-        if (md->a_mode == kDepthwise) continue;  // no accumulator: the epilogue warps compute it
         const int kb_lo = te.kb_end ? te.kb_begin : 0;
         const int k_blocks = te.kb_end ? te.kb_end : md->k_blocks;
         const uint32_t idesc = md->idesc;
@@ -587,7 +615,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 3) {
-    if (lane == 0) {
+    if (lane == 0 && !ra.next_tile) {  // greedy: the producer claims its own tiles
       // ------------------------------------------------ tile scheduler
       // Claims this CTA's next tile (static round-robin, or the head of a
       // ready per-tenant queue) up to kSchedQ tiles ahead of the producer, so
@@ -641,14 +669,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     // -------------------------------------------------- epilogue: 2 warpgroups
     // Warpgroup g drains accumulator buffer g, i.e. every other tile, so one
     // group's store-completion wait (needed before publishing a round
-    // counter) overlaps the other group's TMEM drain.
+    // counter) overlaps the other group's TMEM drain.  (Draining every tile
+    // with both groups halves a tile's drain latency but serialises the
+    // publish waits; measured slower on the headline round.)
     const int quarter = warp & 3;  // the TMEM lane quarter this warp may access
     const uint32_t acc = static_cast<uint32_t>((warp - 4) >> 2);
+    int mma_local = 0;  // accumulator tiles seen (depthwise tiles have none)
     uint8_t* stage_buf = epi + (warp - 4) * 2 * kEpiBufBytes;
     uint32_t acc_phase = 0, buf = 0;
     int issued = 0;
     uint32_t qslot = 0, qphase = 0;
-    int mma_local = 0;     // accumulator tiles seen (depthwise tiles have none)
     bool dw_gated = false;  // PDL wait done before this warp's first depthwise tile
     for (;;) {
       int t = 0;
@@ -663,9 +693,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         qphase ^= 1;
       }
       if (t < 0) break;
-      const TileEntry te = tiles[t];
-      const MemberDesc* md = slots + te.member;
-      if (md->a_mode == kDepthwise) {
+      if (t & kDwTag) {
+        t &= ~kDwTag;
+        const TileEntry te = tiles[t];
+        const MemberDesc* md = slots + te.member;
         // all eight epilogue warps share the tile; gate on the PDL
         // prerequisite and the tenant's previous layer like the A producer
         if (!dw_gated) {
@@ -693,6 +724,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool mine = (mma_local & 1) == static_cast<int>(acc);
       ++mma_local;
       if (!mine) continue;
+      const TileEntry te = tiles[t];
+      const MemberDesc* md = slots + te.member;
       const int m0 = te.m_tile * kBM + quarter * 32;
       const int n0 = te.n_tile * md->n_tile;
       const int cols = min(md->n_tile, md->n - n0);
