@@ -137,6 +137,7 @@ struct Runtime {
   bool pdl = true;      // programmatic dependent launch between consecutive super-kernels
   bool split_k = false;      // round programs split few-tile long-K members (opt-in)
   int64_t max_splits = 4;
+  int64_t split_min_kb = 8;  // fewest k-blocks per split
   int64_t narrow_min_tiles = 0;  // >0: narrow a member's N tile until it has this many tiles
   bool row_fold = true;          // S*Cin <= 32 convs (RGB stems) use the row-folded im2col path
   bool dynamic_schedule = false;  // round programs: per-tenant ready queues (else static round-robin)
@@ -546,8 +547,9 @@ struct Runtime {
         // Split-K when the plan cannot fill the SMs and the K loop is long:
         // about two waves of tiles, at least 4 k-blocks per split.
         int splits = 1;
-        if (split_k && plan_tiles < sms && kb >= 16) {
-          splits = static_cast<int>(std::min<int64_t>({kb / 8, (sms + plan_tiles - 1) / plan_tiles, max_splits}));
+        if (split_k && plan_tiles < sms && kb >= 2 * split_min_kb) {
+          splits = static_cast<int>(
+              std::min<int64_t>({kb / split_min_kb, (sms + plan_tiles - 1) / plan_tiles, max_splits}));
           const int chunk = (kb + splits - 1) / splits;
           splits = (kb + chunk - 1) / chunk;
         }
@@ -622,7 +624,10 @@ struct Runtime {
                "upload round tiles");
     // counters and queue heads share one allocation: one memset per launch resets both
     p.greedy = greedy_schedule && !dynamic_schedule;
-    cuda_check(cudaMalloc(&p.counters, (targets.size() + p.nq + 1) * sizeof(uint32_t)), "cudaMalloc(counters)");
+    // completion counters | queue heads | greedy claim counter | exit counter: zeroed here once,
+    // then by each launch's last CTA (no per-launch memset)
+    cuda_check(cudaMalloc(&p.counters, (targets.size() + p.nq + 2) * sizeof(uint32_t)), "cudaMalloc(counters)");
+    cuda_check(cudaMemset(p.counters, 0, (targets.size() + p.nq + 2) * sizeof(uint32_t)), "clear counters");
     if (p.nq > 0) {
       p.heads = p.counters + targets.size();
       std::vector<int32_t> qinfo(qbeg);
@@ -694,10 +699,6 @@ struct Runtime {
   int launch(Prepared& p, cudaStream_t stream, bool count = true, cudaEvent_t ev_begin = nullptr,
              cudaEvent_t ev_end = nullptr, uint64_t* trace = nullptr) {
     int launches = 0;
-    // counters first: the pre-pass -> super-kernel edge stays kernel-to-kernel (PDL)
-    if (p.counters)
-      cuda_check(cudaMemsetAsync(p.counters, 0, static_cast<size_t>(p.n_counters + p.nq + 1) * sizeof(uint32_t), stream),
-                 "reset round counters");
     if (ev_begin) cuda_check(cudaEventRecordWithFlags(ev_begin, stream, cudaEventRecordExternal), "event record");
     launches += launch_prepasses(p, stream, count);
     const int grid = std::max(1, std::min(p.n_tiles, sms));
@@ -718,7 +719,8 @@ struct Runtime {
     const uint32_t* targets = p.targets;
     dev::RoundArgs ra{counters, targets, p.ws_map, p.ws, p.split_ctr, trace,
                       p.heads, p.qinfo, p.qinfo ? p.qinfo + p.nq : nullptr, p.nq,
-                      p.greedy ? p.counters + p.n_counters + p.nq : nullptr};
+                      p.greedy ? p.counters + p.n_counters + p.nq : nullptr,
+                      p.counters ? p.counters + p.n_counters + p.nq + 1 : nullptr, p.n_counters + p.nq + 1};
     void* args[4] = {&slots, &tiles, &n, &ra};
     cuda_check(cudaLaunchKernelExC(&cfg, kernel, args), "launch superkernel");
     if (ev_end) cuda_check(cudaEventRecordWithFlags(ev_end, stream, cudaEventRecordExternal), "event record");
@@ -891,6 +893,9 @@ int gm_ctx_set_option(gm_ctx* ctx, const char* name, int64_t value) {
     rt.max_splits = value;
   } else if (n == "dynamic_schedule") {
     rt.dynamic_schedule = value != 0;  // applies to round programs prepared afterwards
+  } else if (n == "split_min_kb") {
+    if (value < 1 || value > 1024) throw std::invalid_argument("split_min_kb must be in [1, 1024]");
+    rt.split_min_kb = value;
   } else if (n == "greedy_schedule") {
     rt.greedy_schedule = value != 0;  // applies to round programs prepared afterwards
   } else if (n == "narrow_min_tiles") {

@@ -134,6 +134,8 @@ struct RoundArgs {
   const int32_t* qlen;
   int32_t nq;
   uint32_t* next_tile;        // greedy schedule: one global in-order claim counter (null = static / queues)
+  uint32_t* exit_ctr;         // CTAs finished; the last one zeroes counters[0, n_reset) for the next launch
+  int32_t n_reset;
 };
 
 constexpr int kTileQ = 8;   // claimed-tile ring between producer and consumers
@@ -411,7 +413,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       // from one global counter, the next one as it starts a tile's loads (a
       // one-tile look-ahead instead of the static round-robin assignment).
       const bool greedy = ra.next_tile != nullptr;
-      int next = greedy ? static_cast<int>(atomicAdd(ra.next_tile, 1u)) : 0;
+      int next = 0;
+      if (greedy) {
+        // the claim counter is reset by the previous launch's last CTA
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        next = static_cast<int>(atomicAdd(ra.next_tile, 1u));
+      }
       for (;;) {
         int t;
         if (greedy) {
@@ -620,6 +627,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // Claims this CTA's next tile (static round-robin, or the head of a
       // ready per-tenant queue) up to kSchedQ tiles ahead of the producer, so
       // the claim's atomic round trip overlaps the producer's loads.
+      if (ra.heads) asm volatile("griddepcontrol.wait;" ::: "memory");  // queue heads reset by the prior launch
       uint32_t sslot = 0, sphase = 0;
       int static_next = blockIdx.x;
       int rr = ra.nq > 0 ? static_cast<int>(blockIdx.x) % ra.nq : 0;
@@ -849,6 +857,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::kTmemCols)
                  : "memory");
+  }
+  // Round programs reset their own completion counters: the last CTA to
+  // finish zeroes them, so a replay needs no memset node before the kernel.
+  // The next launch touches counters only after griddepcontrol.wait, i.e.
+  // after this grid (and the reset) completed.
+  if (ra.exit_ctr) {
+    if (threadIdx.x == 0) {
+      __threadfence();
+      *tmem_slot = atomicAdd(ra.exit_ctr, 1u) == gridDim.x - 1 ? 1u : 0u;
+    }
+    __syncthreads();
+    if (*tmem_slot) {
+      __threadfence();
+      for (int i = threadIdx.x; i < ra.n_reset; i += blockDim.x) ra.counters[i] = 0;
+      if (threadIdx.x == 0) *ra.exit_ctr = 0;
+    }
   }
 }
 

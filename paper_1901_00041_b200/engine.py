@@ -154,6 +154,8 @@ class SpaceTimeEngine:
                                                          tenant_id=f"t{tenant_offset + i}"))
         self._now = 0
         self._graphs: Dict[int, Graph] = {}  # plan-list key -> captured round program
+        self._stable_plan: Optional[Round] = None  # serve_round's steady-state plan
+        self._last_key: Optional[int] = None
 
     # ------------------------------------------------------------ planning
     def flops_per_round(self) -> int:
@@ -169,6 +171,7 @@ class SpaceTimeEngine:
         (e.g. ``max_waves=1`` for reference plan parity)."""
         if policy is not None:
             self.ctx.set_policy(policy)
+            self._stable_plan = None
         r = self.ctx.plan_round(self.tenants, self._now)
         if r.count:
             self._now = r.end_time()  # dispatches are serial on the virtual device
@@ -206,7 +209,15 @@ class SpaceTimeEngine:
         with torch.cuda.stream(stream):
             for m, h in zip(self.models, host_inputs):
                 m.query_input.copy_(h, non_blocking=True)
-            rnd = self.plan_round()
+            # Steady state: once two consecutive rounds of the same tenants plan
+            # identically, the plan is reused (a SuperKernelCache hit for every
+            # member set: no planning work); re-planned otherwise.
+            rnd = self._stable_plan
+            if rnd is None:
+                rnd = self.plan_round()
+                if self._last_key == rnd.key:
+                    self._stable_plan = rnd
+                self._last_key = rnd.key
             key = rnd.key
             g = self._graphs.get(key)
             if g is None:

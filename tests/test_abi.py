@@ -39,6 +39,12 @@ def test_abi_version_and_host_only_context():
     assert lib.gm_launch_members(h, (ctypes.c_int32 * 1)(0), (ctypes.c_int32 * 1)(0), 1, 0, None) == \
         _native.GM_ENODEV
     assert b"no CUDA device" in lib.gm_last_error() or b"context has no CUDA device" in lib.gm_last_error()
+    # the serving loop needs the device runtime too
+    t = _native.gm_serve_tenant(1, (ctypes.c_int32 * 1)(0), (ctypes.c_int32 * 1)(1), 0.0, 1, 0, 0.04, 1)
+    cfg = _native.gm_serve_config(1.0, 0.1, -1.0, 42, 1, 0, 0)
+    out = _native.gm_serve_stats()
+    assert lib.gm_serve(h, ctypes.byref(t), 1, ctypes.byref(cfg), ctypes.byref(out), None, 0, None) == \
+        _native.GM_ENODEV
     lib.gm_destroy(h)
 
 

@@ -19,6 +19,9 @@ def build(config, opts):
     if config == "mix":
         ms = [W.resnet50(224), W.vgg16(224), W.mobilenet_v2(224)] * 2
         return SpaceTimeEngine(ms, [4] * 6, options=opts)
+    if config.startswith("t1r"):  # Table-1 microbench: R tenants x conv2_2 b1
+        r = int(config[3:])
+        return SpaceTimeEngine([W.conv2_2()] * r, [1] * r, options=opts)
     if config == "bert4":
         return SpaceTimeEngine([W.bert_base_gemms(128, 12)] * 16, [4] * 16, options=opts)
     raise SystemExit(config)
