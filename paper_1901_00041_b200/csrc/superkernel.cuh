@@ -590,6 +590,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t idesc = md->idesc;
         const bool a_narrow = md->a_mode == kAIm2colNarrow;
         const bool a_fold = md->a_mode == kAIm2colFold;
+        // Smem descriptors (SM100): lo = start >> 4 | LBO >> 4 << 16, hi = SBO
+        // >> 4 | version 1 << 14 | swizzle << 29, built once per tile.  Per
+        // UMMA_K step (16 bf16) the A start advances 32 B inside the 128 B
+        // swizzle atom, or two narrow tap columns, or 32 B inside a folded
+        // 64 B row (then the next column): k1..k3 in 16-byte units.
+        uint32_t a_hi = (1024u >> 4) | (1u << 14) | (2u << 29), a_lbo = 1u << 16;
+        uint32_t k1 = 2, k2 = 4, k3 = 6;
+        if (a_fold) {
+          a_hi = (512u >> 4) | (1u << 14) | (4u << 29);
+          k2 = kFoldTapBytes >> 4;
+          k3 = k2 + 2;
+        } else if (a_narrow) {
+          a_hi = (128u >> 4) | (1u << 14);
+          a_lbo = static_cast<uint32_t>(kNarrowTapBytes >> 4) << 16;
+          k1 = (2 * kNarrowTapBytes) >> 4;
+          k2 = 2 * k1;
+          k3 = 3 * k1;
+        }
+        const uint64_t a_hi64 = static_cast<uint64_t>(a_hi) << 32;
+        constexpr uint64_t b_hi64 = static_cast<uint64_t>((1024u >> 4) | (1u << 14) | (2u << 29)) << 32;
+        const uint32_t ring_base = smem_u32(ring);
         mbar_wait(&acc_empty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -597,18 +618,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (trace && kb == kb_lo) trace[6 * t + 2] = globaltimer();
-          const uint32_t a_addr = smem_u32(ring + stage * C::kStageBytes);
-          const uint32_t b_addr = a_addr + kABytes;
-#pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            // advance 16 bf16 along K: 32 B inside the 128 B swizzle atom, or
-            // two narrow tap columns, or 32 B inside a folded 64 B row
-            const uint64_t a_desc =
-                a_fold     ? sw64_desc(a_addr + (k >> 1) * kFoldTapBytes + (k & 1) * 32)
-                : a_narrow ? interleave_desc(a_addr + k * 2 * kNarrowTapBytes)
-                           : sw128_desc(a_addr + k * 32);
-            umma_bf16(d_tmem, a_desc, sw128_desc(b_addr + k * 32), idesc, (kb != kb_lo || k != 0) ? 1u : 0u);
-          }
+          const uint32_t a_addr = ring_base + stage * C::kStageBytes;
+          const uint32_t a_lo = ((a_addr >> 4) & 0x3FFFu) | a_lbo;
+          const uint32_t b_lo = (((a_addr + kABytes) >> 4) & 0x3FFFu) | (1u << 16);
+          umma_bf16(d_tmem, a_hi64 | a_lo, b_hi64 | b_lo, idesc, kb != kb_lo ? 1u : 0u);
+          umma_bf16(d_tmem, a_hi64 | (a_lo + k1), b_hi64 | (b_lo + 2), idesc, 1u);
+          umma_bf16(d_tmem, a_hi64 | (a_lo + k2), b_hi64 | (b_lo + 4), idesc, 1u);
+          umma_bf16(d_tmem, a_hi64 | (a_lo + k3), b_hi64 | (b_lo + 6), idesc, 1u);
           umma_commit(&empty[stage]);  // frees the smem stage once these MMAs retire
           if (++stage == kStages) {
             stage = 0;
