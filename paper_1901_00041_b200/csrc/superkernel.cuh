@@ -479,6 +479,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           c_blocks = md->c_blocks;
           s_taps = md->s_taps;
         }
+        // TMA im2col coordinates advance incrementally (load_a runs in k-block
+        // order within a tile): no integer divisions on the producer's path
+        int cb = 0, s_ = 0, r_ = 0;
+        if (md->a_mode == kAIm2col) {
+          const int tap = kb_lo / c_blocks;
+          cb = kb_lo - tap * c_blocks;
+          r_ = tap / s_taps;
+          s_ = tap - r_ * s_taps;
+        }
+        const int taps = md->taps, images = md->images;
+        const CUtensorMap* amap = &md->a;
         auto load_a = [&](int kb, uint32_t st) {
           uint8_t* a_dst = ring + st * C::kStageBytes;
           if (fold) {
@@ -486,8 +497,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < kFoldTaps; ++j) {
               const int r = kb * kFoldTaps + j;
-              tma_load_im2col(a_dst + j * kFoldTapBytes, &md->a, &full[st], 0, w0, h0, img, 0,
-                              static_cast<uint16_t>(r < md->taps ? r : 0));
+              tma_load_im2col(a_dst + j * kFoldTapBytes, amap, &full[st], 0, w0, h0, img, 0,
+                              static_cast<uint16_t>(r < taps ? r : 0));
             }
           } else if (narrow) {
             // eight 16 B tap columns; taps past R*S load an out-of-range image
@@ -495,21 +506,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
             for (int j = 0; j < kNarrowTaps; ++j) {
               const int tap = kb * kNarrowTaps + j;
-              const bool real = tap < md->taps;
+              const bool real = tap < taps;
               const int r = real ? tap / s_taps : 0;
               const int s = real ? tap - r * s_taps : 0;
-              tma_load_im2col(a_dst + j * kNarrowTapBytes, &md->a, &full[st], 0, w0, h0, real ? img : md->images,
+              tma_load_im2col(a_dst + j * kNarrowTapBytes, amap, &full[st], 0, w0, h0, real ? img : images,
                               static_cast<uint16_t>(s), static_cast<uint16_t>(r));
             }
           } else if (im2col) {
-            const int tap = kb / c_blocks;
-            const int c0 = (kb - tap * c_blocks) * kBK;
-            const int r = tap / s_taps;
-            const int s = tap - r * s_taps;
-            tma_load_im2col(a_dst, &md->a, &full[st], c0, w0, h0, img, static_cast<uint16_t>(s),
-                            static_cast<uint16_t>(r));
+            tma_load_im2col(a_dst, amap, &full[st], cb * kBK, w0, h0, img, static_cast<uint16_t>(s_),
+                            static_cast<uint16_t>(r_));
+            if (++cb == c_blocks) {
+              cb = 0;
+              if (++s_ == s_taps) {
+                s_ = 0;
+                ++r_;
+              }
+            }
           } else {
-            tma_load_2d(a_dst, &md->a, &full[st], kb * kBK, m0);
+            tma_load_2d(a_dst, amap, &full[st], kb * kBK, m0);
           }
         };
         auto load_b = [&](int kb, uint32_t st) {
