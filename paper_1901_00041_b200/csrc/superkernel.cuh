@@ -142,6 +142,12 @@ constexpr int kTileQ = 8;   // claimed-tile ring between producer and consumers
 constexpr int kDwTag = 1 << 30;  // tile-ring tag: a depthwise tile (no TMA / MMA work)
 constexpr int kSchedQ = 2;  // scheduler look-ahead: tiles claimed before the producer needs them
 
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p = 0;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(p));
+  return p != 0;
+}
+
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -583,73 +589,78 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (first) asm volatile("griddepcontrol.wait;" ::: "memory");
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------ MMA issuer
-      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      uint32_t qslot = 0, qphase = 0;
-      for (;;) {
-        mbar_wait(&tq_full[qslot], qphase);
-        const int t = tq[qslot];
-        mbar_arrive(&tq_empty[qslot]);
-        if (++qslot == kTileQ) {
-          qslot = 0;
-          qphase ^= 1;
-        }
-        if (t < 0) break;
-        if (t & kDwTag) continue;  // depthwise: no accumulator, the epilogue warps compute it
-        const TileEntry te = tiles[t];
-        const MemberDesc* md = slots + te.member;
-        const int kb_lo = te.kb_end ? te.kb_begin : 0;
-        const int k_blocks = te.kb_end ? te.kb_end : md->k_blocks;
-        const uint32_t idesc = md->idesc;
-        const bool a_narrow = md->a_mode == kAIm2colNarrow;
-        const bool a_fold = md->a_mode == kAIm2colFold;
-        // Smem descriptors (SM100): lo = start >> 4 | LBO >> 4 << 16, hi = SBO
-        // >> 4 | version 1 << 14 | swizzle << 29, built once per tile.  Per
-        // UMMA_K step (16 bf16) the A start advances 32 B inside the 128 B
-        // swizzle atom, or two narrow tap columns, or 32 B inside a folded
-        // 64 B row (then the next column): k1..k3 in 16-byte units.
-        uint32_t a_hi = (1024u >> 4) | (1u << 14) | (2u << 29), a_lbo = 1u << 16;
-        uint32_t k1 = 2, k2 = 4, k3 = 6;
-        if (a_fold) {
-          a_hi = (512u >> 4) | (1u << 14) | (4u << 29);
-          k2 = kFoldTapBytes >> 4;
-          k3 = k2 + 2;
-        } else if (a_narrow) {
-          a_hi = (128u >> 4) | (1u << 14);
-          a_lbo = static_cast<uint32_t>(kNarrowTapBytes >> 4) << 16;
-          k1 = (2 * kNarrowTapBytes) >> 4;
-          k2 = 2 * k1;
-          k3 = 3 * k1;
-        }
-        const uint64_t a_hi64 = static_cast<uint64_t>(a_hi) << 32;
-        constexpr uint64_t b_hi64 = static_cast<uint64_t>((1024u >> 4) | (1u << 14) | (2u << 29)) << 32;
-        const uint32_t ring_base = smem_u32(ring);
-        mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+    // ------------------------------------------------ MMA issuer
+    // The whole warp runs the loop on warp-uniform values (tile fields are
+    // broadcast from lane 0 with shfl), so the descriptor arithmetic lives in
+    // uniform registers; one elected lane issues tcgen05.mma / commit.
+    uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+    uint32_t qslot = 0, qphase = 0;
+    const uint32_t ring_base = smem_u32(ring);
+    for (;;) {
+      mbar_wait(&tq_full[qslot], qphase);
+      const int t = __shfl_sync(0xffffffffu, tq[qslot], 0);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tq_empty[qslot]);
+      if (++qslot == kTileQ) {
+        qslot = 0;
+        qphase ^= 1;
+      }
+      if (t < 0) break;
+      if (t & kDwTag) continue;  // depthwise: no accumulator, the epilogue warps compute it
+      const TileEntry te = tiles[t];
+      const MemberDesc* md = slots + te.member;
+      const int kb_lo = __shfl_sync(0xffffffffu, te.kb_end ? te.kb_begin : 0, 0);
+      const int k_blocks = __shfl_sync(0xffffffffu, te.kb_end ? te.kb_end : md->k_blocks, 0);
+      const uint32_t idesc = __shfl_sync(0xffffffffu, md->idesc, 0);
+      const int a_mode = __shfl_sync(0xffffffffu, md->a_mode, 0);
+      // Smem descriptors (SM100): lo = start >> 4 | LBO >> 4 << 16, hi = SBO
+      // >> 4 | version 1 << 14 | swizzle << 29, built once per tile.  Per
+      // UMMA_K step (16 bf16) the A start advances 32 B inside the 128 B
+      // swizzle atom, or two narrow tap columns, or 32 B inside a folded
+      // 64 B row (then the next column): k1..k3 in 16-byte units.
+      uint32_t a_hi = (1024u >> 4) | (1u << 14) | (2u << 29), a_lbo = 1u << 16;
+      uint32_t k1 = 2, k2 = 4, k3 = 6;
+      if (a_mode == kAIm2colFold) {
+        a_hi = (512u >> 4) | (1u << 14) | (4u << 29);
+        k2 = kFoldTapBytes >> 4;
+        k3 = k2 + 2;
+      } else if (a_mode == kAIm2colNarrow) {
+        a_hi = (128u >> 4) | (1u << 14);
+        a_lbo = static_cast<uint32_t>(kNarrowTapBytes >> 4) << 16;
+        k1 = (2 * kNarrowTapBytes) >> 4;
+        k2 = 2 * k1;
+        k3 = 3 * k1;
+      }
+      const uint64_t a_hi64 = static_cast<uint64_t>(a_hi) << 32;
+      constexpr uint64_t b_hi64 = static_cast<uint64_t>((1024u >> 4) | (1u << 14) | (2u << 29)) << 32;
+      mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = kb_lo; kb < k_blocks; ++kb) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = kb_lo; kb < k_blocks; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          if (trace && kb == kb_lo) trace[6 * t + 2] = globaltimer();
-          const uint32_t a_addr = ring_base + stage * C::kStageBytes;
-          const uint32_t a_lo = ((a_addr >> 4) & 0x3FFFu) | a_lbo;
-          const uint32_t b_lo = (((a_addr + kABytes) >> 4) & 0x3FFFu) | (1u << 16);
+        if (trace && kb == kb_lo && lane == 0) trace[6 * t + 2] = globaltimer();
+        const uint32_t a_addr = ring_base + stage * C::kStageBytes;
+        const uint32_t a_lo = ((a_addr >> 4) & 0x3FFFu) | a_lbo;
+        const uint32_t b_lo = (((a_addr + kABytes) >> 4) & 0x3FFFu) | (1u << 16);
+        if (elect_one()) {
           umma_bf16(d_tmem, a_hi64 | a_lo, b_hi64 | b_lo, idesc, kb != kb_lo ? 1u : 0u);
           umma_bf16(d_tmem, a_hi64 | (a_lo + k1), b_hi64 | (b_lo + 2), idesc, 1u);
           umma_bf16(d_tmem, a_hi64 | (a_lo + k2), b_hi64 | (b_lo + 4), idesc, 1u);
           umma_bf16(d_tmem, a_hi64 | (a_lo + k3), b_hi64 | (b_lo + 6), idesc, 1u);
           umma_commit(&empty[stage]);  // frees the smem stage once these MMAs retire
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
-          }
         }
-        umma_commit(&acc_full[acc]);  // accumulator ready for the epilogue
-        if (trace) trace[6 * t + 3] = globaltimer();
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        __syncwarp();
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
       }
+      if (elect_one()) umma_commit(&acc_full[acc]);  // accumulator ready for the epilogue
+      __syncwarp();
+      if (trace && lane == 0) trace[6 * t + 3] = globaltimer();
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
     }
   } else if (warp == 3) {
     if (lane == 0 && !ra.next_tile) {  // greedy: the producer claims its own tiles
