@@ -57,16 +57,6 @@ int b_box_rows(int64_t n, int bn) { return static_cast<int>(std::min<int64_t>(bn
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-// Tile width per member: the widest of {bn, bn/2, ..., 64} that still gives
-// the member >= 32 tiles, so few-tile (small-M) members spread their long K
-// loops over more SMs instead of serialising on a handful.
-int pick_n_tile(const Shape& s, int bn, int64_t min_tiles) {
-  if (min_tiles <= 0) return bn;
-  const int64_t mt = (s.m + dev::kBM - 1) / dev::kBM;
-  for (int w = bn; w > 64; w /= 2)
-    if (mt * ((s.n + w - 1) / w) >= min_tiles) return w;
-  return 64;
-}
 
 }  // namespace
 
@@ -78,7 +68,13 @@ struct Operator {
   int batch = 1;
   int slot = -1;    // index into the device MemberDesc array
   int tenant = -1, layer = -1;
-  int n_tile = 256;  // output columns per tile (<= the kernel's BN)
+  int n_tile = 256;  // output columns per tile (the kernel's BN)
+  // narrower-N variants of the same operator (descriptor slots), chosen per
+  // plan when the plan's full-width tiles cannot fill the SMs
+  int narrow_slot[2] = {-1, -1};
+  int narrow_w[2] = {0, 0};
+  const void* b_ptr = nullptr;  // weights as the B operand (for the variants' maps)
+  int64_t b_k = 0, b_ld = 0;
   bool prepass = false;
   bool fold = false;        // the pre-pass is the row fold (kAIm2colFold)
   const void* x = nullptr;
@@ -128,6 +124,7 @@ struct Runtime {
   std::vector<std::vector<int>> tenant_ops;  // tenant -> indices into flat
   std::vector<double> tenant_slo;            // seconds per pass
   std::vector<Operator> flat;
+  std::vector<int> slot_op;  // descriptor slot -> index into flat
   std::vector<dev::MemberDesc> host_desc;
   dev::MemberDesc* d_desc = nullptr;
   size_t d_cap = 0;
@@ -138,7 +135,8 @@ struct Runtime {
   bool split_k = false;      // round programs split few-tile long-K members (opt-in)
   int64_t max_splits = 4;
   int64_t split_min_kb = 8;  // fewest k-blocks per split
-  int64_t narrow_min_tiles = 0;  // >0: narrow a member's N tile until it has this many tiles
+  int64_t narrow_min_tiles = 20;  // >0: in a plan that cannot fill the SMs, narrow a member's N tile
+                                 // (256 -> 128 -> 64) until it has this many tiles
   bool row_fold = true;          // S*Cin <= 32 convs (RGB stems) use the row-folded im2col path
   bool dynamic_schedule = false;  // round programs: per-tenant ready queues (else static round-robin)
   bool greedy_schedule = false;   // round programs: greedy in-order tile claiming (else static round-robin)
@@ -271,6 +269,7 @@ struct Runtime {
     std::vector<int> ops;
     std::vector<Operator> fresh;
     std::vector<dev::MemberDesc> descs;
+    std::vector<int> slot_of_new;  // per new descriptor: its operator's index into flat
     for (size_t i = 0; i < t.n_layers; ++i) {
       const gm_layer_desc& L = t.layers[i];
       Operator op;
@@ -286,12 +285,15 @@ struct Runtime {
         op.conv = to_conv(L.conv);
         op.batch = L.batch < 1 ? 1 : L.batch;
         op.shape = with_batch(lower_conv(op.conv), op.batch);
-        op.n_tile = pick_n_tile(op.shape, bn, narrow_min_tiles);
+        op.n_tile = bn;
         const Conv& c = op.conv;
         const int64_t K = op.shape.k;
         const int64_t ldw = L.ldw > 0 ? L.ldw : K;
         if (ldw < K) throw std::invalid_argument("register_tenant: ldw < R*S*Cin");
         tiled_map(&md.b, L.w, op.shape.n, K, ldw, b_box_rows(op.shape.n, op.n_tile));
+        op.b_ptr = L.w;
+        op.b_k = K;
+        op.b_ld = ldw;
         const int64_t P = (c.image_h + 2 * c.padding - c.kernel_h) / c.stride + 1;
         const int64_t Q = (c.image_w + 2 * c.padding - c.kernel_w) / c.stride + 1;
         const bool pointwise = c.kernel_h == 1 && c.kernel_w == 1 && c.stride == 1 && c.padding == 0;
@@ -334,6 +336,9 @@ struct Runtime {
           cuda_check(cudaGetLastError(), "launch pad_narrow_weights");
           cuda_check(cudaDeviceSynchronize(), "pad_narrow_weights");
           tiled_map(&md.b, op.wpad, op.shape.n, op.kernel_k, op.kernel_k, b_box_rows(op.shape.n, op.n_tile));
+          op.b_ptr = op.wpad;
+          op.b_k = op.kernel_k;
+          op.b_ld = op.kernel_k;
         } else if (row_fold && c.kernel_w * c.in_channels <= dev::kFoldC &&
                    (L.ldx <= 0 || L.ldx == c.in_channels) && c.stride <= 8 && c.padding <= 127 &&
                    c.kernel_h - 1 - c.padding <= 128) {
@@ -360,6 +365,9 @@ struct Runtime {
           cuda_check(cudaGetLastError(), "launch fold_weights");
           cuda_check(cudaDeviceSynchronize(), "fold_weights");
           tiled_map(&md.b, op.wpad, op.shape.n, op.kernel_k, op.kernel_k, b_box_rows(op.shape.n, op.n_tile));
+          op.b_ptr = op.wpad;
+          op.b_k = op.kernel_k;
+          op.b_ld = op.kernel_k;
         } else {
           md.a_mode = dev::kATiled;  // explicit im2col pre-pass, then GEMM
           op.prepass = true;
@@ -404,13 +412,16 @@ struct Runtime {
         md.images = op.batch;
       } else if (L.kind == GM_LAYER_GEMM) {
         op.shape = to_shape(L.gemm);
-        op.n_tile = pick_n_tile(op.shape, bn, narrow_min_tiles);
+        op.n_tile = bn;
         if (!op.shape.valid()) throw std::invalid_argument("register_tenant: invalid GEMM shape");
         const int64_t ldx = L.ldx > 0 ? L.ldx : op.shape.k;
         const int64_t ldw = L.ldw > 0 ? L.ldw : op.shape.k;
         md.a_mode = dev::kATiled;
         tiled_map(&md.a, L.x, op.shape.m, op.shape.k, ldx, a_box_rows(op.shape.m));
         tiled_map(&md.b, L.w, op.shape.n, op.shape.k, ldw, b_box_rows(op.shape.n, op.n_tile));
+        op.b_ptr = L.w;
+        op.b_k = op.shape.k;
+        op.b_ld = ldw;
       } else {
         throw std::invalid_argument("register_tenant: unknown layer kind");
       }
@@ -429,8 +440,28 @@ struct Runtime {
       md.relu = L.relu ? 1 : 0;
       md.n_tile = op.n_tile;
       op.slot = static_cast<int>(host_desc.size() + descs.size());
-      if (op.slot > 0xFFFF) throw std::invalid_argument("register_tenant: too many registered operators");
+      const int f_index = static_cast<int>(flat.size() + fresh.size());
       descs.push_back(md);
+      slot_of_new.push_back(f_index);
+      // narrower-N variants (same operands, smaller B box / UMMA N)
+      if (op.kind != GM_LAYER_DWCONV && op.b_ptr) {
+        int v = 0;
+        for (int w = bn / 2; w >= 64 && v < 2; w /= 2) {
+          if (op.shape.n <= w) break;
+          dev::MemberDesc md2 = md;
+          tiled_map(&md2.b, op.b_ptr, op.shape.n, op.b_k, op.b_ld, b_box_rows(op.shape.n, w));
+          md2.idesc = make_idesc(b_box_rows(op.shape.n, w));
+          md2.tx_bytes = static_cast<uint32_t>((a_box_rows(op.shape.m) + b_box_rows(op.shape.n, w)) * dev::kBK * 2);
+          md2.n_tile = w;
+          op.narrow_slot[v] = static_cast<int>(host_desc.size() + descs.size());
+          op.narrow_w[v] = w;
+          descs.push_back(md2);
+          slot_of_new.push_back(f_index);
+          ++v;
+        }
+      }
+      if (host_desc.size() + descs.size() > 0x10000)
+        throw std::invalid_argument("register_tenant: too many registered operators");
       fresh.push_back(op);
     }
     // Commit: grow the device descriptor array and upload.
@@ -460,6 +491,7 @@ struct Runtime {
       ops.push_back(static_cast<int>(flat.size()));
       flat.push_back(op);
     }
+    slot_op.insert(slot_op.end(), slot_of_new.begin(), slot_of_new.end());
     tenant_ops.push_back(std::move(ops));
     tenant_slo.push_back(t.slo_latency > 0 ? t.slo_latency : 0.1);
     return static_cast<int>(tenant_ops.size() - 1);
@@ -479,6 +511,27 @@ struct Runtime {
     return tenant_ops[tenant][layer];
   }
 
+  // (descriptor slot, N tile) of operator f inside a plan whose members have
+  // plan_tiles full-width tiles: when the plan leaves most SMs idle, a member
+  // with few tiles uses a narrower-N variant (256 -> 128 -> 64) until it has
+  // narrow_min_tiles tiles -- more SMs share the plan's long K loops.
+  std::pair<int, int> variant(int f, int64_t plan_tiles) const {
+    const Operator& op = flat[f];
+    int slot = op.slot, w = op.n_tile;
+    if (narrow_min_tiles <= 0 || 2 * plan_tiles > sms) return {slot, w};  // the plan fills half the SMs already
+    const int64_t mt = (op.shape.m + dev::kBM - 1) / dev::kBM;
+    for (int i = 0; i < 2 && op.narrow_slot[i] >= 0; ++i) {
+      if (mt * ((op.shape.n + w - 1) / w) >= narrow_min_tiles) break;
+      slot = op.narrow_slot[i];
+      w = op.narrow_w[i];
+    }
+    return {slot, w};
+  }
+  int64_t full_tiles(int f) const {
+    const Operator& op = flat[f];
+    return ((op.shape.m + dev::kBM - 1) / dev::kBM) * ((op.shape.n + op.n_tile - 1) / op.n_tile);
+  }
+
   // Device tile table for a member list (cached: the B200 meaning of a
   // SuperKernelCache hit is that descriptors and table are already resident).
   Prepared& prepare(const std::vector<int>& members) {
@@ -492,13 +545,16 @@ struct Runtime {
     if (it != prepared.end()) return it->second;
     Prepared p;
     std::vector<dev::TileEntry> table;
+    int64_t plan_tiles = 0;
+    for (int f : members) plan_tiles += full_tiles(f);
     for (int f : members) {
       const Operator& op = flat[f];
+      const auto [slot, w] = variant(f, plan_tiles);
       const int64_t mt = (op.shape.m + dev::kBM - 1) / dev::kBM;
-      const int64_t nt = (op.shape.n + op.n_tile - 1) / op.n_tile;
+      const int64_t nt = (op.shape.n + w - 1) / w;
       for (int64_t a = 0; a < mt; ++a)
         for (int64_t b = 0; b < nt; ++b)
-          table.push_back(dev::TileEntry{static_cast<uint16_t>(op.slot), 0, static_cast<uint16_t>(a),
+          table.push_back(dev::TileEntry{static_cast<uint16_t>(slot), 0, static_cast<uint16_t>(a),
                                          static_cast<uint16_t>(b), -1, -1, 0, 0, -1});
       if (op.prepass) p.prepass_ops.push_back(f);
     }
@@ -530,10 +586,10 @@ struct Runtime {
     int n_ws = 0;
     for (const auto& pl : plans) {
       int64_t plan_tiles = 0;
-      for (int f : pl)
-        plan_tiles += ((flat[f].shape.m + dev::kBM - 1) / dev::kBM) * ((flat[f].shape.n + flat[f].n_tile - 1) / flat[f].n_tile);
+      for (int f : pl) plan_tiles += full_tiles(f);
       for (int f : pl) {
         const Operator& op = flat[f];
+        const auto [slot, w] = variant(f, plan_tiles);
         const int inst = static_cast<int>(targets.size());
         int dep = -1;
         if (op.layer > 0) {
@@ -542,7 +598,7 @@ struct Runtime {
         }
         last_instance[f] = inst;
         const int64_t mt = (op.shape.m + dev::kBM - 1) / dev::kBM;
-        const int64_t nt = (op.shape.n + op.n_tile - 1) / op.n_tile;
+        const int64_t nt = (op.shape.n + w - 1) / w;
         const int kb = static_cast<int>((op.shape.k + dev::kBK - 1) / dev::kBK);
         // Split-K when the plan cannot fill the SMs and the K loop is long:
         // about two waves of tiles, at least 4 k-blocks per split.
@@ -558,13 +614,13 @@ struct Runtime {
         for (int64_t a = 0; a < mt; ++a)
           for (int64_t b = 0; b < nt; ++b) {
             if (splits == 1) {
-              table.push_back(dev::TileEntry{static_cast<uint16_t>(op.slot), 1, static_cast<uint16_t>(a),
+              table.push_back(dev::TileEntry{static_cast<uint16_t>(slot), 1, static_cast<uint16_t>(a),
                                              static_cast<uint16_t>(b), inst, dep, 0, 0, -1});
               continue;
             }
             const int chunk = (kb + splits - 1) / splits;
             for (int s = 0; s < splits; ++s)
-              table.push_back(dev::TileEntry{static_cast<uint16_t>(op.slot), static_cast<uint16_t>(splits),
+              table.push_back(dev::TileEntry{static_cast<uint16_t>(slot), static_cast<uint16_t>(splits),
                                              static_cast<uint16_t>(a), static_cast<uint16_t>(b), inst, dep,
                                              static_cast<uint16_t>(s * chunk),
                                              static_cast<uint16_t>(std::min(kb, (s + 1) * chunk)), n_ws});
@@ -579,7 +635,7 @@ struct Runtime {
     if (dynamic_schedule && !table.empty()) {
       std::vector<size_t> idx(table.size());
       for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
-      auto tenant_of = [&](size_t i) { return flat[table[i].member].tenant; };
+      auto tenant_of = [&](size_t i) { return flat[slot_op[table[i].member]].tenant; };
       std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return tenant_of(a) < tenant_of(b); });
       std::vector<dev::TileEntry> sorted(table.size());
       std::vector<uint16_t> sorted_plan(table.size());
@@ -590,7 +646,7 @@ struct Runtime {
       table.swap(sorted);
       p.tile_plan.swap(sorted_plan);
       for (size_t i = 0; i < table.size(); ++i) {
-        if (i == 0 || flat[table[i].member].tenant != flat[table[i - 1].member].tenant) {
+        if (i == 0 || tenant_of(i) != tenant_of(i - 1)) {
           qbeg.push_back(static_cast<int32_t>(i));
           qlen.push_back(0);
         }
@@ -899,7 +955,7 @@ int gm_ctx_set_option(gm_ctx* ctx, const char* name, int64_t value) {
   } else if (n == "greedy_schedule") {
     rt.greedy_schedule = value != 0;  // applies to round programs prepared afterwards
   } else if (n == "narrow_min_tiles") {
-    rt.narrow_min_tiles = value;  // applies to tenants registered afterwards
+    rt.narrow_min_tiles = value;  // applies to plans prepared afterwards (0 = always full width)
   } else if (n == "row_fold") {
     rt.row_fold = value != 0;  // applies to tenants registered afterwards
   } else {
