@@ -322,13 +322,20 @@ int gm_ctx_cache(gm_ctx* ctx, gm_cache** c);
 int gm_ctx_device_spec(const gm_ctx* ctx, gm_device_spec* out);
 /* Replace the BatchPolicy gm_plan_round uses (e.g. parity vs b200 mode). */
 int gm_ctx_set_policy(gm_ctx* ctx, const gm_batch_policy* p);
-/* Execution options of the device runtime (none changes results):
+/* Execution options of the device runtime (none changes results; defaults in
+ * parentheses; tile-shape options apply to plans prepared afterwards):
  *   "pdl"               programmatic dependent launch between launches (1)
- *   "split_k"           round programs split few-tile long-K members (0)
- *   "max_splits"        split-K fan-out cap (4)
- *   "narrow_min_tiles"  narrow a member's N tile (256/128/64) until it has at
- *                       least this many tiles; 0 = off; applies to tenants
- *                       registered afterwards (0) */
+ *   "narrow_min_tiles"  in a plan that leaves most SMs idle, narrow a member's
+ *                       N tile (256/128/64) until it has this many tiles; 0 = off (20)
+ *   "tall_tiles"        256-row tiles for N <= 128 members of throughput-bound
+ *                       plans (1); "tall_min_tiles": concurrent same-shape tiles
+ *                       that count as throughput-bound (0 = 2 x SMs)
+ *   "split_k"           round programs split few-tile long-K members (0);
+ *                       "max_splits" (4), "split_min_kb" (8)
+ *   "greedy_schedule"   greedy in-order tile claiming instead of static
+ *                       round-robin (0); "dynamic_schedule": per-tenant queues (0)
+ *   "row_fold"          row-folded im2col for RGB stems (1)
+ */
 int gm_ctx_set_option(gm_ctx* ctx, const char* name, int64_t value);
 
 /* Registers a tenant and builds its per-layer member descriptors (TMA maps)

@@ -73,6 +73,7 @@ struct Operator {
   // plan when the plan's full-width tiles cannot fill the SMs
   int narrow_slot[2] = {-1, -1};
   int narrow_w[2] = {0, 0};
+  int tall_slot = -1;  // 256-row x <=128-column variant (tiled / im2col A, M >= 256, N <= 128)
   const void* b_ptr = nullptr;  // weights as the B operand (for the variants' maps)
   int64_t b_k = 0, b_ld = 0;
   bool prepass = false;
@@ -140,6 +141,8 @@ struct Runtime {
   bool row_fold = true;          // S*Cin <= 32 convs (RGB stems) use the row-folded im2col path
   bool dynamic_schedule = false;  // round programs: per-tenant ready queues (else static round-robin)
   bool greedy_schedule = false;   // round programs: greedy in-order tile claiming (else static round-robin)
+  bool tall_tiles = true;         // 256-row tiles for narrow members of throughput-bound plans
+  int64_t tall_min_tiles = 0;     // concurrent same-shape tiles that make a member "throughput-bound" (0 = 2 x SMs)
   int bn = 256;     // N tile of the super-kernel (== DeviceSpec.tile_n)
   int smem_bytes = 0;
   const void* kernel = nullptr;
@@ -460,6 +463,17 @@ struct Runtime {
           ++v;
         }
       }
+      // tall variant: two 128-row halves per tile sharing the B box
+      if (op.kind != GM_LAYER_DWCONV && op.b_ptr && op.shape.m >= 2 * dev::kBM && op.shape.n <= 128 &&
+          (md.a_mode == dev::kATiled || md.a_mode == dev::kAIm2col) && a_box_rows(op.shape.m) == dev::kBM) {
+        dev::MemberDesc md3 = md;
+        md3.tall = 1;
+        md3.n_tile = 128;  // the second half's accumulator starts at column 128 of the tile's buffer
+        md3.tx_bytes = static_cast<uint32_t>((2 * dev::kBM + b_box_rows(op.shape.n, op.n_tile)) * dev::kBK * 2);
+        op.tall_slot = static_cast<int>(host_desc.size() + descs.size());
+        descs.push_back(md3);
+        slot_of_new.push_back(f_index);
+      }
       if (host_desc.size() + descs.size() > 0x10000)
         throw std::invalid_argument("register_tenant: too many registered operators");
       fresh.push_back(op);
@@ -515,9 +529,12 @@ struct Runtime {
   // plan_tiles full-width tiles: when the plan leaves most SMs idle, a member
   // with few tiles uses a narrower-N variant (256 -> 128 -> 64) until it has
   // narrow_min_tiles tiles -- more SMs share the plan's long K loops.
-  std::pair<int, int> variant(int f, int64_t plan_tiles) const {
+  std::pair<int, int> variant(int f, int64_t plan_tiles, int64_t concurrent = 0) const {
     const Operator& op = flat[f];
     int slot = op.slot, w = op.n_tile;
+    // throughput-bound (many tiles of this shape run at once): tall tiles
+    if (tall_tiles && op.tall_slot >= 0 && concurrent >= (tall_min_tiles > 0 ? tall_min_tiles : 2 * sms))
+      return {op.tall_slot, w};
     if (narrow_min_tiles <= 0 || 2 * plan_tiles > sms) return {slot, w};  // the plan fills half the SMs already
     const int64_t mt = (op.shape.m + dev::kBM - 1) / dev::kBM;
     for (int i = 0; i < 2 && op.narrow_slot[i] >= 0; ++i) {
@@ -527,6 +544,7 @@ struct Runtime {
     }
     return {slot, w};
   }
+  bool is_tall(int slot) const { return host_desc[slot].tall != 0; }
   int64_t full_tiles(int f) const {
     const Operator& op = flat[f];
     return ((op.shape.m + dev::kBM - 1) / dev::kBM) * ((op.shape.n + op.n_tile - 1) / op.n_tile);
@@ -549,8 +567,9 @@ struct Runtime {
     for (int f : members) plan_tiles += full_tiles(f);
     for (int f : members) {
       const Operator& op = flat[f];
-      const auto [slot, w] = variant(f, plan_tiles);
-      const int64_t mt = (op.shape.m + dev::kBM - 1) / dev::kBM;
+      const auto [slot, w] = variant(f, plan_tiles, plan_tiles);
+      const int64_t tm = dev::kBM << (is_tall(slot) ? 1 : 0);
+      const int64_t mt = (op.shape.m + tm - 1) / tm;
       const int64_t nt = (op.shape.n + w - 1) / w;
       for (int64_t a = 0; a < mt; ++a)
         for (int64_t b = 0; b < nt; ++b)
@@ -584,12 +603,18 @@ struct Runtime {
     std::vector<uint32_t> targets;
     std::unordered_map<int, int> last_instance;  // flat op -> instance id
     int n_ws = 0;
+    // Concurrency estimate per shape: tenants run their chains in step, so
+    // all members of a shape across the round's plans are in flight together.
+    std::map<Shape, int64_t> shape_tiles;
+    for (const auto& pl : plans)
+      for (int f : pl) shape_tiles[flat[f].shape] += full_tiles(f);
     for (const auto& pl : plans) {
       int64_t plan_tiles = 0;
       for (int f : pl) plan_tiles += full_tiles(f);
       for (int f : pl) {
         const Operator& op = flat[f];
-        const auto [slot, w] = variant(f, plan_tiles);
+        auto [slot, w] = variant(f, plan_tiles, shape_tiles[op.shape]);
+        const bool tall = is_tall(slot);
         const int inst = static_cast<int>(targets.size());
         int dep = -1;
         if (op.layer > 0) {
@@ -597,13 +622,13 @@ struct Runtime {
           if (prev != last_instance.end()) dep = prev->second;
         }
         last_instance[f] = inst;
-        const int64_t mt = (op.shape.m + dev::kBM - 1) / dev::kBM;
+        const int64_t mt = (op.shape.m + (dev::kBM << (tall ? 1 : 0)) - 1) / (dev::kBM << (tall ? 1 : 0));
         const int64_t nt = (op.shape.n + w - 1) / w;
         const int kb = static_cast<int>((op.shape.k + dev::kBK - 1) / dev::kBK);
         // Split-K when the plan cannot fill the SMs and the K loop is long:
         // about two waves of tiles, at least 4 k-blocks per split.
         int splits = 1;
-        if (split_k && plan_tiles < sms && kb >= 2 * split_min_kb) {
+        if (split_k && !tall && plan_tiles < sms && kb >= 2 * split_min_kb) {
           splits = static_cast<int>(
               std::min<int64_t>({kb / split_min_kb, (sms + plan_tiles - 1) / plan_tiles, max_splits}));
           const int chunk = (kb + splits - 1) / splits;
@@ -952,6 +977,11 @@ int gm_ctx_set_option(gm_ctx* ctx, const char* name, int64_t value) {
   } else if (n == "split_min_kb") {
     if (value < 1 || value > 1024) throw std::invalid_argument("split_min_kb must be in [1, 1024]");
     rt.split_min_kb = value;
+  } else if (n == "tall_min_tiles") {
+    if (value < 0) throw std::invalid_argument("tall_min_tiles must be >= 0");
+    rt.tall_min_tiles = value;
+  } else if (n == "tall_tiles") {
+    rt.tall_tiles = value != 0;  // applies to plans prepared afterwards
   } else if (n == "greedy_schedule") {
     rt.greedy_schedule = value != 0;  // applies to round programs prepared afterwards
   } else if (n == "narrow_min_tiles") {

@@ -28,6 +28,8 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace gmb {
 namespace dev {
 
@@ -88,6 +90,12 @@ struct alignas(128) MemberDesc {
   int32_t n_tile;       // output columns per tile (<= BN): narrower for few-tile members
   int32_t taps;         // narrow im2col: R*S filter taps
   int32_t images;       // narrow im2col: batch (an out-of-range image zero-fills a box)
+  // Tall tile (N tile <= 128, tiled / im2col A only): 256 output rows as two
+  // 128-row halves sharing one B box -- two A boxes per k-block, two UMMAs
+  // per K step into accumulator columns [0, n_tile) and [n_tile, 2 n_tile).
+  // Doubles the work per k-block of a narrow tile, whose k-block rate is set
+  // by operand latency, not by the tensor pipe.
+  int32_t tall;
   // depthwise members: raw operands and geometry (x NHWC [b, H, W, C],
   // w [C, ldw] with R*S taps per row, y [b*P*Q, C])
   const __nv_bfloat16* dx;
@@ -469,8 +477,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kb_lo = te.kb_end ? te.kb_begin : 0;
         const int k_blocks = te.kb_end ? te.kb_end : md->k_blocks;
         const uint32_t tx = md->tx_bytes;
-        const int m0 = te.m_tile * kBM;
+        const int tall = md->tall;
+        const int m0 = te.m_tile * (kBM << tall);
         const int n0 = te.n_tile * md->n_tile;
+        const uint32_t b_off = static_cast<uint32_t>(kABytes << tall);
         const bool narrow = md->a_mode == kAIm2colNarrow;
         const bool fold = md->a_mode == kAIm2colFold;
         const bool im2col = md->a_mode != kATiled;
@@ -484,6 +494,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           w0 = fold ? q0 : q0 * md->stride - md->pad;  // folded columns are already strided
           c_blocks = md->c_blocks;
           s_taps = md->s_taps;
+        }
+        int img1 = 0, h1 = 0, w1 = 0;  // tall tiles: the second 128-row half
+        if (tall && im2col) {
+          const int m1 = m0 + kBM;
+          img1 = m1 / md->pq;
+          const int rem = m1 - img1 * md->pq;
+          const int p1 = rem / md->q;
+          const int q1 = rem - p1 * md->q;
+          h1 = p1 * md->stride - md->pad;
+          w1 = q1 * md->stride - md->pad;
         }
         // TMA im2col coordinates advance incrementally (load_a runs in k-block
         // order within a tile): no integer divisions on the producer's path
@@ -521,6 +541,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else if (im2col) {
             tma_load_im2col(a_dst, amap, &full[st], cb * kBK, w0, h0, img, static_cast<uint16_t>(s_),
                             static_cast<uint16_t>(r_));
+            if (tall)
+              tma_load_im2col(a_dst + kABytes, amap, &full[st], cb * kBK, w1, h1, img1, static_cast<uint16_t>(s_),
+                              static_cast<uint16_t>(r_));
             if (++cb == c_blocks) {
               cb = 0;
               if (++s_ == s_taps) {
@@ -530,10 +553,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           } else {
             tma_load_2d(a_dst, amap, &full[st], kb * kBK, m0);
+            if (tall) tma_load_2d(a_dst + kABytes, amap, &full[st], kb * kBK, m0 + kBM);
           }
         };
         auto load_b = [&](int kb, uint32_t st) {
-          tma_load_2d(ring + st * C::kStageBytes + kABytes, &md->b, &full[st], kb * kBK, n0);
+          tma_load_2d(ring + st * C::kStageBytes + b_off, &md->b, &full[st], kb * kBK, n0);
         };
         // Activation gate: the prerequisite grid (PDL) before the first tile,
         // and in a round program the tenant's previous layer (all its tiles
@@ -575,14 +599,63 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if (greedy) next = static_cast<int>(atomicAdd(ra.next_tile, 1u));  // latency hides under the loads
-        for (; kb < k_blocks; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], tx);
-          load_a(kb, stage);
-          load_b(kb, stage);
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
+        // Steady state, specialised per A mode and tile height so the
+        // per-k-block issue path (a single thread: it bounds narrow tiles)
+        // carries no mode tests.
+        auto steady = [&](auto mode_c, auto tall_c) {
+          constexpr int kMode = decltype(mode_c)::value;
+          constexpr int kTall = decltype(tall_c)::value;
+          for (; kb < k_blocks; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint64_t* bar = &full[stage];
+            mbar_expect_tx(bar, tx);
+            uint8_t* a_dst = ring + stage * C::kStageBytes;
+            if constexpr (kMode == kATiled) {
+              tma_load_2d(a_dst, amap, bar, kb * kBK, m0);
+              if constexpr (kTall) tma_load_2d(a_dst + kABytes, amap, bar, kb * kBK, m0 + kBM);
+            } else {
+              tma_load_im2col(a_dst, amap, bar, cb * kBK, w0, h0, img, static_cast<uint16_t>(s_),
+                              static_cast<uint16_t>(r_));
+              if constexpr (kTall)
+                tma_load_im2col(a_dst + kABytes, amap, bar, cb * kBK, w1, h1, img1, static_cast<uint16_t>(s_),
+                                static_cast<uint16_t>(r_));
+              if (++cb == c_blocks) {
+                cb = 0;
+                if (++s_ == s_taps) {
+                  s_ = 0;
+                  ++r_;
+                }
+              }
+            }
+            tma_load_2d(a_dst + kABytes * (1 + kTall), &md->b, bar, kb * kBK, n0);
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        };
+        using I0 = std::integral_constant<int, 0>;
+        using I1 = std::integral_constant<int, 1>;
+        if (md->a_mode == kATiled) {
+          if (tall)
+            steady(std::integral_constant<int, kATiled>{}, I1{});
+          else
+            steady(std::integral_constant<int, kATiled>{}, I0{});
+        } else if (md->a_mode == kAIm2col) {
+          if (tall)
+            steady(std::integral_constant<int, kAIm2col>{}, I1{});
+          else
+            steady(std::integral_constant<int, kAIm2col>{}, I0{});
+        } else {
+          for (; kb < k_blocks; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], tx);
+            load_a(kb, stage);
+            load_b(kb, stage);
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
       }
@@ -613,6 +686,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int k_blocks = __shfl_sync(0xffffffffu, te.kb_end ? te.kb_end : md->k_blocks, 0);
       const uint32_t idesc = __shfl_sync(0xffffffffu, md->idesc, 0);
       const int a_mode = __shfl_sync(0xffffffffu, md->a_mode, 0);
+      const int tall = __shfl_sync(0xffffffffu, md->tall, 0);
+      const uint32_t d_half = static_cast<uint32_t>(__shfl_sync(0xffffffffu, md->n_tile, 0));  // tall: 2nd half's columns
       // Smem descriptors (SM100): lo = start >> 4 | LBO >> 4 << 16, hi = SBO
       // >> 4 | version 1 << 14 | swizzle << 29, built once per tile.  Per
       // UMMA_K step (16 bf16) the A start advances 32 B inside the 128 B
@@ -636,26 +711,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&acc_empty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = kb_lo; kb < k_blocks; ++kb) {
-        mbar_wait(&full[stage], phase);
-        tc_fence_after();
-        if (trace && kb == kb_lo && lane == 0) trace[6 * t + 2] = globaltimer();
-        const uint32_t a_addr = ring_base + stage * C::kStageBytes;
-        const uint32_t a_lo = ((a_addr >> 4) & 0x3FFFu) | a_lbo;
-        const uint32_t b_lo = (((a_addr + kABytes) >> 4) & 0x3FFFu) | (1u << 16);
-        if (elect_one()) {
-          umma_bf16(d_tmem, a_hi64 | a_lo, b_hi64 | b_lo, idesc, kb != kb_lo ? 1u : 0u);
-          umma_bf16(d_tmem, a_hi64 | (a_lo + k1), b_hi64 | (b_lo + 2), idesc, 1u);
-          umma_bf16(d_tmem, a_hi64 | (a_lo + k2), b_hi64 | (b_lo + 4), idesc, 1u);
-          umma_bf16(d_tmem, a_hi64 | (a_lo + k3), b_hi64 | (b_lo + 6), idesc, 1u);
-          umma_commit(&empty[stage]);  // frees the smem stage once these MMAs retire
+      // One k-block: wait for its stage, issue `halves` x 4 UMMA_K steps, free
+      // the stage.  Two loop instances so the common path carries no test.
+      auto kloop = [&](auto halves_c) {
+        constexpr int kHalves = decltype(halves_c)::value;
+        for (int kb = kb_lo; kb < k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (trace && kb == kb_lo && lane == 0) trace[6 * t + 2] = globaltimer();
+          const uint32_t a_addr = ring_base + stage * C::kStageBytes;
+          const uint32_t a_lo = ((a_addr >> 4) & 0x3FFFu) | a_lbo;
+          const uint32_t b_lo = (((a_addr + (kABytes * kHalves)) >> 4) & 0x3FFFu) | (1u << 16);
+          if (elect_one()) {
+#pragma unroll
+            for (int h = 0; h < kHalves; ++h) {
+              // half h: A box at +16 KB * h, accumulator columns + n_tile * h
+              const uint32_t ah = a_lo + h * (kABytes >> 4);
+              const uint32_t dh = d_tmem + h * d_half;
+              umma_bf16(dh, a_hi64 | ah, b_hi64 | b_lo, idesc, kb != kb_lo ? 1u : 0u);
+              umma_bf16(dh, a_hi64 | (ah + k1), b_hi64 | (b_lo + 2), idesc, 1u);
+              umma_bf16(dh, a_hi64 | (ah + k2), b_hi64 | (b_lo + 4), idesc, 1u);
+              umma_bf16(dh, a_hi64 | (ah + k3), b_hi64 | (b_lo + 6), idesc, 1u);
+            }
+            umma_commit(&empty[stage]);  // frees the smem stage once these MMAs retire
+          }
+          __syncwarp();
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
-        __syncwarp();
-        if (++stage == kStages) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
+      };
+      if (tall)
+        kloop(std::integral_constant<int, 2>{});
+      else
+        kloop(std::integral_constant<int, 1>{});
       if (elect_one()) umma_commit(&acc_full[acc]);  // accumulator ready for the epilogue
       __syncwarp();
       if (trace && lane == 0) trace[6 * t + 3] = globaltimer();
@@ -775,7 +865,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!mine) continue;
       const TileEntry te = tiles[t];
       const MemberDesc* md = slots + te.member;
-      const int m0 = te.m_tile * kBM + quarter * 32;
+      const int tall = md->tall;
+      const int m0 = te.m_tile * (kBM << tall) + quarter * 32;
       const int n0 = te.n_tile * md->n_tile;
       const int cols = min(md->n_tile, md->n - n0);
       const int relu = md->relu;
@@ -792,7 +883,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         buf ^= 1;
       };
       // 32 fp32 accumulators of this lane's row -> bf16 -> one 32x32 store box.
-      auto store_bf16 = [&](const uint32_t (&v)[32], int c) {
+      auto store_bf16 = [&](const uint32_t (&v)[32], int c, int mrow) {
         uint8_t* sbuf = claim();
         uint8_t* row = sbuf + lane * 64;
 #pragma unroll
@@ -807,7 +898,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&md->c, sbuf, n0 + c, m0);
+          tma_store_2d(&md->c, sbuf, n0 + c, mrow);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
         issue();
@@ -861,7 +952,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + f.w);
               __stcg(src + j * 32, make_float4(0.f, 0.f, 0.f, 0.f));
             }
-            if (m0 < md->m) store_bf16(v, c);
+            if (m0 < md->m) store_bf16(v, c, m0);
           }
           tc_fence_before();
           mbar_arrive(&acc_empty[acc]);
@@ -873,7 +964,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c = 0; c < cols; c += kEpiChunk) {
             uint32_t v[32];
             tmem_ld32(taddr + c, v);
-            store_bf16(v, c);
+            store_bf16(v, c, m0);
+          }
+        }
+        if (tall && m0 + kBM < md->m) {  // tall tile: the second 128-row half
+          for (int c = 0; c < cols; c += kEpiChunk) {
+            uint32_t v[32];
+            tmem_ld32(taddr + md->n_tile + c, v);
+            store_bf16(v, c, m0 + kBM);
           }
         }
         tc_fence_before();

@@ -16,6 +16,9 @@ from paper_1901_00041_b200.engine import SpaceTimeEngine  # noqa: E402
 def build(config, opts):
     if config == "headline":
         return SpaceTimeEngine([W.resnet50(224)] * 4, [8] * 4, options=opts)
+    if config.startswith("r50x"):  # r50x<T>b<B>: T tenants x ResNet-50 batch B
+        t, b = config[4:].split("b")
+        return SpaceTimeEngine([W.resnet50(224)] * int(t), [int(b)] * int(t), options=opts)
     if config == "mix":
         ms = [W.resnet50(224), W.vgg16(224), W.mobilenet_v2(224)] * 2
         return SpaceTimeEngine(ms, [4] * 6, options=opts)
