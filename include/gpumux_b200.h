@@ -442,6 +442,14 @@ typedef struct gm_serve_config {
   int32_t prewarm;   /* > 0: plan + upload every formable member set before the clock starts
                         (fails if there are more than this many); 0 = plan on first use */
   uint64_t stream;   /* cudaStream_t */
+  /* inject_degradation (sim.cpp:60-68, 98-110): from degrade_start seconds on,
+   * tenant degrade_tenant's observed completions stretch by degrade_slowdown
+   * (a tenant-local post-dispatch delay; the device is not held).  Off when
+   * degrade_slowdown == 0 or degrade_tenant < 0. */
+  int32_t degrade_tenant;
+  int32_t reserved1;
+  double degrade_slowdown;
+  double degrade_start;
 } gm_serve_config;
 
 typedef struct gm_serve_stats {
@@ -454,6 +462,7 @@ typedef struct gm_serve_stats {
   double mean_queries_per_round, mean_round_ms;
   int64_t plan_hits, plan_misses;          /* member-set plan / device-table cache */
   int32_t evicted, reserved0;
+  uint64_t evicted_mask;                   /* bit i: logical tenant i was evicted (i < 64) */
 } gm_serve_stats;
 
 int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, const gm_serve_config* cfg,

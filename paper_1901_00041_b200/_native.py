@@ -114,7 +114,9 @@ class gm_serve_tenant(C.Structure):
 
 class gm_serve_config(C.Structure):
     _fields_ = [("duration", C.c_double), ("warmup", C.c_double), ("max_wait", C.c_double), ("seed", C.c_uint64),
-                ("depth", C.c_int32), ("prewarm", C.c_int32), ("stream", C.c_uint64)]
+                ("depth", C.c_int32), ("prewarm", C.c_int32), ("stream", C.c_uint64),
+                ("degrade_tenant", C.c_int32), ("reserved1", C.c_int32), ("degrade_slowdown", C.c_double),
+                ("degrade_start", C.c_double)]
 
 
 class gm_serve_stats(C.Structure):
@@ -123,7 +125,7 @@ class gm_serve_stats(C.Structure):
                 ("p99_ms", C.c_double), ("max_ms", C.c_double), ("mean_ms", C.c_double),
                 ("slo_violation_frac", C.c_double), ("mean_queries_per_round", C.c_double),
                 ("mean_round_ms", C.c_double), ("plan_hits", C.c_int64), ("plan_misses", C.c_int64),
-                ("evicted", C.c_int32), ("reserved0", C.c_int32)]
+                ("evicted", C.c_int32), ("reserved0", C.c_int32), ("evicted_mask", C.c_uint64)]
 
 
 _SIGS = {

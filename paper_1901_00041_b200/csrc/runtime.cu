@@ -1350,6 +1350,11 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
   Runtime& rt = runtime_of(ctx);
   cuda_check(cudaSetDevice(rt.device), "cudaSetDevice");
   if (cfg->prewarm < 0) throw std::invalid_argument("serve: prewarm cap must be >= 0");
+  // degradation is off when degrade_slowdown == 0 (a zero-initialised config)
+  const int deg_t = cfg->degrade_slowdown != 0.0 ? cfg->degrade_tenant : -1;
+  if (deg_t >= static_cast<int>(n)) throw std::invalid_argument("serve: degradation names unknown tenant");
+  if (deg_t >= 0 && cfg->degrade_slowdown < 1.0) throw std::invalid_argument("serve: degradation slowdown must be >= 1");
+  const int64_t deg_start_ns = deg_t >= 0 ? to_ns(cfg->degrade_start) : 0;
   if (cfg->duration <= 0 || cfg->warmup < 0 || cfg->warmup >= cfg->duration)
     throw std::invalid_argument("serve: need 0 <= warmup < duration");
   const int depth = std::max(1, cfg->depth);
@@ -1363,6 +1368,7 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
     int conc = 0;
     int64_t flops = 0;
     std::deque<int64_t> pending;
+    std::vector<int64_t> delayed;  // closed-loop re-arrivals after a degraded (delayed) completion
     int64_t next_arrival = 0;
     std::mt19937_64 rng;
     bool live = true;
@@ -1467,12 +1473,22 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
   double round_ms_sum = 0;
   double predicted_s = 0;  // EWMA of measured round device time (SLO trigger)
   int evicted = 0;
+  uint64_t evicted_mask = 0;
   const auto t0 = std::chrono::steady_clock::now();
 
   for (;;) {
     int64_t now = since(t0);
     // arrivals (stop admitting at the end of the window)
     for (T& t : ts) {
+      if (!t.delayed.empty() && t.live) {
+        auto keep = t.delayed.begin();
+        for (int64_t a : t.delayed)
+          if (a <= now)
+            t.pending.push_back(a);
+          else
+            *keep++ = a;
+        t.delayed.erase(keep, t.delayed.end());
+      }
       if (!t.live || t.rate <= 0) continue;
       while (t.next_arrival <= now && t.next_arrival < duration_ns) {
         t.pending.push_back(t.next_arrival);
@@ -1492,24 +1508,36 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
       predicted_s = rounds == 1 && predicted_s == 0 ? ms * 1e-3 : 0.8 * predicted_s + 0.2 * ms * 1e-3;
       for (auto& [ti, arr] : r.members) {
         T& t = ts[ti];
+        // a degraded tenant's completion is observed exec x slowdown after its
+        // dispatch (completion_with_degradation, sim.cpp:105-110)
+        const bool deg = static_cast<int>(ti) == deg_t && r.dispatch_ns >= deg_start_ns && cfg->degrade_slowdown > 1.0;
+        const double exec_s = ms * 1e-3 * (deg ? cfg->degrade_slowdown : 1.0);
+        const int64_t seen = deg ? done + std::llround(ms * 1e6 * (cfg->degrade_slowdown - 1.0)) : done;
         for (int64_t a : arr) {
-          const double l = (done - a) * 1e-6;
-          if (a >= warmup_ns && done <= duration_ns) {
+          const double l = (seen - a) * 1e-6;
+          if (a >= warmup_ns && seen <= duration_ns) {
             lat_ms.push_back(l);
             ++queries;
             flops_done += t.flops;
             if (l * 1e-3 > t.slo) ++slo_miss;
           }
-          if (t.rate <= 0 && t.live && done < duration_ns) t.pending.push_back(done);  // closed loop
+          if (t.rate <= 0 && t.live && seen < duration_ns) {  // closed loop: the next query
+            if (seen <= done)
+              t.pending.push_back(seen);
+            else
+              t.delayed.push_back(seen);
+          }
         }
-        if (!health[ti].evicted) observe(health[ti], ms * 1e-3);
+        if (!health[ti].evicted) observe(health[ti], exec_s);
       }
       if (ctx->det.evict_stragglers) {
         for (int s : stragglers(health, ctx->det.threshold_ratio, ctx->det.min_observations)) {
           health[s].evicted = true;  // terminal (scheduler.cpp:225-244): pending queries are cancelled
           ts[s].live = false;
           ts[s].pending.clear();
+          ts[s].delayed.clear();
           ++evicted;
+          evicted_mask |= 1ull << std::min<int>(s, 63);
         }
       }
       now = since(t0);
@@ -1597,6 +1625,7 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
   out->plan_hits = plan_hits;
   out->plan_misses = plan_misses;
   out->evicted = evicted;
+  out->evicted_mask = evicted_mask;
   if (n_lat) *n_lat = lat_ms.size();
   if (latencies_ms && cap) std::copy(lat_ms.begin(), lat_ms.begin() + std::min(cap, lat_ms.size()), latencies_ms);
   GM_API_END

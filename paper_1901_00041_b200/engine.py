@@ -298,7 +298,12 @@ class ServingEngine:
         return sum(L.flops(1) for L in self.specs[i].layers)
 
     def serve(self, duration: float, warmup: float = 0.1, max_wait: float = -1.0, depth: int = 1,
-              seed: int = 42, stream: Optional[torch.cuda.Stream] = None, prewarm: int = 4096) -> ServeResult:
+              seed: int = 42, stream: Optional[torch.cuda.Stream] = None, prewarm: int = 4096,
+              degrade: Optional[Tuple[int, float, float]] = None) -> ServeResult:
+        """``degrade`` = (tenant, slowdown, start_s): inject_degradation
+        (sim.cpp:60-68) on real hardware -- that tenant's observed completions
+        stretch by ``slowdown`` from ``start_s`` on, feeding the straggler
+        monitor, which evicts it (terminal)."""
         n = len(self.specs)
         arr = (N.gm_serve_tenant * n)()
         keep = []
@@ -309,8 +314,9 @@ class ServingEngine:
             arr[i] = N.gm_serve_tenant(len(vs), tid, bat, float(spec.rate_qps), int(spec.concurrency), 0,
                                        float(spec.slo_latency), self.flops_per_query(i))
         s = stream or torch.cuda.Stream(self.device)
+        dt, dslow, dstart = degrade if degrade is not None else (-1, 1.0, 0.0)
         cfg = N.gm_serve_config(float(duration), float(warmup), float(max_wait), int(seed), int(depth),
-                                int(prewarm), int(s.cuda_stream))
+                                int(prewarm), int(s.cuda_stream), int(dt), 0, float(dslow), float(dstart))
         out = N.gm_serve_stats()
         cap = 1 << 20
         lat = (C.c_double * cap)()

@@ -66,3 +66,17 @@ def test_served_outputs_match_direct_round():
     torch.cuda.synchronize()
     for a, m in zip(served, eng.models):
         assert torch.equal(a, m.query_output)
+
+
+def test_degraded_tenant_is_detected_and_evicted():
+    """inject_degradation on real hardware (sim.cpp:60-68, 98-110): tenant 1's
+    observed completions stretch x3 after 0.1 s; the EWMA monitor flags it
+    against the median of its peers (detect_stragglers, scheduler.cpp:246-271)
+    and evicts it -- terminal, its queries stop while the others keep serving."""
+    eng = _engine(concurrency=1, slo_latency=0.5)
+    r = eng.serve(duration=0.8, warmup=0.05, degrade=(1, 3.0, 0.1))
+    s = r.stats
+    assert s["evicted"] == 1 and s["evicted_mask"] == 0b10
+    assert s["queries"] > 50  # tenants 0 and 2 kept serving
+    clean = eng.serve(duration=0.4, warmup=0.05)
+    assert clean.stats["evicted"] == 0
