@@ -134,6 +134,24 @@ def b200_profile() -> DeviceSpec:
     return DeviceSpec._from(c)
 
 
+def b200_calibrated_profile(path: Optional[str] = None) -> DeviceSpec:
+    """The b200 profile with peak_flops / mem_bandwidth / launch_overhead fitted
+    to measured super-kernel times (tools/calibrate_b200.py writes
+    profiles/b200_calibrated.json).  Falls back to the
+    nominal profile when no calibration exists.  Tile shape and slot count are
+    the kernel's, so plans stay those of b200_profile()."""
+    import json
+    import os
+    path = path or os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                                "b200_calibrated.json")
+    spec = b200_profile()
+    if os.path.exists(path):
+        with open(path) as f:
+            for k, v in json.load(f)["fitted"].items():
+                setattr(spec, k, v)
+    return spec
+
+
 # ---------------------------------------------------------------- cost model
 
 @dataclass

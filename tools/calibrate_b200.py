@@ -1,0 +1,119 @@
+"""Calibrate the b200 DeviceSpec against measured super-kernel times
+(the reference's calibrator fits simulator knobs to
+targets by coordinate descent, proj/src/calibrate.cpp:64-146).
+
+Each formed super-kernel of several workloads is launched on its own
+(``packed_per_plan``: one launch per plan, CUDA-event timed in a graph) and
+its time compared with ``dispatch_duration`` (cost_model.cpp:18-46) under a
+candidate spec.  Coordinate descent over peak_flops, mem_bandwidth and
+launch_overhead minimises the mean squared log error; the result goes to
+profiles/b200_calibrated.json, which ``scheduler.b200_calibrated_profile()``
+loads, so SLO predictions and wake timers (slo_headroom, the batcher's SLO
+trigger) use measured B200 behaviour instead of nominal peaks.
+
+  python tools/calibrate_b200.py            # needs a B200
+"""
+import json
+import math
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_1901_00041_b200 import workload as W  # noqa: E402
+from paper_1901_00041_b200.engine import SpaceTimeEngine  # noqa: E402
+from paper_1901_00041_b200.scheduler import (KernelGroup, b200_profile, dispatch_duration,  # noqa: E402
+                                             GemmShape)
+
+FIT = ("peak_flops", "mem_bandwidth", "launch_overhead")
+
+
+def measure(engines):
+    samples = []  # (groups, measured seconds)
+    s = torch.cuda.Stream()
+    for name, eng in engines:
+        rnd = eng.plan_round()
+        g = eng.capture_packed(rnd, timed=True)
+        for _ in range(3):
+            g.launch(s.cuda_stream)
+        acc = None
+        reps = 5
+        for _ in range(reps):
+            g.launch(s.cuda_stream)
+            t = g.kernel_times_ms()
+            acc = t if acc is None else [a + b for a, b in zip(acc, t)]
+        for k, ms in zip(rnd.kernels, acc):
+            groups = []
+            for r in k.members:
+                sh = GemmShape(r.shape.m, r.shape.n, r.shape.k)
+                if groups and groups[-1].shape == sh:
+                    groups[-1].count += 1
+                else:
+                    groups.append(KernelGroup(sh, 1))
+            samples.append((name, groups, ms / reps / 1e3))
+        del g
+    return samples
+
+
+def loss(spec, samples):
+    err = []
+    for _, groups, t in samples:
+        p = dispatch_duration(groups, spec, spec.slot_total(), 1).duration
+        err.append(math.log(p / t) ** 2)
+    return sum(err) / len(err)
+
+
+def rel_errors(spec, samples):
+    out = []
+    for _, groups, t in samples:
+        p = dispatch_duration(groups, spec, spec.slot_total(), 1).duration
+        out.append(abs(p - t) / t)
+    out.sort()
+    return out[len(out) // 2], out[int(0.9 * (len(out) - 1))]
+
+
+def main():
+    engines = [("resnet50x4b8", SpaceTimeEngine([W.resnet50(224)] * 4, [8] * 4)),
+               ("bert16b4", SpaceTimeEngine([W.bert_base_gemms(128, 2)] * 16, [4] * 16)),
+               ("conv2_2x32", SpaceTimeEngine([W.conv2_2()] * 32, [1] * 32)),
+               ("mobilenetv2x4b8", SpaceTimeEngine([W.mobilenet_v2(224)] * 4, [8] * 4))]
+    samples = measure(engines)
+    spec = b200_profile()
+    before = rel_errors(spec, samples)
+    best = loss(spec, samples)
+    step = 2.0
+    for _ in range(40):
+        improved = False
+        for f in FIT:
+            for mul in (step, 1.0 / step):
+                cand = b200_profile()
+                for g in FIT:
+                    setattr(cand, g, getattr(spec, g))
+                setattr(cand, f, getattr(spec, f) * mul)
+                l_ = loss(cand, samples)
+                if l_ < best:
+                    best, spec, improved = l_, cand, True
+        if not improved:
+            step = math.sqrt(step)
+            if step < 1.001:
+                break
+    after = rel_errors(spec, samples)
+    out = {
+        "fitted": {f: getattr(spec, f) for f in FIT},
+        "spec": spec.as_dict(),
+        "samples": len(samples),
+        "workloads": [n for n, _ in engines],
+        "median_rel_err": {"nominal": before[0], "calibrated": after[0]},
+        "p90_rel_err": {"nominal": before[1], "calibrated": after[1]},
+        "method": "coordinate descent on mean squared log error of dispatch_duration vs per-plan CUDA-event "
+                  "times (packed_per_plan launches, 5 replays)",
+    }
+    os.makedirs("profiles", exist_ok=True)
+    with open("profiles/b200_calibrated.json", "w") as f:
+        json.dump(out, f, indent=1)
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
