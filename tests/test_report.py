@@ -1,0 +1,35 @@
+"""CSV v1 emitter of measured runs against the
+reference's schema (proj/include/gpumux/csv.hpp:13-16, csv.cpp:10-41)."""
+import json
+import os
+import re
+
+from refshim import ROOT
+
+from paper_1901_00041_b200 import report
+
+
+def test_header_is_the_reference_contract():
+    ref = "/root/reference/proj/include/gpumux/csv.hpp"
+    if os.path.exists(ref):
+        text = open(ref).read()
+        parts = re.findall(r'"([^"]*)"', text[text.index("kCsvHeader"):text.index(";", text.index("kCsvHeader"))])
+        assert report.CSV_HEADER == "".join(parts)
+    assert report.CSV_HEADER.count(",") == 16
+
+
+def test_line_format_matches_csv_cpp():
+    ok = report.csv_line("w", "space-time", 4, 8, 42, "ok", {"throughput_gflops": 349248.45937, "p99_ms": 0.7493,
+                                                            "launches": 1})
+    f = ok.split(",")
+    assert len(f) == 17 and f[:7] == ["1", "w", "space-time", "4", "8", "42", "ok"]
+    assert f[7] == "349248.459" and f[11] == "0.7493" and f[14] == "1"
+    bad = report.csv_line("w", "time-mux", 4, 8, 42, "oom")
+    assert bad.endswith(",oom" + "," * 10) and len(bad.split(",")) == 17
+
+
+def test_bench_line_rows():
+    line = json.loads(open(os.path.join(ROOT, "profiles", "r01c_bench_line.json")).read())
+    rows = report.bench_rows(line)
+    assert len(rows) == 3 + 3 * len(line["table1"]["rows"])
+    assert {r.split(",")[2] for r in rows} == {"space-time", "time-mux", "space-implicit"}
