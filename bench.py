@@ -40,6 +40,7 @@ def parse_args():
     ap.add_argument("--table1", default="2,4,8,10,16,20,32,40,64,80,100,120",
                     help="R values of the conv2_2 microbench sweep ('' to skip)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--csv", default="", help="also write the reference's CSV v1 rows (report.py) to this path")
     ap.add_argument("--extra", default="mix,bert",
                     help="extra BASELINE configs at N=1: mix (configs[2]) and bert (configs[3]); '' to skip")
     ap.add_argument("--serve-seconds", type=float, default=1.5,
@@ -487,6 +488,9 @@ def run_ours(args):
     for name, sec in extra.items():
         line["config_" + name] = sec
     print(json.dumps(line), flush=True)
+    if args.csv:
+        from paper_1901_00041_b200 import report
+        report.write_csv(args.csv, report.bench_rows(line))
     if world > 1:
         dist.destroy_process_group()
     return 0
