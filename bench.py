@@ -475,7 +475,7 @@ def run_ours(args):
         },
         "e2e": {"value": world * flops_round / e2e_s / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
-                "api": "SpaceTimeEngine.serve_round (H2D, steady-state cached plan, graph replay, D2H), pinned host buffers"},
+                "api": "SpaceTimeEngine.serve_round (steady-state plan; one graph: per-tenant H2D gating its chain in the round kernel, D2H), pinned host buffers"},
         "gpu_launches": args.steps * g_packed.kernels,
         "clocks": clocks.summary(),
     }

@@ -402,6 +402,16 @@ int gm_graph_capture_round(gm_ctx* ctx, const gm_plans* p, int timed, gm_graph**
  * (member = registered slot, flags = plan index). */
 int gm_trace_round(gm_ctx* ctx, const gm_plans* p, uint64_t stream, uint64_t* out, size_t cap, size_t* n_tiles);
 int gm_round_tiles(gm_ctx* ctx, const gm_plans* p, gm_tile* out, size_t cap, size_t* n);
+/* End-to-end round program (the serving call with host buffers): per tenant
+ * i, an H2D copy h_in[i] -> d_in[i] (its query batch) and its layer-0
+ * pre-pass run on a copy branch that then opens the tenant's input gate; the
+ * round kernel runs concurrently and starts each tenant's chain when its
+ * gate opens; D2H copies d_out[i] -> h_out[i] follow the kernel.  Host
+ * buffers should be pinned; the graph is bound to these pointers. */
+int gm_graph_capture_round_e2e(gm_ctx* ctx, const gm_plans* p, size_t n, const int32_t* tenants,
+                               const void* const* h_in, void* const* d_in, const size_t* in_bytes,
+                               const void* const* d_out, void* const* h_out, const size_t* out_bytes,
+                               gm_graph** out);
 int gm_graph_launch(gm_graph* g, uint64_t stream);
 int gm_graph_launch_count(const gm_graph* g, int32_t* superkernels, int32_t* kernels);
 /* timed graphs: synchronizes on the last launch and returns the elapsed ms of

@@ -211,6 +211,9 @@ _SIGS = {
     "gm_graph_capture_round": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, P(C.c_void_p)]),
     "gm_trace_round": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, P(C.c_uint64), C.c_size_t, P(C.c_size_t)]),
     "gm_round_tiles": (C.c_int, [C.c_void_p, C.c_void_p, P(gm_tile), C.c_size_t, P(C.c_size_t)]),
+    "gm_graph_capture_round_e2e": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, P(C.c_int32), P(C.c_void_p),
+                                             P(C.c_void_p), P(C.c_size_t), P(C.c_void_p), P(C.c_void_p),
+                                             P(C.c_size_t), P(C.c_void_p)]),
     "gm_graph_launch": (C.c_int, [C.c_void_p, C.c_uint64]),
     "gm_graph_launch_count": (C.c_int, [C.c_void_p, P(C.c_int32), P(C.c_int32)]),
     "gm_graph_kernel_times": (C.c_int, [C.c_void_p, P(C.c_float), C.c_size_t, P(C.c_size_t)]),

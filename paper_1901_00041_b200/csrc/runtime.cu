@@ -104,6 +104,11 @@ struct Prepared {
   int32_t* qinfo = nullptr;  // [nq] begins then [nq] lengths
   int nq = 0;
   bool greedy = false;  // greedy in-order claiming (one claim counter after the counters and queue heads)
+  // input-gated round programs (end-to-end serving): per tenant, a counter
+  // (target 1) its first layer depends on, set by a 4-byte DMA after the
+  // tenant's H2D copy (and layer-0 pre-pass) on a side stream
+  std::vector<std::pair<int, int>> gates;  // (tenant, counter index)
+  std::vector<int> gated_prepass;          // layer-0 pre-pass ops, run per tenant on the copy stream
 
   void release() {
     cudaFree(qinfo);
@@ -144,6 +149,7 @@ struct Runtime {
   bool tall_tiles = true;         // 256-row tiles for narrow members of throughput-bound plans
   int64_t tall_min_tiles = 0;     // concurrent same-shape tiles that make a member "throughput-bound" (0 = 2 x SMs)
   int bn = 256;     // N tile of the super-kernel (== DeviceSpec.tile_n)
+  uint32_t* host_one = nullptr;  // pinned 4-byte 1: DMA source that opens an input gate
   int smem_bytes = 0;
   const void* kernel = nullptr;
 
@@ -158,6 +164,7 @@ struct Runtime {
       cudaFree(op.wpad);
     }
     cudaFree(d_desc);
+    cudaFreeHost(host_one);
   }
 
   void init(int dev_index, const Device& spec) {
@@ -187,6 +194,8 @@ struct Runtime {
     }
     cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes),
                "cudaFuncSetAttribute");
+    cuda_check(cudaHostAlloc(&host_one, sizeof(uint32_t), cudaHostAllocDefault), "cudaHostAlloc");
+    *host_one = 1;
   }
 
   // [rows, cols] bf16 row-major with row stride ld (elements), box kBK x box_rows.
@@ -587,8 +596,8 @@ struct Runtime {
   // Round program: every plan of a round, in plan order, as ONE persistent
   // launch.  Member instances get completion counters; a member depends on the
   // same tenant's previous layer when that layer ran earlier in the round.
-  Prepared& prepare_round(const std::vector<std::vector<int>>& plans) {
-    std::string key = "R";
+  Prepared& prepare_round(const std::vector<std::vector<int>>& plans, bool gated = false) {
+    std::string key = gated ? "G" : "R";
     for (const auto& pl : plans) {
       for (int f : pl) {
         key += std::to_string(f);
@@ -620,6 +629,11 @@ struct Runtime {
         if (op.layer > 0) {
           auto prev = last_instance.find(tenant_ops[op.tenant][op.layer - 1]);
           if (prev != last_instance.end()) dep = prev->second;
+        } else if (gated) {
+          // the tenant's query input: gate counter (target 1), set after its H2D
+          dep = static_cast<int>(targets.size());
+          targets.push_back(1);
+          p.gates.emplace_back(op.tenant, dep);
         }
         last_instance[f] = inst;
         const int64_t mt = (op.shape.m + (dev::kBM << (tall ? 1 : 0)) - 1) / (dev::kBM << (tall ? 1 : 0));
@@ -651,7 +665,7 @@ struct Runtime {
                                              static_cast<uint16_t>(std::min(kb, (s + 1) * chunk)), n_ws});
             ++n_ws;
           }
-        if (op.prepass) p.prepass_ops.push_back(f);
+        if (op.prepass) (gated && op.layer == 0 ? p.gated_prepass : p.prepass_ops).push_back(f);
       }
       p.tile_plan.resize(table.size(), static_cast<uint16_t>(&pl - plans.data()));
     }
@@ -732,6 +746,9 @@ struct Runtime {
     return (folds + kFoldJobs - 1) / kFoldJobs + other;
   }
   int launch_prepasses(const Prepared& p, cudaStream_t stream, bool count) {
+    return launch_prepass_ops(p.prepass_ops, stream, count);
+  }
+  int launch_prepass_ops(const std::vector<int>& ops, cudaStream_t stream, bool count) {
     int launches = 0;
     dev::FoldBatch fb{};
     int nj = 0, max_pixels = 0;
@@ -745,7 +762,7 @@ struct Runtime {
       nj = 0;
       max_pixels = 0;
     };
-    for (int f : p.prepass_ops) {
+    for (int f : ops) {
       const Operator& op = flat[f];
       const Conv& c = op.conv;
       const int H = static_cast<int>(c.image_h), W = static_cast<int>(c.image_w), Cin = static_cast<int>(c.in_channels);
@@ -1259,6 +1276,59 @@ int gm_graph_capture_round(gm_ctx* ctx, const gm_plans* p, int timed, gm_graph**
     g.kernels += rt.launch(*pr, cs, false, ev.first, ev.second);
     g.superkernels += 1;
     g.tiles += pr->n_tiles;
+  });
+  GM_API_END
+}
+
+int gm_graph_capture_round_e2e(gm_ctx* ctx, const gm_plans* p, size_t n, const int32_t* tenants,
+                               const void* const* h_in, void* const* d_in, const size_t* in_bytes,
+                               const void* const* d_out, void* const* h_out, const size_t* out_bytes,
+                               gm_graph** out) {
+  GM_API_BEGIN
+  if (!p || !out || (n && (!tenants || !h_in || !d_in || !in_bytes || !d_out || !h_out || !out_bytes)))
+    throw std::invalid_argument("null argument");
+  Runtime& rt = runtime_of(ctx);
+  std::vector<std::vector<int>> plans;
+  for (const Plan& plan : p->plans) plans.push_back(members_of(rt, plan));
+  Prepared* pr = &rt.prepare_round(plans, true);
+  for (size_t i = 0; i < n; ++i) {
+    bool found = false;
+    for (const auto& gt : pr->gates) found |= gt.first == tenants[i];
+    if (!found) throw std::invalid_argument("e2e round: tenant " + std::to_string(tenants[i]) + " is not in the round");
+  }
+  *out = capture(ctx, [&](cudaStream_t cs, gm_graph& g) {
+    // copy branch: each tenant's H2D, its layer-0 pre-pass, then the gate
+    // DMA; the round kernel runs concurrently and starts a tenant's chain as
+    // soon as its gate opens (the pre-pass blocks co-reside with the
+    // persistent CTAs: 31 registers x 256 threads fit the SM's spare file)
+    cudaStream_t ss;
+    cuda_check(cudaStreamCreateWithFlags(&ss, cudaStreamNonBlocking), "cudaStreamCreate");
+    g.streams.push_back(ss);
+    cudaEvent_t fork, join;
+    cuda_check(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaEventCreateWithFlags(&join, cudaEventDisableTiming), "cudaEventCreate");
+    g.joins.push_back(fork);
+    g.joins.push_back(join);
+    cuda_check(cudaEventRecord(fork, cs), "cudaEventRecord");
+    cuda_check(cudaStreamWaitEvent(ss, fork, 0), "cudaStreamWaitEvent");
+    for (size_t i = 0; i < n; ++i) {
+      cuda_check(cudaMemcpyAsync(d_in[i], h_in[i], in_bytes[i], cudaMemcpyHostToDevice, ss), "H2D query");
+      std::vector<int> ops;
+      for (int f : pr->gated_prepass)
+        if (rt.flat[f].tenant == tenants[i]) ops.push_back(f);
+      g.kernels += rt.launch_prepass_ops(ops, ss, false);
+      for (const auto& gt : pr->gates)
+        if (gt.first == tenants[i])
+          cuda_check(cudaMemcpyAsync(pr->counters + gt.second, rt.host_one, sizeof(uint32_t), cudaMemcpyHostToDevice, ss),
+                     "open input gate");
+    }
+    cuda_check(cudaEventRecord(join, ss), "cudaEventRecord");
+    g.kernels += rt.launch(*pr, cs, false);
+    g.superkernels += 1;
+    g.tiles += pr->n_tiles;
+    cuda_check(cudaStreamWaitEvent(cs, join, 0), "cudaStreamWaitEvent");
+    for (size_t i = 0; i < n; ++i)
+      cuda_check(cudaMemcpyAsync(h_out[i], d_out[i], out_bytes[i], cudaMemcpyDeviceToHost, cs), "D2H result");
   });
   GM_API_END
 }

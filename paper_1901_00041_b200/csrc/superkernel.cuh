@@ -168,6 +168,23 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   return v;
 }
 
+// Wait until *ctr >= want (acquire).  A dependency that never resolves (a
+// broken launch program) traps after ~4 s instead of hanging the GPU.
+__device__ __forceinline__ void wait_counter(const uint32_t* ctr, uint32_t want, uint32_t sleep_ns) {
+  uint32_t spins = 0;
+  uint64_t t0 = 0;
+  while (ld_acquire(ctr) < want) {
+    __nanosleep(sleep_ns);
+    if ((++spins & 4095u) == 0) {
+      const uint64_t now = globaltimer();
+      if (t0 == 0)
+        t0 = now;
+      else if (now - t0 > 4000000000ull)
+        __trap();
+    }
+  }
+}
+
 // ---------------------------------------------------------------- PTX helpers
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -565,7 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto gate = [&]() {
           if (first) asm volatile("griddepcontrol.wait;" ::: "memory");
           if (te.dep >= 0) {
-            while (ld_acquire(counters + te.dep) < targets[te.dep]) __nanosleep(32);
+            wait_counter(counters + te.dep, targets[te.dep], 32);
             asm volatile("fence.proxy.async.global;" ::: "memory");
           }
         };
@@ -844,7 +861,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (te.dep >= 0) {
           if (lane == 0)
-            while (ld_acquire(counters + te.dep) < targets[te.dep]) __nanosleep(32);
+            wait_counter(counters + te.dep, targets[te.dep], 32);
           __syncwarp();
         }
         if (trace && warp == 4 && lane == 0) {
@@ -938,7 +955,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // finisher: wait for the other splits' lanes, add its own TMEM
           // partial to their sum, store bf16, clear the workspace
           const uint32_t want = static_cast<uint32_t>(te.splits - 1) * 32u;
-          while (ld_acquire(ctr) < want) __nanosleep(40);
+          wait_counter(ctr, want, 40);
           for (int c = 0; c < cols; c += kEpiChunk) {
             uint32_t v[32];
             tmem_ld32(taddr + c, v);

@@ -153,7 +153,7 @@ class SpaceTimeEngine:
             self.tenants.append(self.ctx.register_tenant(m.buffers, slo_latency=slo_latency,
                                                          tenant_id=f"t{tenant_offset + i}"))
         self._now = 0
-        self._graphs: Dict[int, Graph] = {}  # plan-list key -> captured round program
+        self._graphs: Dict[tuple, Graph] = {}  # (plan key, host buffers) -> end-to-end launch program
         self._stable_plan: Optional[Round] = None  # serve_round's steady-state plan
         self._last_key: Optional[int] = None
 
@@ -197,34 +197,52 @@ class SpaceTimeEngine:
         return Graph(h.value, timed)
 
     # ------------------------------------------------------------ public serving call
+    def capture_round_e2e(self, rnd: Round, host_inputs: Sequence[torch.Tensor],
+                          host_outputs: Sequence[torch.Tensor]) -> Graph:
+        """The round program with its host traffic: per tenant the H2D copy of
+        its query batch opens that tenant's input gate, so the kernel starts a
+        tenant's chain as soon as its input has landed (copies overlap compute);
+        D2H of every tenant's result after the kernel."""
+        n = len(self.models)
+        tid = (C.c_int32 * n)(*self.tenants)
+        h_in = (C.c_void_p * n)(*[h.data_ptr() for h in host_inputs])
+        d_in = (C.c_void_p * n)(*[m.query_input.data_ptr() for m in self.models])
+        ib = (C.c_size_t * n)(*[h.numel() * h.element_size() for h in host_inputs])
+        d_out = (C.c_void_p * n)(*[m.query_output.data_ptr() for m in self.models])
+        h_out = (C.c_void_p * n)(*[h.data_ptr() for h in host_outputs])
+        ob = (C.c_size_t * n)(*[h.numel() * h.element_size() for h in host_outputs])
+        h = C.c_void_p()
+        check(lib().gm_graph_capture_round_e2e(self.ctx.handle, rnd.handle, n, tid, h_in, d_in, ib, d_out, h_out, ob,
+                                               C.byref(h)))
+        return Graph(h.value, False)
+
+    # ------------------------------------------------------------ public serving call
     def serve_round(self, host_inputs: Sequence[torch.Tensor], host_outputs: Sequence[torch.Tensor],
                     stream: torch.cuda.Stream) -> Round:
         """End-to-end round through the public API with host buffers.
 
-        Copies each tenant's query batch host->device, plans the round with the
-        space-time scheduler, replays (or captures, on a new signature
-        sequence) the packed launch program, and copies each tenant's result
-        device->host.  Returns after the results are on the host.
+        Plans the round with the space-time scheduler (re-planned until two
+        consecutive rounds plan identically, then the steady-state plan is
+        reused: a SuperKernelCache hit for every member set) and
+        replays (or captures, on a new plan or new host buffers) the
+        end-to-end launch program: H2D of each tenant's query batch gating its
+        chain, the round kernel, D2H of each tenant's result.  Returns after
+        the results are on the host.
         """
-        with torch.cuda.stream(stream):
-            for m, h in zip(self.models, host_inputs):
-                m.query_input.copy_(h, non_blocking=True)
-            # Steady state: once two consecutive rounds of the same tenants plan
-            # identically, the plan is reused (a SuperKernelCache hit for every
-            # member set: no planning work, PAPER.md:171); re-planned otherwise.
-            rnd = self._stable_plan
-            if rnd is None:
-                rnd = self.plan_round()
-                if self._last_key == rnd.key:
-                    self._stable_plan = rnd
-                self._last_key = rnd.key
-            key = rnd.key
-            g = self._graphs.get(key)
-            if g is None:
-                g = self._graphs[key] = self.capture_round(rnd)
-            g.launch(stream.cuda_stream)
-            for m, h in zip(self.models, host_outputs):
-                h.copy_(m.query_output, non_blocking=True)
+        for m, h in zip(self.models, host_inputs):
+            if h.numel() != m.query_input.numel() or h.dtype != m.query_input.dtype:
+                raise ValueError("host input does not match the tenant's query batch")
+        rnd = self._stable_plan
+        if rnd is None:
+            rnd = self.plan_round()
+            if self._last_key == rnd.key:
+                self._stable_plan = rnd
+            self._last_key = rnd.key
+        key = (rnd.key, tuple(h.data_ptr() for h in host_inputs), tuple(h.data_ptr() for h in host_outputs))
+        g = self._graphs.get(key)
+        if g is None:
+            g = self._graphs[key] = self.capture_round_e2e(rnd, host_inputs, host_outputs)
+        g.launch(stream.cuda_stream)
         stream.synchronize()
         return rnd
 
