@@ -147,6 +147,8 @@ struct Runtime {
   bool dynamic_schedule = false;  // round programs: per-tenant ready queues (else static round-robin)
   bool greedy_schedule = false;   // round programs: greedy in-order tile claiming (else static round-robin)
   bool tall_tiles = true;         // 256-row tiles for narrow members of throughput-bound plans
+  int critical_order = -1;        // round programs: tile order 0 plan, 1 remaining chain work, 2 chain progress,
+                                  // -1 auto (2 for homogeneous tenants, else 0)
   int64_t tall_min_tiles = 0;     // concurrent same-shape tiles that make a member "throughput-bound" (0 = 2 x SMs)
   int bn = 256;     // N tile of the super-kernel (== DeviceSpec.tile_n)
   uint32_t* host_one = nullptr;  // pinned 4-byte 1: DMA source that opens an input gate
@@ -669,6 +671,63 @@ struct Runtime {
       }
       p.tile_plan.resize(table.size(), static_cast<uint16_t>(&pl - plans.data()));
     }
+    // Critical-path order (option): tiles sorted by their tenant's remaining
+    // work from this layer on (FLOPs of the layer and every later layer),
+    // longest first.  Remaining work strictly decreases along a chain, so the
+    // order stays topological; with heterogeneous tenants the longest chain's
+    // tiles reach the SMs first instead of following the virtual-clock plan.
+    int order = critical_order;
+    if (order < 0) {
+      // auto: progress order when every tenant of the round runs the same
+      // layer list (measured +5-9% on ResNet-50 / BERT rounds), else the
+      // virtual-clock plan order (better for mixed models)
+      std::vector<int> ts_round;
+      for (const auto& pl : plans)
+        for (int f : pl) ts_round.push_back(flat[f].tenant);
+      std::sort(ts_round.begin(), ts_round.end());
+      ts_round.erase(std::unique(ts_round.begin(), ts_round.end()), ts_round.end());
+      bool same = true;
+      for (int t2 : ts_round) {
+        const auto& a = tenant_ops[t2];
+        const auto& b = tenant_ops[ts_round.front()];
+        if (a.size() != b.size()) {
+          same = false;
+          break;
+        }
+        for (size_t j = 0; j < a.size() && same; ++j) same = flat[a[j]].shape == flat[b[j]].shape;
+        if (!same) break;
+      }
+      order = same ? 2 : 0;
+    }
+    if (order && !table.empty()) {
+      // mode 1: remaining FLOPs (longest chain first); mode 2: chain progress
+      // (fraction of the tenant's FLOPs before this layer, ascending), which
+      // keeps heterogeneous chains advancing together
+      std::vector<double> tail(flat.size(), 0.0);
+      for (const auto& ops : tenant_ops) {
+        double acc = 0;
+        for (auto it2 = ops.rbegin(); it2 != ops.rend(); ++it2) {
+          const Shape& sh = flat[*it2].shape;
+          acc += 2.0 * static_cast<double>(sh.m) * static_cast<double>(sh.n) * static_cast<double>(sh.k);
+          tail[*it2] = acc;
+        }
+        if (order == 2)
+          for (int f2 : ops) tail[f2] = tail[f2] / acc;  // 1 - progress: descending == progress ascending
+      }
+      std::vector<size_t> idx(table.size());
+      for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
+      std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) {
+        return tail[slot_op[table[a].member]] > tail[slot_op[table[b].member]];
+      });
+      std::vector<dev::TileEntry> sorted(table.size());
+      std::vector<uint16_t> sorted_plan(table.size());
+      for (size_t i = 0; i < idx.size(); ++i) {
+        sorted[i] = table[idx[i]];
+        sorted_plan[i] = p.tile_plan[idx[i]];
+      }
+      table.swap(sorted);
+      p.tile_plan.swap(sorted_plan);
+    }
     // Dynamic schedule: one work queue per tenant, its tiles in plan order.
     std::vector<int32_t> qbeg, qlen;
     if (dynamic_schedule && !table.empty()) {
@@ -997,6 +1056,9 @@ int gm_ctx_set_option(gm_ctx* ctx, const char* name, int64_t value) {
   } else if (n == "tall_min_tiles") {
     if (value < 0) throw std::invalid_argument("tall_min_tiles must be >= 0");
     rt.tall_min_tiles = value;
+  } else if (n == "critical_order") {
+    if (value < -1 || value > 2) throw std::invalid_argument("critical_order must be -1 (auto), 0, 1 or 2");
+    rt.critical_order = static_cast<int>(value);  // applies to round programs prepared afterwards
   } else if (n == "tall_tiles") {
     rt.tall_tiles = value != 0;  // applies to plans prepared afterwards
   } else if (n == "greedy_schedule") {
