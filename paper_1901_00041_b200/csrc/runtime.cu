@@ -476,7 +476,8 @@ struct Runtime {
       }
       // tall variant: two 128-row halves per tile sharing the B box
       if (op.kind != GM_LAYER_DWCONV && op.b_ptr && op.shape.m >= 2 * dev::kBM && op.shape.n <= 128 &&
-          (md.a_mode == dev::kATiled || md.a_mode == dev::kAIm2col) && a_box_rows(op.shape.m) == dev::kBM) {
+          (md.a_mode == dev::kATiled || md.a_mode == dev::kAIm2col || md.a_mode == dev::kAIm2colFold) &&
+          a_box_rows(op.shape.m) == dev::kBM) {
         dev::MemberDesc md3 = md;
         md3.tall = 1;
         md3.n_tile = 128;  // the second half's accumulator starts at column 128 of the tile's buffer

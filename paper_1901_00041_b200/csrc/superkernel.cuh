@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int p1 = rem / md->q;
           const int q1 = rem - p1 * md->q;
           h1 = p1 * md->stride - md->pad;
-          w1 = q1 * md->stride - md->pad;
+          w1 = fold ? q1 : q1 * md->stride - md->pad;
         }
         // TMA im2col coordinates advance incrementally (load_a runs in k-block
         // order within a tile): no integer divisions on the producer's path
@@ -542,6 +542,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int r = kb * kFoldTaps + j;
               tma_load_im2col(a_dst + j * kFoldTapBytes, amap, &full[st], 0, w0, h0, img, 0,
                               static_cast<uint16_t>(r < taps ? r : 0));
+              if (tall)
+                tma_load_im2col(a_dst + kABytes + j * kFoldTapBytes, amap, &full[st], 0, w1, h1, img1, 0,
+                                static_cast<uint16_t>(r < taps ? r : 0));
             }
           } else if (narrow) {
             // eight 16 B tap columns; taps past R*S load an out-of-range image
@@ -630,6 +633,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             if constexpr (kMode == kATiled) {
               tma_load_2d(a_dst, amap, bar, kb * kBK, m0);
               if constexpr (kTall) tma_load_2d(a_dst + kABytes, amap, bar, kb * kBK, m0 + kBM);
+            } else if constexpr (kMode == kAIm2colFold) {
+              // two filter rows; a row past R re-reads row 0 (its weights are zero)
+#pragma unroll
+              for (int j = 0; j < kFoldTaps; ++j) {
+                const int r = kb * kFoldTaps + j;
+                const uint16_t rr = static_cast<uint16_t>(r < taps ? r : 0);
+                tma_load_im2col(a_dst + j * kFoldTapBytes, amap, bar, 0, w0, h0, img, 0, rr);
+                if constexpr (kTall) tma_load_im2col(a_dst + kABytes + j * kFoldTapBytes, amap, bar, 0, w1, h1, img1, 0, rr);
+              }
             } else {
               tma_load_im2col(a_dst, amap, bar, cb * kBK, w0, h0, img, static_cast<uint16_t>(s_),
                               static_cast<uint16_t>(r_));
@@ -663,6 +675,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             steady(std::integral_constant<int, kAIm2col>{}, I1{});
           else
             steady(std::integral_constant<int, kAIm2col>{}, I0{});
+        } else if (md->a_mode == kAIm2colFold) {
+          if (tall)
+            steady(std::integral_constant<int, kAIm2colFold>{}, I1{});
+          else
+            steady(std::integral_constant<int, kAIm2colFold>{}, I0{});
         } else {
           for (; kb < k_blocks; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
