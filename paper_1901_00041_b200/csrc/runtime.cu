@@ -814,8 +814,10 @@ struct Runtime {
     int nj = 0, max_pixels = 0;
     auto flush = [&]() {
       if (!nj) return;
-      const int gx = std::min((max_pixels + 255) / 256, sms * 8);
-      dev::fold_rows<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(nj)), 256, 0, stream>>>(fb);
+      // 128-thread blocks (~4K registers): small enough to co-reside with the
+      // persistent super-kernel's CTAs when an e2e graph runs them beside it
+      const int gx = std::min((max_pixels + 127) / 128, sms * 16);
+      dev::fold_rows<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(nj)), 128, 0, stream>>>(fb);
       cuda_check(cudaGetLastError(), "launch fold_rows");
       ++launches;
       if (count) ++n_prepasses;
@@ -838,8 +840,8 @@ struct Runtime {
         continue;
       }
       const int64_t total = op.shape.m * (op.ldk / 8);
-      const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, int64_t(sms) * 16));
-      dev::im2col_prepass<<<grid, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(op.x),
+      const int grid = static_cast<int>(std::min<int64_t>((total + 127) / 128, int64_t(sms) * 32));
+      dev::im2col_prepass<<<grid, 128, 0, stream>>>(static_cast<const __nv_bfloat16*>(op.x),
                                                      static_cast<__nv_bfloat16*>(op.scratch), op.batch, H, W, Cin, R,
                                                      S, st, pad, P, Q, ldk);
       cuda_check(cudaGetLastError(), "launch im2col_prepass");
@@ -1353,6 +1355,32 @@ int gm_graph_capture_round_e2e(gm_ctx* ctx, const gm_plans* p, size_t n, const i
   Runtime& rt = runtime_of(ctx);
   std::vector<std::vector<int>> plans;
   for (const Plan& plan : p->plans) plans.push_back(members_of(rt, plan));
+  // The copy branch's pre-pass blocks must fit beside a persistent CTA
+  // (registers: the CTA's allocation plus one 128-thread pre-pass block);
+  // otherwise gates could wait on work that cannot be scheduled, so the
+  // program is captured serially instead (copies, round, results).
+  auto regs_of = [](const void* fn) {
+    cudaFuncAttributes a{};
+    cuda_check(cudaFuncGetAttributes(&a, fn), "cudaFuncGetAttributes");
+    return (a.numRegs + 7) / 8 * 8;
+  };
+  const int pre_regs = std::max(regs_of(reinterpret_cast<const void*>(&dev::fold_rows)),
+                                regs_of(reinterpret_cast<const void*>(&dev::im2col_prepass)));
+  const bool co_resident = regs_of(rt.kernel) * dev::kThreads + pre_regs * 128 <= 65536;
+  if (!co_resident) {
+    Prepared* sp = &rt.prepare_round(plans);
+    *out = capture(ctx, [&](cudaStream_t cs, gm_graph& g) {
+      for (size_t i = 0; i < n; ++i)
+        if (in_bytes[i]) cuda_check(cudaMemcpyAsync(d_in[i], h_in[i], in_bytes[i], cudaMemcpyHostToDevice, cs), "H2D query");
+      g.kernels += rt.launch(*sp, cs, false);
+      g.superkernels += 1;
+      g.tiles += sp->n_tiles;
+      for (size_t i = 0; i < n; ++i)
+        if (out_bytes[i])
+          cuda_check(cudaMemcpyAsync(h_out[i], d_out[i], out_bytes[i], cudaMemcpyDeviceToHost, cs), "D2H result");
+    });
+    return GM_OK;
+  }
   Prepared* pr = &rt.prepare_round(plans, true);
   for (size_t i = 0; i < n; ++i) {
     bool found = false;

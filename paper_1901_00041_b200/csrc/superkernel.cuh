@@ -330,44 +330,72 @@ __device__ __forceinline__ uint32_t pack_bf16(uint32_t lo_bits, uint32_t hi_bits
 // and pixel per lane (a warp reads 256 contiguous bytes of channels).
 __device__ __forceinline__ void depthwise_tile(const MemberDesc* __restrict__ md, const TileEntry& te, int ew, int lane) {
   const int M = md->m, C = md->ch, H = md->h_in, W = md->w_in;
-  const int c = te.n_tile * kDwTileC + lane * 4;
-  if (c >= C) return;
+  // lanes -> (channel group of 4, pixel): a narrow channel tile packs several
+  // pixels per warp instruction instead of idling lanes
+  const int cbase = te.n_tile * kDwTileC;
+  const int g = min(kDwTileC, C - cbase) >> 2;  // channel groups in this tile
+  const int gp = g <= 8 ? 8 : (g <= 16 ? 16 : 32);
+  const int pp = 32 / gp;  // pixels per pass
+  const int cg = lane & (gp - 1), sub = lane / gp;
+  if (cg >= g) return;
+  const int c = cbase + cg * 4;
   const int taps = md->r_taps, S = md->s_taps, st = md->stride, pad = md->pad, PQ = md->pq, Q = md->q;
-  const int R = taps / S;
   float wv[4][kDwMaxTaps];
 #pragma unroll
   for (int j = 0; j < 4; ++j)
 #pragma unroll
     for (int k = 0; k < kDwMaxTaps; ++k)
       wv[j][k] = k < taps ? __bfloat162float(md->dw[static_cast<int64_t>(c + j) * md->ldw + k]) : 0.f;
-  const int m_base = te.m_tile * kBM + ew * 16;
-  for (int i = 0; i < 16; ++i) {
-    const int m = m_base + i;
-    if (m >= M) break;
-    const int b = m / PQ;
-    const int rem = m - b * PQ;
-    const int p = rem / Q;
-    const int q = rem - p * Q;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  // 16 pixels per warp: this lane's are m_base + sub + pp * i.  Tap-major
+  // over groups of 8 pixels keeps 8 independent loads in flight per tap.
+  constexpr int kG = 4;
+  const int m_base = te.m_tile * kBM + ew * 16 + sub;
+  const int npx = 16 / pp;
+  for (int i0 = 0; i0 < npx; i0 += kG) {
+    int bb[kG], hh[kG], ww[kG];
+    float acc[kG][4];
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      const int m = m_base + pp * (i0 + j);
+      const bool ok = i0 + j < npx && m < M;
+      const int b = ok ? m / PQ : -1;
+      const int rem = m - b * PQ;
+      const int p = rem / Q;
+      bb[j] = b;
+      hh[j] = p * st - pad;
+      ww[j] = (rem - p * Q) * st - pad;
+      acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+    }
 #pragma unroll
     for (int k = 0; k < kDwMaxTaps; ++k) {
       if (k >= taps) break;
       const int r = k / S, s = k - r * S;
-      const int ih = p * st - pad + r, iw = q * st - pad + s;
-      if (ih < 0 || ih >= H || iw < 0 || iw >= W) continue;
-      const uint2 raw = __ldcg(reinterpret_cast<const uint2*>(md->dx + ((static_cast<int64_t>(b) * H + ih) * W + iw) * C + c));
-      const __nv_bfloat162 x01 = *reinterpret_cast<const __nv_bfloat162*>(&raw.x);
-      const __nv_bfloat162 x23 = *reinterpret_cast<const __nv_bfloat162*>(&raw.y);
-      acc[0] = fmaf(__low2float(x01), wv[0][k], acc[0]);
-      acc[1] = fmaf(__high2float(x01), wv[1][k], acc[1]);
-      acc[2] = fmaf(__low2float(x23), wv[2][k], acc[2]);
-      acc[3] = fmaf(__high2float(x23), wv[3][k], acc[3]);
+      uint2 raw[kG];
+#pragma unroll
+      for (int j = 0; j < kG; ++j) {
+        const int ih = hh[j] + r, iw = ww[j] + s;
+        raw[j] = make_uint2(0u, 0u);
+        if (bb[j] >= 0 && ih >= 0 && ih < H && iw >= 0 && iw < W)
+          raw[j] = __ldcg(reinterpret_cast<const uint2*>(md->dx + ((static_cast<int64_t>(bb[j]) * H + ih) * W + iw) * C + c));
+      }
+#pragma unroll
+      for (int j = 0; j < kG; ++j) {
+        const __nv_bfloat162 x01 = *reinterpret_cast<const __nv_bfloat162*>(&raw[j].x);
+        const __nv_bfloat162 x23 = *reinterpret_cast<const __nv_bfloat162*>(&raw[j].y);
+        acc[j][0] = fmaf(__low2float(x01), wv[0][k], acc[j][0]);
+        acc[j][1] = fmaf(__high2float(x01), wv[1][k], acc[j][1]);
+        acc[j][2] = fmaf(__low2float(x23), wv[2][k], acc[j][2]);
+        acc[j][3] = fmaf(__high2float(x23), wv[3][k], acc[j][3]);
+      }
     }
-    (void)R;
-    uint2 o;
-    o.x = pack_bf16(__float_as_uint(acc[0]), __float_as_uint(acc[1]), md->relu);
-    o.y = pack_bf16(__float_as_uint(acc[2]), __float_as_uint(acc[3]), md->relu);
-    *reinterpret_cast<uint2*>(md->dy + static_cast<int64_t>(m) * C + c) = o;
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      if (bb[j] < 0) continue;
+      uint2 o;
+      o.x = pack_bf16(__float_as_uint(acc[j][0]), __float_as_uint(acc[j][1]), md->relu);
+      o.y = pack_bf16(__float_as_uint(acc[j][2]), __float_as_uint(acc[j][3]), md->relu);
+      *reinterpret_cast<uint2*>(md->dy + static_cast<int64_t>(m_base + pp * (i0 + j)) * C + c) = o;
+    }
   }
 }
 
@@ -1089,7 +1117,7 @@ struct FoldBatch {
   FoldJob job[16];
 };
 
-__global__ void __launch_bounds__(256) fold_rows(const __grid_constant__ FoldBatch fb) {
+__global__ void __launch_bounds__(128) fold_rows(const __grid_constant__ FoldBatch fb) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const FoldJob& j = fb.job[blockIdx.y];
   const unsigned short* xs = reinterpret_cast<const unsigned short*>(j.x);

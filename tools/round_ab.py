@@ -25,6 +25,10 @@ def build(config, opts):
     if config.startswith("t1r"):  # Table-1 microbench: R tenants x conv2_2 b1
         r = int(config[3:])
         return SpaceTimeEngine([W.conv2_2()] * r, [1] * r, options=opts)
+    if config.startswith("solo_"):  # solo_<model>b<B>: one tenant alone (chain latency)
+        name, b = config[5:].rsplit("b", 1)
+        layers = {"vgg16": W.vgg16(224), "resnet50": W.resnet50(224), "mobilenet": W.mobilenet_v2(224)}[name]
+        return SpaceTimeEngine([layers], [int(b)], options=opts)
     if config == "bert4":
         return SpaceTimeEngine([W.bert_base_gemms(128, 12)] * 16, [4] * 16, options=opts)
     raise SystemExit(config)
