@@ -440,7 +440,8 @@ struct Runtime {
         throw std::invalid_argument("register_tenant: unknown layer kind");
       }
       if (op.shape.n % 8 != 0) throw std::invalid_argument("register_tenant: output channels must be a multiple of 8");
-      if (op.shape.m > int64_t(0xFFFF) * dev::kBM || op.shape.m > INT32_MAX)
+      if (op.shape.m > int64_t(0xFFFF) * (op.kind == GM_LAYER_DWCONV ? dev::kDwTileM : dev::kBM) ||
+          op.shape.m > INT32_MAX)
         throw std::invalid_argument("register_tenant: M too large for the tile table");
       store_map(&md.c, L.y, op.shape.m, op.shape.n);
       md.m = static_cast<int32_t>(op.shape.m);
@@ -580,7 +581,7 @@ struct Runtime {
     for (int f : members) {
       const Operator& op = flat[f];
       const auto [slot, w] = variant(f, plan_tiles, plan_tiles);
-      const int64_t tm = dev::kBM << (is_tall(slot) ? 1 : 0);
+      const int64_t tm = op.kind == GM_LAYER_DWCONV ? dev::kDwTileM : dev::kBM << (is_tall(slot) ? 1 : 0);
       const int64_t mt = (op.shape.m + tm - 1) / tm;
       const int64_t nt = (op.shape.n + w - 1) / w;
       for (int64_t a = 0; a < mt; ++a)
@@ -639,7 +640,8 @@ struct Runtime {
           p.gates.emplace_back(op.tenant, dep);
         }
         last_instance[f] = inst;
-        const int64_t mt = (op.shape.m + (dev::kBM << (tall ? 1 : 0)) - 1) / (dev::kBM << (tall ? 1 : 0));
+        const int64_t tm = op.kind == GM_LAYER_DWCONV ? dev::kDwTileM : dev::kBM << (tall ? 1 : 0);
+        const int64_t mt = (op.shape.m + tm - 1) / tm;
         const int64_t nt = (op.shape.n + w - 1) / w;
         const int kb = static_cast<int>((op.shape.k + dev::kBK - 1) / dev::kBK);
         // Split-K when the plan cannot fill the SMs and the K loop is long:

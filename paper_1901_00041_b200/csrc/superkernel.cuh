@@ -62,8 +62,12 @@ enum : int32_t { kATiled = 0, kAIm2col = 1, kAIm2colNarrow = 2, kAIm2colFold = 3
 // Depthwise conv (MobileNet-v2) is a CUDA-core tile type inside the same
 // persistent kernel (tensor cores do not apply: one filter per channel).  Its
 // tiles skip the TMA/MMA pipeline; the eight epilogue warps compute them
-// directly (16 output pixels each x kDwTileC channels, 4 channels per lane).
+// directly (kDwPixW output pixels each x kDwTileC channels, 4 channels per
+// lane).  Tiles are short (kDwTileM pixels) so a layer spreads over many SMs:
+// a depthwise layer sits on its tenant's chain, its latency is one tile's.
 constexpr int kDwTileC = 128;
+constexpr int kDwPixW = 4;               // output pixels per epilogue warp
+constexpr int kDwTileM = 8 * kDwPixW;    // output pixels per depthwise tile
 constexpr int kDwMaxTaps = 9;
 constexpr int kNarrowC = 8;                     // channels per pixel of a narrow-im2col input
 constexpr int kNarrowTaps = kBK / kNarrowC;     // filter taps per k-block
@@ -346,11 +350,11 @@ __device__ __forceinline__ void depthwise_tile(const MemberDesc* __restrict__ md
 #pragma unroll
     for (int k = 0; k < kDwMaxTaps; ++k)
       wv[j][k] = k < taps ? __bfloat162float(md->dw[static_cast<int64_t>(c + j) * md->ldw + k]) : 0.f;
-  // 16 pixels per warp: this lane's are m_base + sub + pp * i.  Tap-major
-  // over groups of 8 pixels keeps 8 independent loads in flight per tap.
+  // kDwPixW pixels per warp: this lane's are m_base + pp * i.  Tap-major over
+  // groups of kG pixels keeps kG independent loads in flight per tap.
   constexpr int kG = 4;
-  const int m_base = te.m_tile * kBM + ew * 16 + sub;
-  const int npx = 16 / pp;
+  const int m_base = te.m_tile * kDwTileM + ew * kDwPixW + sub;
+  const int npx = (kDwPixW + pp - 1) / pp;
   for (int i0 = 0; i0 < npx; i0 += kG) {
     int bb[kG], hh[kG], ww[kG];
     float acc[kG][4];
