@@ -643,15 +643,21 @@ def run_table1(torch, rs, dev, stream):
         for name, g in gs.items():
             for _ in range(3):
                 g.launch(stream.cuda_stream)
-            per, _ = time_graph(torch, g, stream, 10, flush=flush)
-            ms = sum(per) / len(per)
-            row[name + "_tflops"] = eng.flops_per_round() / (ms / 1e3) / 1e12
+            # best of 3 repetitions per mode: the space-only baseline's stream
+            # concurrency at large R varies run to run; every mode gets its best
+            best = None
+            for _ in range(3):
+                per, _ = time_graph(torch, g, stream, 10, flush=flush)
+                ms = sum(per) / len(per)
+                best = ms if best is None else min(best, ms)
+            row[name + "_tflops"] = eng.flops_per_round() / (best / 1e3) / 1e12
         row["over_space_only"] = row["packed_tflops"] / row["space_only_tflops"]
         row["over_time_only"] = row["packed_tflops"] / row["time_only_tflops"]
         rows.append(row)
         del eng, gs
     from paper_1901_00041_b200.scheduler import geomean
-    return {"workload": "conv2_2 (256,128,1152) b1 per tenant, L2 flushed between steps",
+    return {"workload": "conv2_2 (256,128,1152) b1 per tenant, L2 flushed between steps; best of 3 x 10 steps "
+                        "per mode",
             "rows": rows,
             "geomean_over_space_only": geomean([r["over_space_only"] for r in rows]),
             "geomean_over_time_only": geomean([r["over_time_only"] for r in rows])}
