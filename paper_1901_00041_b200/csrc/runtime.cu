@@ -147,6 +147,7 @@ struct Runtime {
   bool dynamic_schedule = false;  // round programs: per-tenant ready queues (else static round-robin)
   bool greedy_schedule = false;   // round programs: greedy in-order tile claiming (else static round-robin)
   bool tall_tiles = true;         // 256-row tiles for narrow members of throughput-bound plans
+  int ring_layouts = 1;           // narrow members use the 6 x 32 KB ring layout (applies at registration)
   int critical_order = -1;        // round programs: tile order 0 plan, 1 remaining chain work, 2 chain progress,
                                   // -1 auto (2 for homogeneous tenants, else 0)
   int64_t tall_min_tiles = 0;     // concurrent same-shape tiles that make a member "throughput-bound" (0 = 2 x SMs)
@@ -198,6 +199,14 @@ struct Runtime {
                "cudaFuncSetAttribute");
     cuda_check(cudaHostAlloc(&host_one, sizeof(uint32_t), cudaHostAllocDefault), "cudaHostAlloc");
     *host_one = 1;
+  }
+
+  // A member's k-block stage (A region + B box) fits a 32 KB narrow-layout slot.
+  int ring_narrow_of(const dev::MemberDesc& md, int b_rows) const {
+    if (ring_layouts == 0) return 0;
+    const bool cols = md.a_mode == dev::kAIm2colNarrow || md.a_mode == dev::kAIm2colFold;
+    const int a_bytes = cols ? dev::kABytes : a_box_rows(md.m) * dev::kBK * 2;
+    return a_bytes + b_rows * dev::kBK * 2 <= 32768 ? 1 : 0;
   }
 
   // [rows, cols] bf16 row-major with row stride ld (elements), box kBK x box_rows.
@@ -454,6 +463,7 @@ struct Runtime {
       md.tx_bytes = static_cast<uint32_t>((a_box_rows(op.shape.m) + b_box_rows(op.shape.n, op.n_tile)) * dev::kBK * 2);
       md.relu = L.relu ? 1 : 0;
       md.n_tile = op.n_tile;
+      md.ring_narrow = ring_narrow_of(md, b_box_rows(op.shape.n, op.n_tile));
       op.slot = static_cast<int>(host_desc.size() + descs.size());
       const int f_index = static_cast<int>(flat.size() + fresh.size());
       descs.push_back(md);
@@ -468,6 +478,7 @@ struct Runtime {
           md2.idesc = make_idesc(b_box_rows(op.shape.n, w));
           md2.tx_bytes = static_cast<uint32_t>((a_box_rows(op.shape.m) + b_box_rows(op.shape.n, w)) * dev::kBK * 2);
           md2.n_tile = w;
+          md2.ring_narrow = ring_narrow_of(md2, b_box_rows(op.shape.n, w));
           op.narrow_slot[v] = static_cast<int>(host_desc.size() + descs.size());
           op.narrow_w[v] = w;
           descs.push_back(md2);
@@ -481,6 +492,7 @@ struct Runtime {
           a_box_rows(op.shape.m) == dev::kBM) {
         dev::MemberDesc md3 = md;
         md3.tall = 1;
+        md3.ring_narrow = 0;  // two A boxes: a wide-layout stage
         md3.n_tile = 128;  // the second half's accumulator starts at column 128 of the tile's buffer
         md3.tx_bytes = static_cast<uint32_t>((2 * dev::kBM + b_box_rows(op.shape.n, op.n_tile)) * dev::kBK * 2);
         op.tall_slot = static_cast<int>(host_desc.size() + descs.size());
@@ -1064,6 +1076,8 @@ int gm_ctx_set_option(gm_ctx* ctx, const char* name, int64_t value) {
   } else if (n == "critical_order") {
     if (value < -1 || value > 2) throw std::invalid_argument("critical_order must be -1 (auto), 0, 1 or 2");
     rt.critical_order = static_cast<int>(value);  // applies to round programs prepared afterwards
+  } else if (n == "ring_layouts") {
+    rt.ring_layouts = value != 0 ? 1 : 0;  // applies to tenants registered afterwards
   } else if (n == "tall_tiles") {
     rt.tall_tiles = value != 0;  // applies to plans prepared afterwards
   } else if (n == "greedy_schedule") {

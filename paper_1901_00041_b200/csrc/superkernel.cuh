@@ -49,6 +49,13 @@ struct Cfg {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;
   static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 512 /*barriers, tile ring*/;
+  // Two ring layouts over the same bytes: wide (kStages slots of kStageBytes)
+  // and narrow (32 KB slots) for members whose stage fits in 32 KB (N tile
+  // <= 128), which then keep more k-blocks in flight -- their k-block rate
+  // is set by operand latency.  Switching layout drains the ring.
+  static constexpr int kNarrowBytes = 32768;
+  static constexpr int kNarrowSlots = kStages * kStageBytes / kNarrowBytes;
+  static constexpr int kMaxSlots = kNarrowSlots > kStages ? kNarrowSlots : kStages;
 };
 
 // A-operand modes: 2-D tiled box; TMA im2col (C_in % 64 == 0: one 128 B
@@ -100,6 +107,7 @@ struct alignas(128) MemberDesc {
   // Doubles the work per k-block of a narrow tile, whose k-block rate is set
   // by operand latency, not by the tensor pipe.
   int32_t tall;
+  int32_t ring_narrow;  // 1: the stage (A region + B box) fits a 32 KB narrow-layout slot
   // depthwise members: raw operands and geometry (x NHWC [b, H, W, C],
   // w [C, ldw] with R*S taps per row, y [b*P*Q, C])
   const __nv_bfloat16* dx;
@@ -413,14 +421,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* __restrict__ counters = ra.counters;
   const uint32_t* __restrict__ targets = ra.targets;
   uint64_t* __restrict__ trace = ra.trace;
-  constexpr int kStages = C::kStages;
+  constexpr uint32_t kStages = C::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* ring = smem;                                // kStages x (A | B)
   uint8_t* epi = smem + kStages * C::kStageBytes;     // store staging
   uint64_t* full = reinterpret_cast<uint64_t*>(epi + kEpiBytes);
-  uint64_t* empty = full + kStages;
-  uint64_t* acc_full = empty + kStages;
+  uint64_t* empty = full + C::kMaxSlots;
+  uint64_t* acc_full = empty + C::kMaxSlots;
   uint64_t* acc_empty = acc_full + 2;
   uint64_t* tq_full = acc_empty + 2;     // claimed-tile ring: producer -> consumers
   uint64_t* tq_empty = tq_full + kTileQ;
@@ -434,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < C::kMaxSlots; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -469,7 +477,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
-      uint32_t stage = 0, phase = 0;
+      // ring: current layout, next slot, per-slot use parity, last issued
+      uint32_t stage = 0, ubits = 0, nslots = kStages, sbytes = C::kStageBytes;
+      int layout = 0;
+      int last_slot = -1;
+      uint32_t last_par = 0;
+      auto advance = [&]() {
+        last_slot = static_cast<int>(stage);
+        last_par = (ubits >> stage) & 1u;
+        ubits ^= 1u << stage;
+        stage = stage + 1 == nslots ? 0 : stage + 1;
+      };
+      auto wait_free = [&]() { mbar_wait(&empty[stage], ((ubits >> stage) & 1u) ^ 1u); };
       bool first = true;
       uint32_t qslot = 0, qphase = 0, sslot = 0, sphase = 0;
       // Greedy schedule: the producer claims its own tiles in table order
@@ -523,6 +542,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         prefetch_tmap(&md->a);
         prefetch_tmap(&md->b);
+        if (md->ring_narrow != layout) {
+          // drain: the last issued stage consumed means all are (in order)
+          if (last_slot >= 0) mbar_wait(&empty[last_slot], last_par);
+          layout = md->ring_narrow;
+          nslots = layout ? C::kNarrowSlots : kStages;
+          sbytes = layout ? C::kNarrowBytes : C::kStageBytes;
+          stage = 0;
+        }
         const int kb_lo = te.kb_end ? te.kb_begin : 0;
         const int k_blocks = te.kb_end ? te.kb_end : md->k_blocks;
         const uint32_t tx = md->tx_bytes;
@@ -566,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int taps = md->taps, images = md->images;
         const CUtensorMap* amap = &md->a;
         auto load_a = [&](int kb, uint32_t st) {
-          uint8_t* a_dst = ring + st * C::kStageBytes;
+          uint8_t* a_dst = ring + st * sbytes;
           if (fold) {
             // two filter rows; a row past R re-reads row 0 (its weights are zero)
 #pragma unroll
@@ -609,7 +636,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         };
         auto load_b = [&](int kb, uint32_t st) {
-          tma_load_2d(ring + st * C::kStageBytes + b_off, &md->b, &full[st], kb * kBK, n0);
+          tma_load_2d(ring + st * sbytes + b_off, &md->b, &full[st], kb * kBK, n0);
         };
         // Activation gate: the prerequisite grid (PDL) before the first tile,
         // and in a round program the tenant's previous layer (all its tiles
@@ -624,8 +651,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (trace) trace[6 * t + 0] = globaltimer();
         int kb = kb_lo;
         if (first) {
-          // All stages are free: stream the first stages' B tiles, then gate.
-          const int pre = min(k_blocks - kb_lo, kStages);
+          // All slots are free (stage 0, fresh barriers): stream the first
+          // stages' B tiles, then gate.
+          const int pre = min(k_blocks - kb_lo, static_cast<int>(nslots));
           for (int j = 0; j < pre; ++j) {
             mbar_expect_tx(&full[j], tx);
             load_b(kb_lo + j, j);
@@ -633,22 +661,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           gate();
           if (trace) trace[6 * t + 1] = globaltimer();
           first = false;
-          for (int j = 0; j < pre; ++j) load_a(kb_lo + j, j);
+          for (int j = 0; j < pre; ++j) {
+            load_a(kb_lo + j, j);
+            advance();
+          }
           kb = kb_lo + pre;
-          stage = pre % kStages;
-          phase = pre == kStages ? 1u : 0u;
         } else if (te.dep >= 0) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          wait_free();
           mbar_expect_tx(&full[stage], tx);
           load_b(kb_lo, stage);
           gate();
           if (trace) trace[6 * t + 1] = globaltimer();
           load_a(kb_lo, stage);
+          advance();
           kb = kb_lo + 1;
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
-          }
         }
         if (greedy) next = static_cast<int>(atomicAdd(ra.next_tile, 1u));  // latency hides under the loads
         // Steady state, specialised per A mode and tile height so the
@@ -658,10 +684,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           constexpr int kMode = decltype(mode_c)::value;
           constexpr int kTall = decltype(tall_c)::value;
           for (; kb < k_blocks; ++kb) {
-            mbar_wait(&empty[stage], phase ^ 1);
+            wait_free();
             uint64_t* bar = &full[stage];
             mbar_expect_tx(bar, tx);
-            uint8_t* a_dst = ring + stage * C::kStageBytes;
+            uint8_t* a_dst = ring + stage * sbytes;
             if constexpr (kMode == kATiled) {
               tma_load_2d(a_dst, amap, bar, kb * kBK, m0);
               if constexpr (kTall) tma_load_2d(a_dst + kABytes, amap, bar, kb * kBK, m0 + kBM);
@@ -689,10 +715,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
             tma_load_2d(a_dst + kABytes * (1 + kTall), &md->b, bar, kb * kBK, n0);
-            if (++stage == kStages) {
-              stage = 0;
-              phase ^= 1;
-            }
+            advance();
           }
         };
         using I0 = std::integral_constant<int, 0>;
@@ -714,14 +737,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             steady(std::integral_constant<int, kAIm2colFold>{}, I0{});
         } else {
           for (; kb < k_blocks; ++kb) {
-            mbar_wait(&empty[stage], phase ^ 1);
+            wait_free();
             mbar_expect_tx(&full[stage], tx);
             load_a(kb, stage);
             load_b(kb, stage);
-            if (++stage == kStages) {
-              stage = 0;
-              phase ^= 1;
-            }
+            advance();
           }
         }
       }
@@ -732,7 +752,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // The whole warp runs the loop on warp-uniform values (tile fields are
     // broadcast from lane 0 with shfl), so the descriptor arithmetic lives in
     // uniform registers; one elected lane issues tcgen05.mma / commit.
-    uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+    uint32_t stage = 0, fbits = 0, nslots = kStages, sbytes = C::kStageBytes, acc = 0, acc_phase = 0;
+    int layout = 0;
     uint32_t qslot = 0, qphase = 0;
     const uint32_t ring_base = smem_u32(ring);
     for (;;) {
@@ -751,6 +772,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int kb_lo = __shfl_sync(0xffffffffu, te.kb_end ? te.kb_begin : 0, 0);
       const int k_blocks = __shfl_sync(0xffffffffu, te.kb_end ? te.kb_end : md->k_blocks, 0);
       const uint32_t idesc = __shfl_sync(0xffffffffu, md->idesc, 0);
+      const int lay = __shfl_sync(0xffffffffu, md->ring_narrow, 0);
+      if (lay != layout) {  // the producer drained the ring before switching
+        layout = lay;
+        nslots = lay ? C::kNarrowSlots : kStages;
+        sbytes = lay ? C::kNarrowBytes : C::kStageBytes;
+        stage = 0;
+      }
       const int a_mode = __shfl_sync(0xffffffffu, md->a_mode, 0);
       const int tall = __shfl_sync(0xffffffffu, md->tall, 0);
       const uint32_t d_half = static_cast<uint32_t>(__shfl_sync(0xffffffffu, md->n_tile, 0));  // tall: 2nd half's columns
@@ -782,10 +810,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto kloop = [&](auto halves_c) {
         constexpr int kHalves = decltype(halves_c)::value;
         for (int kb = kb_lo; kb < k_blocks; ++kb) {
-          mbar_wait(&full[stage], phase);
+          mbar_wait(&full[stage], (fbits >> stage) & 1u);
           tc_fence_after();
           if (trace && kb == kb_lo && lane == 0) trace[6 * t + 2] = globaltimer();
-          const uint32_t a_addr = ring_base + stage * C::kStageBytes;
+          const uint32_t a_addr = ring_base + stage * sbytes;
           const uint32_t a_lo = ((a_addr >> 4) & 0x3FFFu) | a_lbo;
           const uint32_t b_lo = (((a_addr + (kABytes * kHalves)) >> 4) & 0x3FFFu) | (1u << 16);
           if (elect_one()) {
@@ -802,10 +830,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma_commit(&empty[stage]);  // frees the smem stage once these MMAs retire
           }
           __syncwarp();
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
-          }
+          fbits ^= 1u << stage;
+          stage = stage + 1 == nslots ? 0 : stage + 1;
         }
       };
       if (tall)
