@@ -1408,28 +1408,44 @@ int gm_graph_capture_round_e2e(gm_ctx* ctx, const gm_plans* p, size_t n, const i
     // DMA; the round kernel runs concurrently and starts a tenant's chain as
     // soon as its gate opens (the pre-pass blocks co-reside with the
     // persistent CTAs: 31 registers x 256 threads fit the SM's spare file)
-    cudaStream_t ss;
+    // (copies back to back on one stream; a tenant's layer-0 pre-pass and
+    // gate on a second, so pre-passes do not hold up the next tenant's copy)
+    cudaStream_t ss, sp;
     cuda_check(cudaStreamCreateWithFlags(&ss, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaStreamCreateWithFlags(&sp, cudaStreamNonBlocking), "cudaStreamCreate");
     g.streams.push_back(ss);
-    cudaEvent_t fork, join;
-    cuda_check(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "cudaEventCreate");
-    cuda_check(cudaEventCreateWithFlags(&join, cudaEventDisableTiming), "cudaEventCreate");
-    g.joins.push_back(fork);
-    g.joins.push_back(join);
+    g.streams.push_back(sp);
+    auto new_event = [&]() {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+      g.joins.push_back(e);
+      return e;
+    };
+    cudaEvent_t fork = new_event(), join = new_event(), copies = new_event();
     cuda_check(cudaEventRecord(fork, cs), "cudaEventRecord");
     cuda_check(cudaStreamWaitEvent(ss, fork, 0), "cudaStreamWaitEvent");
+    cuda_check(cudaStreamWaitEvent(sp, fork, 0), "cudaStreamWaitEvent");
     for (size_t i = 0; i < n; ++i) {
       cuda_check(cudaMemcpyAsync(d_in[i], h_in[i], in_bytes[i], cudaMemcpyHostToDevice, ss), "H2D query");
       std::vector<int> ops;
       for (int f : pr->gated_prepass)
         if (rt.flat[f].tenant == tenants[i]) ops.push_back(f);
-      g.kernels += rt.launch_prepass_ops(ops, ss, false);
+      cudaStream_t gs = ss;
+      if (!ops.empty()) {
+        cudaEvent_t landed = new_event();
+        cuda_check(cudaEventRecord(landed, ss), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(sp, landed, 0), "cudaStreamWaitEvent");
+        g.kernels += rt.launch_prepass_ops(ops, sp, false);
+        gs = sp;
+      }
       for (const auto& gt : pr->gates)
         if (gt.first == tenants[i])
-          cuda_check(cudaMemcpyAsync(pr->counters + gt.second, rt.host_one, sizeof(uint32_t), cudaMemcpyHostToDevice, ss),
+          cuda_check(cudaMemcpyAsync(pr->counters + gt.second, rt.host_one, sizeof(uint32_t), cudaMemcpyHostToDevice, gs),
                      "open input gate");
     }
-    cuda_check(cudaEventRecord(join, ss), "cudaEventRecord");
+    cuda_check(cudaEventRecord(copies, ss), "cudaEventRecord");
+    cuda_check(cudaStreamWaitEvent(sp, copies, 0), "cudaStreamWaitEvent");
+    cuda_check(cudaEventRecord(join, sp), "cudaEventRecord");
     g.kernels += rt.launch(*pr, cs, false);
     g.superkernels += 1;
     g.tiles += pr->n_tiles;

@@ -217,6 +217,14 @@ class SpaceTimeEngine:
         return Graph(h.value, False)
 
     # ------------------------------------------------------------ public serving call
+    def e2e_steady(self, host_inputs: Sequence[torch.Tensor], host_outputs: Sequence[torch.Tensor]) -> bool:
+        """True once serve_round replays a captured program for these host buffers."""
+        rnd = self._stable_plan
+        if rnd is None:
+            return False
+        key = (rnd.key, tuple(h.data_ptr() for h in host_inputs), tuple(h.data_ptr() for h in host_outputs))
+        return key in self._graphs
+
     def serve_round(self, host_inputs: Sequence[torch.Tensor], host_outputs: Sequence[torch.Tensor],
                     stream: torch.cuda.Stream) -> Round:
         """End-to-end round through the public API with host buffers.
