@@ -1314,12 +1314,16 @@ int gm_trace_round(gm_ctx* ctx, const gm_plans* p, uint64_t stream, uint64_t* ou
   if (n_tiles) *n_tiles = static_cast<size_t>(pr.n_tiles);
   const size_t words = static_cast<size_t>(pr.n_tiles) * 6;
   if (!out || cap < words) throw RangeError("output buffer too small");
+  // the kernel also stamps 6 words per CTA after the tiles (SM cycles: entry,
+  // setup, loops, barrier, TMEM released, exit); returned when the buffer has room
+  const size_t all = words + 6 * static_cast<size_t>(std::max(1, std::min(pr.n_tiles, rt.sms)));
+  const size_t copy = cap >= all ? all : words;
   uint64_t* d_trace = nullptr;
-  cuda_check(cudaMalloc(&d_trace, words * sizeof(uint64_t)), "cudaMalloc(trace)");
+  cuda_check(cudaMalloc(&d_trace, all * sizeof(uint64_t)), "cudaMalloc(trace)");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  cudaMemsetAsync(d_trace, 0, words * sizeof(uint64_t), s);
+  cudaMemsetAsync(d_trace, 0, all * sizeof(uint64_t), s);
   rt.launch(pr, s, true, nullptr, nullptr, d_trace);
-  cudaError_t e = cudaMemcpyAsync(out, d_trace, words * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+  cudaError_t e = cudaMemcpyAsync(out, d_trace, copy * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   cudaFree(d_trace);
   cuda_check(e, "trace copy");

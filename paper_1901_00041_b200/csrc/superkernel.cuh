@@ -440,6 +440,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // trace (debug): per CTA after the tile stamps, SM clock64 cycles: entry,
+  // setup done, producer loop done, all roles done (warp 2 past the final
+  // barrier), TMEM released, exit
+  uint64_t* cta_trace = trace ? trace + 6 * n_tiles + 6 * blockIdx.x : nullptr;
+  if (cta_trace && threadIdx.x == 0) cta_trace[0] = clock64();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kMaxSlots; ++s) {
@@ -470,6 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (cta_trace && threadIdx.x == 0) cta_trace[1] = clock64();
   // Let the next launch in the stream (programmatic dependent launch) start
   // its prologue on SMs this grid frees; it waits in griddepcontrol.wait.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -1082,12 +1088,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
 
+  // (ptxas may hoist this stamp above the barrier: it reads as the
+  // producer's loop end; warp 2's stamp below is the barrier release)
+  if (cta_trace && threadIdx.x == 0) cta_trace[2] = clock64();
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
+    if (cta_trace && lane == 0) cta_trace[3] = clock64();
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::kTmemCols)
                  : "memory");
+    if (cta_trace && lane == 0) cta_trace[4] = clock64();
   }
   // Round programs reset their own completion counters: the last CTA to
   // finish zeroes them, so a replay needs no memset node before the kernel.
@@ -1105,6 +1116,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (threadIdx.x == 0) *ra.exit_ctr = 0;
     }
   }
+  if (cta_trace && threadIdx.x == 0) cta_trace[5] = clock64();
 }
 
 // Registration-time repack of narrow-channel conv weights: KRSC rows with

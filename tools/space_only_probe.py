@@ -33,8 +33,10 @@ def main():
     buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.Stream()
     print("CUDA_DEVICE_MAX_CONNECTIONS", os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS"))
-    for r in [int(x) for x in sys.argv[1:]] or [16, 32, 64, 80, 100, 120]:
-        eng = SpaceTimeEngine([W.conv2_2()] * r, [1] * r, device_index=0)
+    opts = {a.split("=")[0]: int(a.split("=")[1]) for a in sys.argv[1:] if "=" in a}
+    flush = (lambda: None) if "noflush" in sys.argv else (lambda: buf.fill_(1))
+    for r in [int(x) for x in sys.argv[1:] if "=" not in x and x.isdigit()] or [16, 32, 64, 80, 100, 120]:
+        eng = SpaceTimeEngine([W.conv2_2()] * r, [1] * r, device_index=0, options=opts)
         flops = eng.flops_per_round()
         gsp = eng.capture_serial("space_only")
         gpk = eng.capture_round(eng.plan_round())
@@ -43,7 +45,7 @@ def main():
             gpk.launch(stream.cuda_stream)
         res = {}
         for name, g in (("space_graph", gsp), ("packed", gpk)):
-            ms = timeit(lambda: g.launch(stream.cuda_stream), stream, lambda: buf.fill_(1))
+            ms = timeit(lambda: g.launch(stream.cuda_stream), stream, flush)
             res[name] = round(flops / ms / 1e9, 1)
         print("R", r, "tflops", res, "kernels", gsp.kernels, flush=True)
         del eng, gsp, gpk

@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(128, 1) feed(const __grid_constant__ CUtensorM
       asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
                    ::"r"(sa(dst)), "l"((uint64_t)&ma), "r"(sa(&full[s])), "r"(0), "r"(row) : "memory");
       const int brow = ((blockIdx.x * 3 + i) * b_rows) % rows_total;
-      asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+      if (b_rows) asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
                    ::"r"(sa(dst + a_rows * 128)), "l"((uint64_t)&mb), "r"(sa(&full[s])), "r"(0), "r"(brow) : "memory");
       ti += clock64() - c1;
     }
@@ -70,13 +70,15 @@ __global__ void __launch_bounds__(128, 1) feed(const __grid_constant__ CUtensorM
     for (int i = 0; i < iters; ++i) {
       const int s = i % stages;
       wait(&full[s], (i / stages) & 1);
-      if (work == 1) {
+      if (work >= 1 && work <= 4) {
         // real tcgen05.mma: 4 x (M=128, N=b_rows, K=16) from the stage, commit frees it
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t a = sa(ring + s * stage_bytes), b = a + a_rows * 128;
         const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(b_rows >> 3) << 17) | ((128u >> 4) << 24);
-        for (int k = 0; k < 4; ++k) {
-          const uint64_t da = sw128(a + k * 32), db = sw128(b + k * 32);
+        // work 1: 4 MMAs (one K=64 k-block), 2: 8 (the k-block twice), 3: 2, 4: 1
+        const int nmma = work == 1 ? 4 : work == 2 ? 8 : work == 3 ? 2 : 1;
+        for (int k = 0; k < nmma; ++k) {
+          const uint64_t da = sw128(a + (k & 3) * 32), db = sw128(b + (k & 3) * 32);
           asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}"
                        ::"r"(tmem_base), "l"(da), "l"(db), "r"(idesc), "r"(1));
         }
@@ -89,7 +91,7 @@ __global__ void __launch_bounds__(128, 1) feed(const __grid_constant__ CUtensorM
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(&empty[s])) : "memory");
     }
   }
-  if (threadIdx.x == 32 && work == 1) wait(&empty[(iters - 1) % stages], ((iters - 1) / stages) & 1);
+  if (threadIdx.x == 32 && work >= 1 && work <= 4) wait(&empty[(iters - 1) % stages], ((iters - 1) / stages) & 1);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -126,12 +128,17 @@ int main(int argc, char** argv) {
       {128, 256, 4, 8, 0},   {128, 256, 4, 8, 1},   {128, 256, 3, 8, 1},   {128, 256, 4, 148, 1}, {128, 256, 4, 8, 250},
       {128, 128, 6, 8, 1},   {128, 128, 4, 8, 1},   {128, 128, 6, 148, 1}, {128, 64, 8, 8, 1},    {128, 64, 4, 8, 1},
       {128, 64, 8, 148, 1},  {64, 64, 8, 8, 250},   {64, 64, 8, 8, 0},     {8, 8, 8, 8, 500},     {8, 8, 2, 8, 500},
+      // one TMA per stage (no B box): is the floor per instruction or per stage?
+      {128, 0, 4, 8, 0},     {256, 0, 4, 8, 0},     {8, 0, 4, 8, 0},       {128, 0, 8, 148, 0},
+      // MMAs per stage: 8 / 2 / 1 (work 2 / 3 / 4)
+      {128, 256, 4, 8, 2},   {128, 256, 4, 8, 3},   {128, 256, 4, 8, 4},   {128, 128, 6, 8, 2},   {128, 128, 6, 8, 3},
+      {128, 128, 6, 8, 4},   {128, 64, 8, 8, 2},    {128, 64, 8, 8, 4},
   };
   for (auto& c : cfgs) {
     CUtensorMap ma, mb;
     cuuint64_t dims[2] = {64, (cuuint64_t)rows_total};
     cuuint64_t str[1] = {128};
-    cuuint32_t boxa[2] = {64, (cuuint32_t)c.a}, boxb[2] = {64, (cuuint32_t)c.b}, es[2] = {1, 1};
+    cuuint32_t boxa[2] = {64, (cuuint32_t)c.a}, boxb[2] = {64, (cuuint32_t)(c.b ? c.b : 8)}, es[2] = {1, 1};
     enc(&ma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, str, boxa, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     enc(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, str, boxb, es, CU_TENSOR_MAP_INTERLEAVE_NONE,

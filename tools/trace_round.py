@@ -47,7 +47,7 @@ def main():
     lib().gm_round_tiles(eng.ctx.handle, rnd.handle, None, 0, C.byref(n))
     tiles = (N.gm_tile * n.value)()
     check(lib().gm_round_tiles(eng.ctx.handle, rnd.handle, tiles, n.value, C.byref(n)))
-    buf = (C.c_uint64 * (6 * n.value))()
+    buf = (C.c_uint64 * (6 * n.value + 6 * 148))()
     nt = C.c_size_t()
     check(lib().gm_trace_round(eng.ctx.handle, rnd.handle, s.cuda_stream, buf, len(buf), C.byref(nt)))
     t = [[buf[6 * i + j] for j in range(6)] for i in range(n.value)]
@@ -74,6 +74,14 @@ def main():
         print(f"{pi:3d} {k.shape_signature:22s} tiles={len(ts):4d} start={start:7.1f} span={span:6.1f}us "
               f"roof={roof:5.1f} | gate={row['gate']:5.2f} load={row['load']:5.2f} mma={row['mma']:5.2f} "
               f"drain={row['drain']:5.2f} epi={row['epi']:5.2f}")
+    grid = min(n.value, 148)
+    cta = [[buf[6 * n.value + 6 * c + j] for j in range(6)] for c in range(grid)]
+    if all(x[0] for x in cta):
+        # SM cycles from each CTA's own entry (clock64; not comparable across SMs)
+        names = ["setup", "producer-done", "barrier", "tmem-freed", "exit"]
+        print("CTA phases, cycles from entry (min/med/max): " + ", ".join(
+            "%s %d/%d/%d" % (nm, *(lambda v: (v[0], v[len(v) // 2], v[-1]))(
+                sorted(x[j + 1] - x[0] for x in cta))) for j, nm in enumerate(names)))
     total = (max(x[5] for x in t) - t0) / 1e3
     print(f"kernel span {total:.1f}us, roofline {tot_roof:.1f}us, tiles {n.value}")
     if a.out:
