@@ -379,7 +379,19 @@ def run_ours(args):
         eng.serve_round(h_in, h_out, stream)
         e2e_times.append(time.perf_counter() - t0)
     barrier()
-    e2e_s = max_over_ranks(sum(e2e_times) / len(e2e_times))
+    e2e_sync_s = max_over_ranks(sum(e2e_times) / len(e2e_times))
+    # back-to-back rounds through the double-buffered public call: two sets of
+    # pinned host batches alternating, every step's H2D and D2H inside the
+    # timed region (pipeline fill and drain included)
+    h_in2 = [h.clone().pin_memory() for h in h_in]
+    h_out2 = [torch.empty_like(h).pin_memory() for h in h_out]
+    sets = [(h_in, h_out), (h_in2, h_out2)]
+    eng.serve_rounds([sets[i & 1] for i in range(max(args.warmup, 2))], stream)
+    barrier()
+    t0 = time.perf_counter()
+    eng.serve_rounds([sets[i & 1] for i in range(args.steps)], stream)
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps)
+    barrier()
     h2d = sum(t.numel() * t.element_size() for t in h_in)
     d2h = sum(t.numel() * t.element_size() for t in h_out)
 
@@ -486,8 +498,14 @@ def run_ours(args):
         },
         "e2e": {"value": world * flops_round / e2e_s / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
-                "median_ms": sorted(e2e_times)[len(e2e_times) // 2] * 1e3, "min_ms": min(e2e_times) * 1e3,
-                "api": "SpaceTimeEngine.serve_round (steady-state plan; one graph: per-tenant H2D gating its chain in the round kernel, D2H), pinned host buffers"},
+                "api": "SpaceTimeEngine.serve_rounds: K back-to-back rounds from pinned host batches (two sets "
+                       "alternating), double-buffered: step i+1's H2D overlaps round i; every step's H2D, D2D "
+                       "staging move, round program and D2H inside the timed wall-clock region",
+                "single_round": {"value": world * flops_round / e2e_sync_s / 1e12, "ms_per_step": e2e_sync_s * 1e3,
+                                 "median_ms": sorted(e2e_times)[len(e2e_times) // 2] * 1e3,
+                                 "min_ms": min(e2e_times) * 1e3,
+                                 "api": "SpaceTimeEngine.serve_round, one synchronous round per call (one graph: "
+                                        "per-tenant H2D gating its chain in the round kernel, D2H)"}},
         "gpu_launches": args.steps * g_packed.kernels,
         "clocks": clocks.summary(),
     }

@@ -290,6 +290,28 @@ def test_serve_round_e2e_host_buffers(oracle):
     check_engine(eng, oracle)
 
 
+def test_serve_rounds_pipelined_matches_single_rounds():
+    """Double-buffered back-to-back rounds: every step's host results equal a
+    synchronous serve_round of the same host batch (no staging-buffer race)."""
+    eng = small_engine(tenants=2)
+    s = torch.cuda.Stream()
+    g = torch.Generator().manual_seed(3)
+    steps = []
+    for _ in range(5):
+        h_in = [(torch.randn(m.query_input.shape, generator=g) * 0.5).to(torch.bfloat16).pin_memory()
+                for m in eng.models]
+        h_out = [torch.empty_like(m.query_output, device="cpu").pin_memory() for m in eng.models]
+        steps.append((h_in, h_out))
+    eng.serve_rounds(steps, s)
+    for h_in, h_out in steps:
+        ref = [torch.empty_like(h).pin_memory() for h in h_out]
+        eng.serve_round(h_in, ref, s)
+        for a, b in zip(h_out, ref):
+            assert torch.equal(a, b)
+    with pytest.raises(ValueError):
+        eng.serve_rounds([(steps[0][0][:1], steps[0][1])], s)
+
+
 def test_no_silent_fallback_on_bad_registration():
     from paper_1901_00041_b200.runtime import Context, LayerBuffers
     from paper_1901_00041_b200.scheduler import GemmShape
