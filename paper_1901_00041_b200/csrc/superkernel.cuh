@@ -681,6 +681,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           load_a(kb_lo, stage);
           advance();
           kb = kb_lo + 1;
+        } else if (trace) {
+          trace[6 * t + 1] = globaltimer();  // no gate
         }
         if (greedy) next = static_cast<int>(atomicAdd(ra.next_tile, 1u));  // latency hides under the loads
         // Steady state, specialised per A mode and tile height so the
