@@ -332,6 +332,13 @@ int gm_ctx_set_policy(gm_ctx* ctx, const gm_batch_policy* p);
  *                       that count as throughput-bound (0 = 2 x SMs)
  *   "split_k"           round programs split few-tile long-K members (0);
  *                       "max_splits" (4), "split_min_kb" (8)
+ *   "skinny_min_mb"     round programs split weight-streaming GEMM members
+ *                       (M <= 64, at least this many MB of weights, e.g. fc6)
+ *                       over K across the idle SMs; 0 = off (64);
+ *                       "skinny_max_splits" (8)
+ *   "ring_layouts"      narrow members use a 6 x 32 KB operand ring (1)
+ *   "critical_order"    round tile order: -1 auto, 0 plan, 1 remaining work,
+ *                       2 chain progress (-1)
  *   "greedy_schedule"   greedy in-order tile claiming instead of static
  *                       round-robin (0); "dynamic_schedule": per-tenant queues (0)
  *   "row_fold"          row-folded im2col for RGB stems (1)

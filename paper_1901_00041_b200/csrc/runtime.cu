@@ -141,6 +141,11 @@ struct Runtime {
   bool split_k = false;      // round programs split few-tile long-K members (opt-in)
   int64_t max_splits = 4;
   int64_t split_min_kb = 8;  // fewest k-blocks per split
+  // Weight-streaming members (M <= 64 rows, >= skinny_min_mb MB of weights,
+  // e.g. VGG's fc6/fc7): full-width tiles split over K so the weights stream
+  // through (up to) every SM; their fp32 partials are few (M rows).  0 = off.
+  int64_t skinny_min_mb = 64;
+  int64_t skinny_max_splits = 8;
   int64_t narrow_min_tiles = 20;  // >0: in a plan that cannot fill the SMs, narrow a member's N tile
                                  // (256 -> 128 -> 64) until it has this many tiles
   bool row_fold = true;          // S*Cin <= 32 convs (RGB stems) use the row-folded im2col path
@@ -639,6 +644,18 @@ struct Runtime {
       for (int f : pl) {
         const Operator& op = flat[f];
         auto [slot, w] = variant(f, plan_tiles, shape_tiles[op.shape]);
+        int skinny_splits = 1;
+        if (skinny_min_mb > 0 && op.kind == GM_LAYER_GEMM && op.shape.m <= 64 &&
+            op.shape.n * op.shape.k * 2 >= skinny_min_mb * (int64_t{1} << 20)) {
+          const dev::MemberDesc& hd = host_desc[op.slot];
+          const int64_t conc = std::max<int64_t>(1, shape_tiles[op.shape]);  // full-width tiles of the shape in the round
+          const int64_t sp = std::min<int64_t>({hd.k_blocks / split_min_kb, sms / conc, skinny_max_splits});
+          if (hd.a_mode == dev::kATiled && sp >= 2) {
+            slot = op.slot;
+            w = op.n_tile;
+            skinny_splits = static_cast<int>(sp);
+          }
+        }
         const bool tall = is_tall(slot);
         const int inst = static_cast<int>(targets.size());
         int dep = -1;
@@ -659,7 +676,11 @@ struct Runtime {
         // Split-K when the plan cannot fill the SMs and the K loop is long:
         // about two waves of tiles, at least 4 k-blocks per split.
         int splits = 1;
-        if (split_k && !tall && plan_tiles < sms && kb >= 2 * split_min_kb) {
+        if (skinny_splits > 1) {
+          const int kbw = host_desc[slot].k_blocks;
+          const int chunk = (kbw + skinny_splits - 1) / skinny_splits;
+          splits = (kbw + chunk - 1) / chunk;
+        } else if (split_k && !tall && plan_tiles < sms && kb >= 2 * split_min_kb) {
           splits = static_cast<int>(
               std::min<int64_t>({kb / split_min_kb, (sms + plan_tiles - 1) / plan_tiles, max_splits}));
           const int chunk = (kb + splits - 1) / splits;
@@ -674,12 +695,13 @@ struct Runtime {
                                              static_cast<uint16_t>(b), inst, dep, 0, 0, -1});
               continue;
             }
-            const int chunk = (kb + splits - 1) / splits;
+            const int kbt = host_desc[slot].k_blocks;  // the kernel's K loop (padded channels included)
+            const int chunk = (kbt + splits - 1) / splits;
             for (int s = 0; s < splits; ++s)
               table.push_back(dev::TileEntry{static_cast<uint16_t>(slot), static_cast<uint16_t>(splits),
                                              static_cast<uint16_t>(a), static_cast<uint16_t>(b), inst, dep,
                                              static_cast<uint16_t>(s * chunk),
-                                             static_cast<uint16_t>(std::min(kb, (s + 1) * chunk)), n_ws});
+                                             static_cast<uint16_t>(std::min(kbt, (s + 1) * chunk)), n_ws});
             ++n_ws;
           }
         if (op.prepass) (gated && op.layer == 0 ? p.gated_prepass : p.prepass_ops).push_back(f);
@@ -1067,6 +1089,12 @@ int gm_ctx_set_option(gm_ctx* ctx, const char* name, int64_t value) {
     rt.max_splits = value;
   } else if (n == "dynamic_schedule") {
     rt.dynamic_schedule = value != 0;  // applies to round programs prepared afterwards
+  } else if (n == "skinny_min_mb") {
+    if (value < 0) throw std::invalid_argument("skinny_min_mb must be >= 0");
+    rt.skinny_min_mb = value;  // applies to round programs prepared afterwards
+  } else if (n == "skinny_max_splits") {
+    if (value < 2 || value > 64) throw std::invalid_argument("skinny_max_splits must be in [2, 64]");
+    rt.skinny_max_splits = value;
   } else if (n == "split_min_kb") {
     if (value < 1 || value > 1024) throw std::invalid_argument("split_min_kb must be in [1, 1024]");
     rt.split_min_kb = value;

@@ -266,7 +266,9 @@ def test_heterogeneous_models_round_program(oracle):
                                      {"tall_min_tiles": 1}, {"tall_min_tiles": 1, "narrow_min_tiles": 0},
                                      {"tall_tiles": 0, "narrow_min_tiles": 0}, {"critical_order": 0},
                                      {"critical_order": 1}, {"critical_order": 2, "greedy_schedule": 1},
-                                     {"ring_layouts": 0}])
+                                     {"ring_layouts": 0}, {"skinny_min_mb": 0},
+                                     {"skinny_min_mb": 1, "split_min_kb": 2},
+                                     {"skinny_min_mb": 1, "split_min_kb": 1, "skinny_max_splits": 64}])
 def test_execution_options_keep_results(oracle, options):
     eng = small_engine(tenants=2, batch=4, options=options)
     rnd = eng.plan_round()
