@@ -62,11 +62,14 @@ def bench_rows(line: dict, peak_tflops: Optional[float] = None, seed: int = 42) 
             "throughput_gflops": r["tflops"] * 1e3, "utilization": r["tflops"] / peak,
             "mean_ms": r["ms_per_step"], "p50_ms": r["ms_per_step"], "p99_ms": r["p99_ms"],
             "launches": r["launches_per_step"]}))
-    for row in line.get("table1", {}).get("rows", []):
-        for mode, policy in MODE_POLICY.items():
-            tf = row[mode + "_tflops"]
-            rows.append(csv_line("resnet18-conv2_2", policy, row["R"], 1, seed, "ok", {
-                "throughput_gflops": tf * 1e3, "utilization": tf / peak}))
+    t1 = line.get("table1", {})
+    suites = [("resnet18-conv2_2", t1)] + list(t1.get("other_presets", {}).items())
+    for name, suite in suites:
+        for row in suite.get("rows", []):
+            for mode, policy in MODE_POLICY.items():
+                tf = row[mode + "_tflops"]
+                rows.append(csv_line(name, policy, row["R"], 1, seed, "ok", {
+                    "throughput_gflops": tf * 1e3, "utilization": tf / peak}))
     return rows
 
 

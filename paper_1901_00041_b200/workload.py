@@ -218,6 +218,30 @@ def conv2_2() -> List[Layer]:
     return [_conv("conv2_2", 16, 128, 128, 3, 1, 1)]
 
 
+def table1_layers(preset: str) -> List[Layer]:
+    """One tenant's operator for the paper's Table-1 microbenchmarks
+    (reference presets, workload.cpp:18-20): ``resnet18-conv2_2`` as the real
+    3x3 conv (implicit GEMM through TMA im2col), ``square-256`` and
+    ``rnn-matvec`` as GEMMs.  The matvec's N = 1 is computed as N = 8 (output
+    rows must be 16-byte aligned for the TMA store); its FLOPs are counted at
+    the reference shape (``table1_flops``)."""
+    if preset == "resnet18-conv2_2":
+        return conv2_2()
+    p = find_preset(preset)
+    if p is None:
+        raise KeyError(preset)
+    s = p.layers[0]
+    return [Layer(preset, "gemm", rows=s.m, n=max(s.n, 8), k=s.k)]
+
+
+def table1_flops(preset: str) -> int:
+    """Reference FLOPs of one Table-1 member (2mnk at the preset's shape)."""
+    if preset == "resnet18-conv2_2":
+        return conv2_2()[0].flops(1)
+    s = find_preset(preset).layers[0]
+    return 2 * s.m * s.n * s.k
+
+
 MODELS = {
     "resnet50": resnet50,
     "resnet18": resnet18,

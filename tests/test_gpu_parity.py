@@ -116,6 +116,8 @@ CASES = {
     "gemm M=1 (fc b1)": lambda: gemm_layer(1, 1000, 2048),
     "gemm bert qkv 128x2304x768": lambda: gemm_layer(128, 2304, 768),
     "gemm relu": lambda: gemm_layer(130, 136, 200, relu=True),
+    "gemm N=8 (rnn-matvec at N=8) 512x8x512": lambda: gemm_layer(512, 8, 512),
+    "gemm square-256": lambda: gemm_layer(256, 256, 256),
     "conv 3x3 s1 p1 16x16x128->128 b2 (im2col TMA)": lambda: conv_layer(2, 16, 128, 128, 3, 1, 1),
     "conv 3x3 s2 p1 28x28x64->128": lambda: conv_layer(1, 28, 64, 128, 3, 2, 1),
     "conv 1x1 s1 14x14x256->512 b3 (tiled GEMM)": lambda: conv_layer(3, 14, 256, 512, 1, 1, 0),

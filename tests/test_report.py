@@ -33,3 +33,13 @@ def test_bench_line_rows():
     rows = report.bench_rows(line)
     assert len(rows) == 3 + 3 * len(line["table1"]["rows"])
     assert {r.split(",")[2] for r in rows} == {"space-time", "time-mux", "space-implicit"}
+
+
+def test_bench_rows_cover_every_table1_preset():
+    row = {"R": 2, "packed_tflops": 1.0, "time_only_tflops": 0.5, "space_only_tflops": 0.8}
+    line = {"modes": {}, "table1": {"rows": [row], "other_presets": {"rnn-matvec": {"rows": [row, row]},
+                                                                     "square-256": {"rows": [row]}}}}
+    rows = report.bench_rows(line, peak_tflops=1000.0)
+    assert len(rows) == 3 * 4
+    assert {r.split(",")[1] for r in rows} == {"resnet18-conv2_2", "rnn-matvec", "square-256"}
+
