@@ -29,8 +29,8 @@ def build(config, opts):
         name, b = config[5:].rsplit("b", 1)
         layers = {"vgg16": W.vgg16(224), "resnet50": W.resnet50(224), "mobilenet": W.mobilenet_v2(224)}[name]
         return SpaceTimeEngine([layers], [int(b)], options=opts)
-    if config == "bert4":
-        return SpaceTimeEngine([W.bert_base_gemms(128, 12)] * 16, [4] * 16, options=opts)
+    if config.startswith("bert"):  # bert<B>: 16 tenants x BERT-base (12 layers), batch B
+        return SpaceTimeEngine([W.bert_base_gemms(128, 12)] * 16, [int(config[4:])] * 16, options=opts)
     raise SystemExit(config)
 
 
