@@ -103,6 +103,7 @@ struct Prepared {
   uint32_t* heads = nullptr;
   int32_t* qinfo = nullptr;  // [nq] begins then [nq] lengths
   int nq = 0;
+  bool self_reset = true;  // round programs: counters in use, the last CTA resets them
   bool greedy = false;  // greedy in-order claiming (one claim counter after the counters and queue heads)
   // input-gated round programs (end-to-end serving): per tenant, a counter
   // (target 1) its first layer depends on, set by a 4-byte DMA after the
@@ -789,6 +790,22 @@ struct Runtime {
       }
     }
     p.nq = static_cast<int>(qbeg.size());
+    // Members nothing waits on (each tenant's last layer of the round; every
+    // member of a single-layer round) skip the publish -- store-completion
+    // wait, fence and counter atomic on the tail of their chain.  A round
+    // whose tiles neither publish nor wait needs no counters at all, so its
+    // launch also skips the last-CTA reset (the exit counter).
+    {
+      std::vector<char> needed(targets.size(), 0);
+      for (const auto& te : table)
+        if (te.dep >= 0) needed[te.dep] = 1;
+      bool used = greedy_schedule || p.nq > 0;
+      for (auto& te : table) {
+        if (te.splits <= 1 && te.done >= 0 && !needed[te.done]) te.done = -1;
+        used = used || te.done >= 0 || te.dep >= 0;
+      }
+      p.self_reset = used;
+    }
     p.n_tiles = static_cast<int>(table.size());
     p.n_counters = static_cast<int>(targets.size());
     p.n_ws = n_ws;
@@ -916,7 +933,8 @@ struct Runtime {
     dev::RoundArgs ra{counters, targets, p.ws_map, p.ws, p.split_ctr, trace,
                       p.heads, p.qinfo, p.qinfo ? p.qinfo + p.nq : nullptr, p.nq,
                       p.greedy ? p.counters + p.n_counters + p.nq : nullptr,
-                      p.counters ? p.counters + p.n_counters + p.nq + 1 : nullptr, p.n_counters + p.nq + 1};
+                      p.counters && p.self_reset ? p.counters + p.n_counters + p.nq + 1 : nullptr,
+                      p.n_counters + p.nq + 1};
     void* args[4] = {&slots, &tiles, &n, &ra};
     cuda_check(cudaLaunchKernelExC(&cfg, kernel, args), "launch superkernel");
     if (ev_end) cuda_check(cudaEventRecordWithFlags(ev_end, stream, cudaEventRecordExternal), "event record");
