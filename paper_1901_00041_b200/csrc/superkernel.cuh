@@ -445,6 +445,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   // barrier), TMEM released, exit
   uint64_t* cta_trace = trace ? trace + 6 * n_tiles + 6 * blockIdx.x : nullptr;
   if (cta_trace && threadIdx.x == 0) cta_trace[0] = clock64();
+  // Static schedule: this CTA's first tile is blockIdx.x.  While thread 0 and
+  // warp 2 set up barriers and TMEM, the idle scheduler lane pulls that
+  // tile's entry, member descriptor and tensor maps toward the SM, so the
+  // producer's and MMA warp's first reads hit L1 instead of L2.
+  if (warp == 3 && lane == 0 && !ra.heads && !ra.next_tile && static_cast<int>(blockIdx.x) < n_tiles) {
+    const MemberDesc* md0 = slots + tiles[blockIdx.x].member;
+    const char* p0 = reinterpret_cast<const char*>(md0);
+#pragma unroll
+    for (int i = 0; i < static_cast<int>(sizeof(MemberDesc)); i += 128)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(p0 + i));
+    prefetch_tmap(&md0->a);
+    prefetch_tmap(&md0->b);
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kMaxSlots; ++s) {
