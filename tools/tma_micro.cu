@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(128, 1) feed(const __grid_constant__ CUtensorM
   if (threadIdx.x == 0) {
     for (int i = 0; i < 16; ++i) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&full[i])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&empty[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(&empty[i])), "r"(work == 5 ? 2 : 1));
     }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
@@ -66,6 +66,23 @@ __global__ void __launch_bounds__(128, 1) feed(const __grid_constant__ CUtensorM
                    ::"r"(sa(dst + a_rows * 128)), "l"((uint64_t)&mb), "r"(sa(&full[s])), "r"(0), "r"(brow) : "memory");
       ti += clock64() - c1;
     }
+  } else if (work == 5 && (threadIdx.x == 32 || threadIdx.x == 64)) {
+    // two issuing threads (warps 1 and 2), 4 MMAs each per stage into their
+    // own accumulator columns; each commit is one of the stage's two arrivals
+    const uint32_t dcol = threadIdx.x == 64 ? 256u : 0u;
+    for (int i = 0; i < iters; ++i) {
+      const int s = i % stages;
+      wait(&full[s], (i / stages) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t a = sa(ring + s * stage_bytes), b = a + a_rows * 128;
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(b_rows >> 3) << 17) | ((128u >> 4) << 24);
+      for (int k = 0; k < 4; ++k) {
+        const uint64_t da = sw128(a + k * 32), db = sw128(b + k * 32);
+        asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}"
+                     ::"r"(tmem_base + dcol), "l"(da), "l"(db), "r"(idesc), "r"(1));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sa(&empty[s])) : "memory");
+    }
   } else if (threadIdx.x == 32) {
     for (int i = 0; i < iters; ++i) {
       const int s = i % stages;
@@ -91,7 +108,7 @@ __global__ void __launch_bounds__(128, 1) feed(const __grid_constant__ CUtensorM
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(&empty[s])) : "memory");
     }
   }
-  if (threadIdx.x == 32 && work >= 1 && work <= 4) wait(&empty[(iters - 1) % stages], ((iters - 1) / stages) & 1);
+  if ((threadIdx.x == 32 && ((work >= 1 && work <= 4) || work == 5))) wait(&empty[(iters - 1) % stages], ((iters - 1) / stages) & 1);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -130,6 +147,8 @@ int main(int argc, char** argv) {
       {128, 64, 8, 148, 1},  {64, 64, 8, 8, 250},   {64, 64, 8, 8, 0},     {8, 8, 8, 8, 500},     {8, 8, 2, 8, 500},
       // one TMA per stage (no B box): is the floor per instruction or per stage?
       {128, 0, 4, 8, 0},     {256, 0, 4, 8, 0},     {8, 0, 4, 8, 0},       {128, 0, 8, 148, 0},
+      // two issuing warps x 4 MMAs per stage (work 5) vs one warp x 8 (work 2)
+      {128, 64, 8, 8, 5},    {128, 128, 6, 8, 5},   {128, 256, 4, 8, 5},
       // MMAs per stage: 8 / 2 / 1 (work 2 / 3 / 4)
       {128, 256, 4, 8, 2},   {128, 256, 4, 8, 3},   {128, 256, 4, 8, 4},   {128, 128, 6, 8, 2},   {128, 128, 6, 8, 3},
       {128, 128, 6, 8, 4},   {128, 64, 8, 8, 2},    {128, 64, 8, 8, 4},
