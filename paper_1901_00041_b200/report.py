@@ -79,3 +79,97 @@ def write_csv(path: str, rows: Iterable[str]) -> None:
         f.write(CSV_HEADER + "\n")
         for r in rows:
             f.write(r + "\n")
+
+
+# ---------------------------------------------------------------- report --kind table1
+
+# PolicyKind order (policies.hpp:16-22): ties in the next-best count go to the
+# earlier kind, as std::map iteration does in speedup_table.
+_COMPETITORS = ("time-mux", "space-implicit", "space-explicit")
+
+
+def read_csv(path: str) -> List[Dict[str, str]]:
+    """csv.cpp:75-87: header must match, blank lines skipped."""
+    with open(path) as f:
+        lines = f.read().splitlines()
+    if not lines:
+        raise ValueError(f"csv: empty file {path}")
+    if lines[0] != CSV_HEADER:
+        raise ValueError(f"csv: unexpected header in {path}")
+    cols = CSV_HEADER.split(",")
+    out = []
+    for ln in lines[1:]:
+        if ln:
+            vals = ln.split(",")
+            if len(vals) != len(cols):
+                raise ValueError(f"csv: bad row in {path}: {ln}")
+            out.append(dict(zip(cols, vals)))
+    return out
+
+
+def speedup_table(rows: Iterable[Dict[str, str]], workload: str,
+                  r_range: Optional[Iterable[int]] = None) -> Dict[str, object]:
+    """metrics.cpp:90-138 over the ok rows of one workload: per R, space-time
+    throughput / the best competitor's, the geomean of those ratios, and the
+    most frequent best competitor.  Competitors absent from every row are
+    skipped (this path measures time-mux and space-implicit); a missing cell
+    of a present policy raises like the reference."""
+    from .scheduler import geomean
+    cells = {(r["policy"], int(r["replicas"])): float(r["throughput_gflops"])
+             for r in rows if r["workload"] == workload and r["status"] == "ok"}
+    present = [p for p in _COMPETITORS if any(k[0] == p for k in cells)]
+    if not present:
+        raise ValueError(f"speedup_table: no competitor rows for workload={workload}")
+    rs = sorted({k[1] for k in cells}) if r_range is None else list(r_range)
+    out_rows, wins = [], {p: 0 for p in present}
+    for r in rs:
+        if ("space-time", r) not in cells:
+            raise ValueError(f"speedup_table: missing cell workload={workload} R={r} policy=space-time")
+        best, best_p = 0.0, present[0]
+        for p in present:
+            if (p, r) not in cells:
+                raise ValueError(f"speedup_table: missing cell workload={workload} R={r} policy={p}")
+            if cells[(p, r)] > best:
+                best, best_p = cells[(p, r)], p
+        out_rows.append({"R": r, "speedup": cells[("space-time", r)] / best, "next_best": best_p})
+        wins[best_p] += 1
+    top = max(wins.values())
+    return {"workload": workload, "rows": out_rows, "geomean_speedup": geomean([x["speedup"] for x in out_rows]),
+            "next_best": next(p for p in present if wins[p] == top)}
+
+
+def table1_report(rows: List[Dict[str, str]], workloads: Optional[Iterable[str]] = None) -> str:
+    """`gpumux report --kind table1` (gpumux.cpp:195-235): R = 10 / R = 20
+    speedups, geomean and next best per workload, aligned like print_table
+    (gpumux.cpp:153-171).  Default workloads: the Table-1 presets present."""
+    names = sorted({r["workload"] for r in rows}) if workloads is None else list(workloads)
+    if workloads is None:
+        names = [w for w in names if w in ("resnet18-conv2_2", "rnn-matvec", "square-256")]
+    tables = [speedup_table(rows, w) for w in names]
+    table = [["row"] + names]
+    present = {x["R"] for t in tables for x in t["rows"]}
+    for spot in (10, 20):
+        if spot not in present:
+            continue
+        row = ["R = %d" % spot]
+        for t in tables:
+            cell = "-"
+            for x in t["rows"]:
+                if x["R"] == spot:
+                    cell = "%.2fx" % x["speedup"]
+            row.append(cell)
+        table.append(row)
+    table.append(["geomean"] + ["%.2fx" % t["geomean_speedup"] for t in tables])
+    table.append(["next best"] + [t["next_best"] for t in tables])
+    widths = [max(len(r[i]) for r in table) for i in range(len(table[0]))]
+    lines = []
+    for r in table:
+        lines.append("".join(c + (" " * (widths[i] - len(c) + 2) if i + 1 < len(r) else "") for i, c in enumerate(r)))
+    return "\n".join(lines) + "\n"
+
+
+if __name__ == "__main__":  # python -m paper_1901_00041_b200.report table1 <runs.csv>
+    import sys
+    if len(sys.argv) != 3 or sys.argv[1] != "table1":
+        raise SystemExit("usage: python -m paper_1901_00041_b200.report table1 <runs.csv>")
+    sys.stdout.write(table1_report(read_csv(sys.argv[2])))

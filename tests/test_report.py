@@ -4,6 +4,8 @@ import json
 import os
 import re
 
+import pytest
+
 from refshim import ROOT
 
 from paper_1901_00041_b200 import report
@@ -43,3 +45,33 @@ def test_bench_rows_cover_every_table1_preset():
     assert len(rows) == 3 * 4
     assert {r.split(",")[1] for r in rows} == {"resnet18-conv2_2", "rnn-matvec", "square-256"}
 
+
+
+def test_table1_report_matches_bench_geomeans():
+    """report --kind table1 (gpumux.cpp:195-235) over a committed CSV of a
+    real run: the speedup_table geomeans equal the bench line's."""
+    csv = os.path.join(ROOT, "profiles", "r01i_runs.csv")
+    line = json.loads(open(os.path.join(ROOT, "profiles", "r01i_bench_line.json")).read())
+    rows = report.read_csv(csv)
+    t = report.speedup_table(rows, "resnet18-conv2_2")
+    assert t["geomean_speedup"] == pytest.approx(line["table1"]["geomean_over_space_only"], rel=1e-6)
+    assert [x["R"] for x in t["rows"]] == [r["R"] for r in line["table1"]["rows"]]
+    for name, suite in line["table1"]["other_presets"].items():
+        assert report.speedup_table(rows, name)["geomean_speedup"] == pytest.approx(
+            suite["geomean_over_space_only"], rel=1e-6)
+    text = report.table1_report(rows)
+    lines = text.splitlines()
+    assert lines[0].split() == ["row", "resnet18-conv2_2", "rnn-matvec", "square-256"]
+    assert lines[1].startswith("R = 10") and lines[3].startswith("geomean") and lines[4].startswith("next best")
+
+
+def test_speedup_table_semantics():
+    def row(w, p, r, g):
+        return {"workload": w, "policy": p, "replicas": str(r), "status": "ok", "throughput_gflops": str(g)}
+    rows = [row("w", "space-time", 2, 10), row("w", "time-mux", 2, 5), row("w", "space-implicit", 2, 4),
+            row("w", "space-time", 4, 12), row("w", "time-mux", 4, 3), row("w", "space-implicit", 4, 6)]
+    t = report.speedup_table(rows, "w")
+    assert [x["speedup"] for x in t["rows"]] == [2.0, 2.0]
+    assert t["next_best"] == "time-mux"  # one win each: the earlier PolicyKind
+    with pytest.raises(ValueError, match="missing cell"):
+        report.speedup_table(rows[:5], "w")
