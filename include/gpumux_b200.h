@@ -485,6 +485,24 @@ typedef struct gm_serve_stats {
 int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, const gm_serve_config* cfg,
              gm_serve_stats* out, double* latencies_ms, size_t cap, size_t* n_lat);
 
+/* One dispatch of the last gm_serve on this ctx: the real-clock counterpart
+ * of the reference's DispatchEvent / NDJSON trace line (sim.hpp Trace,
+ * gpumux.cpp:64-79).  Times are from the serving clock's start. */
+typedef struct gm_dispatch_event {
+  int64_t start_ns;   /* host dispatch */
+  int64_t end_ns;     /* host-observed completion (CUDA event) */
+  double device_ms;   /* round-program device time (CUDA events) */
+  double flops;       /* the dispatched queries' FLOPs */
+  int32_t queries;    /* member queries */
+  int32_t tenants;    /* distinct tenants in the round */
+  int32_t launches;   /* 1: one round-program launch */
+  int32_t tiles;      /* tile-table entries executed */
+} gm_dispatch_event;
+
+/* Copies the last gm_serve's dispatch events (n = count; out == NULL queries
+ * the count only).  GM_EINVAL when cap < count. */
+int gm_serve_trace(gm_ctx* ctx, gm_dispatch_event* out, size_t cap, size_t* n);
+
 #ifdef __cplusplus
 }  /* extern "C" */
 #endif

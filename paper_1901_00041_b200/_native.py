@@ -128,6 +128,11 @@ class gm_serve_stats(C.Structure):
                 ("evicted", C.c_int32), ("reserved0", C.c_int32), ("evicted_mask", C.c_uint64)]
 
 
+class gm_dispatch_event(C.Structure):
+    _fields_ = [("start_ns", C.c_int64), ("end_ns", C.c_int64), ("device_ms", C.c_double), ("flops", C.c_double),
+                ("queries", C.c_int32), ("tenants", C.c_int32), ("launches", C.c_int32), ("tiles", C.c_int32)]
+
+
 _SIGS = {
     "gm_last_error": (C.c_char_p, []),
     "gm_abi_version": (C.c_int, []),
@@ -221,6 +226,7 @@ _SIGS = {
     "gm_ctx_launch_stats": (C.c_int, [C.c_void_p, P(C.c_int64), P(C.c_int64), P(C.c_int64)]),
     "gm_serve": (C.c_int, [C.c_void_p, P(gm_serve_tenant), C.c_size_t, P(gm_serve_config), P(gm_serve_stats),
                            P(C.c_double), C.c_size_t, P(C.c_size_t)]),
+    "gm_serve_trace": (C.c_int, [C.c_void_p, P(gm_dispatch_event), C.c_size_t, P(C.c_size_t)]),
 }
 
 _lib = None

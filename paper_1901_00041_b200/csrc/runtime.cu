@@ -123,6 +123,7 @@ struct Prepared {
 };
 
 struct Runtime {
+  std::vector<gm_dispatch_event> serve_trace;  // the last gm_serve's dispatches (gm_serve_trace)
   int device = -1;
   int sms = 0;
   int driver_version = 0;
@@ -1506,6 +1507,16 @@ int gm_graph_capture_round_e2e(gm_ctx* ctx, const gm_plans* p, size_t n, const i
   GM_API_END
 }
 
+int gm_serve_trace(gm_ctx* ctx, gm_dispatch_event* out, size_t cap, size_t* n) {
+  GM_API_BEGIN
+  Runtime& rt = runtime_of(ctx);
+  if (n) *n = rt.serve_trace.size();
+  if (!out) return GM_OK;
+  if (cap < rt.serve_trace.size()) throw RangeError("output buffer too small");
+  std::copy(rt.serve_trace.begin(), rt.serve_trace.end(), out);
+  GM_API_END
+}
+
 int gm_graph_launch(gm_graph* g, uint64_t stream) {
   GM_API_BEGIN
   if (!g) throw std::invalid_argument("null graph");
@@ -1577,6 +1588,8 @@ struct ServeRound {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<std::pair<int, std::vector<int64_t>>> members;  // (logical tenant, arrival ns of its queries)
   int64_t dispatch_ns = 0;
+  double flops = 0;  // the members' queries' FLOPs (served work)
+  int32_t tiles = 0;
 };
 
 int64_t since(std::chrono::steady_clock::time_point t0) {
@@ -1711,6 +1724,7 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
     return e;
   };
   std::deque<ServeRound> inflight;
+  std::vector<gm_dispatch_event> trace;
   std::vector<double> lat_ms;
   int64_t queries = 0, rounds = 0, dispatched_queries = 0, slo_miss = 0, flops_done = 0;
   double round_ms_sum = 0;
@@ -1748,6 +1762,18 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
       pool.push_back(r.ev0);
       pool.push_back(r.ev1);
       round_ms_sum += ms;
+      {
+        gm_dispatch_event ev{};
+        ev.start_ns = r.dispatch_ns;
+        ev.end_ns = done;
+        ev.device_ms = ms;
+        ev.flops = r.flops;
+        for (auto& m : r.members) ev.queries += static_cast<int32_t>(m.second.size());
+        ev.tenants = static_cast<int32_t>(r.members.size());
+        ev.launches = 1;
+        ev.tiles = r.tiles;
+        trace.push_back(ev);
+      }
       predicted_s = rounds == 1 && predicted_s == 0 ? ms * 1e-3 : 0.8 * predicted_s + 0.2 * ms * 1e-3;
       for (auto& [ti, arr] : r.members) {
         T& t = ts[ti];
@@ -1820,6 +1846,7 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
           std::vector<int64_t> arr(t.pending.begin(), t.pending.begin() + q);
           t.pending.erase(t.pending.begin(), t.pending.begin() + q);
           dispatched_queries += q;
+          r.flops += static_cast<double>(q) * static_cast<double>(t.flops);
           r.members.emplace_back(static_cast<int>(i), std::move(arr));
         }
         auto it = cache.find(key);
@@ -1833,6 +1860,7 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
         r.ev0 = get_event();
         r.ev1 = get_event();
         r.dispatch_ns = now;
+        r.tiles = it->second.prep->n_tiles;
         cuda_check(cudaEventRecord(r.ev0, stream), "cudaEventRecord");
         rt.launch(*it->second.prep, stream);
         cuda_check(cudaEventRecord(r.ev1, stream), "cudaEventRecord");
@@ -1846,6 +1874,7 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
   }
   cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
   for (cudaEvent_t e : pool) cudaEventDestroy(e);
+  rt.serve_trace = std::move(trace);
 
   std::memset(out, 0, sizeof(*out));
   out->queries = queries;

@@ -336,6 +336,10 @@ class ServeTenant:
 class ServeResult:
     stats: Dict[str, float]
     latencies_ms: List[float] = field(default_factory=list)
+    # one dict per dispatch (gm_serve_trace): start_ns, end_ns, device_ms,
+    # flops, queries, tenants, launches, tiles; report.write_trace_ndjson
+    # renders them as the reference's NDJSON trace lines
+    dispatches: List[Dict[str, float]] = field(default_factory=list)
 
 
 def _variant(buf: LayerBuffers, max_batch: int, b: int) -> LayerBuffers:
@@ -409,4 +413,9 @@ class ServingEngine:
         nl = C.c_size_t()
         check(lib().gm_serve(self.ctx.handle, arr, n, C.byref(cfg), C.byref(out), lat, cap, C.byref(nl)))
         stats = {f: getattr(out, f) for f, _ in N.gm_serve_stats._fields_ if not f.startswith("reserved")}
-        return ServeResult(stats, [lat[i] for i in range(min(nl.value, cap))])
+        ne = C.c_size_t()
+        check(lib().gm_serve_trace(self.ctx.handle, None, 0, C.byref(ne)))
+        evs = (N.gm_dispatch_event * max(1, ne.value))()
+        check(lib().gm_serve_trace(self.ctx.handle, evs, ne.value, C.byref(ne)))
+        dispatches = [{f: getattr(evs[i], f) for f, _ in N.gm_dispatch_event._fields_} for i in range(ne.value)]
+        return ServeResult(stats, [lat[i] for i in range(min(nl.value, cap))], dispatches)

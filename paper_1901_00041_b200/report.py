@@ -168,6 +168,30 @@ def table1_report(rows: List[Dict[str, str]], workloads: Optional[Iterable[str]]
     return "\n".join(lines) + "\n"
 
 
+def trace_ndjson_lines(dispatches: Iterable[Dict[str, float]]) -> List[str]:
+    """The reference's NDJSON trace (gpumux.cpp:64-79: one JSON object per
+    dispatch event, keys start_ns, end_ns, policy, launches, flops, members)
+    for real-clock serving dispatches (ServeResult.dispatches).  ``members``
+    is the number of queries served; device_ms, tenants and tiles are
+    measured extras; the modelled occupancy / context_switches are not
+    emitted."""
+    import json
+    out = []
+    for d in dispatches:
+        out.append(json.dumps({"start_ns": int(d["start_ns"]), "end_ns": int(d["end_ns"]), "policy": "space-time",
+                               "launches": int(d["launches"]), "flops": float(d["flops"]),
+                               "members": int(d["queries"]), "tenants": int(d["tenants"]),
+                               "device_ms": float(d["device_ms"]), "tiles": int(d["tiles"])},
+                              separators=(",", ":")))
+    return out
+
+
+def write_trace_ndjson(path: str, dispatches: Iterable[Dict[str, float]]) -> None:
+    with open(path, "w") as f:
+        for ln in trace_ndjson_lines(dispatches):
+            f.write(ln + "\n")
+
+
 if __name__ == "__main__":  # python -m paper_1901_00041_b200.report table1 <runs.csv>
     import sys
     if len(sys.argv) != 3 or sys.argv[1] != "table1":

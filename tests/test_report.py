@@ -75,3 +75,12 @@ def test_speedup_table_semantics():
     assert t["next_best"] == "time-mux"  # one win each: the earlier PolicyKind
     with pytest.raises(ValueError, match="missing cell"):
         report.speedup_table(rows[:5], "w")
+
+
+def test_trace_ndjson_lines():
+    d = {"start_ns": 10, "end_ns": 700010, "device_ms": 0.66, "flops": 2.6e11, "queries": 32, "tenants": 4,
+         "launches": 1, "tiles": 14224}
+    (ln,) = report.trace_ndjson_lines([d])
+    obj = json.loads(ln)
+    assert obj["policy"] == "space-time" and obj["members"] == 32 and obj["start_ns"] == 10
+    assert set(obj) >= {"start_ns", "end_ns", "policy", "launches", "flops", "members"}

@@ -35,6 +35,13 @@ def test_closed_loop_accounting():
     assert s["plan_misses"] <= 16 and s["plan_hits"] > s["plan_misses"]
     flops = sum(eng.flops_per_query(i) for i in range(3)) / 3
     assert s["tflops"] == pytest.approx(s["queries"] * flops / s["window_s"] / 1e12, rel=1e-6)
+    # the dispatch trace (gm_serve_trace): one event per round, in dispatch order
+    ev = r.dispatches
+    assert len(ev) == s["rounds"]
+    assert all(e["launches"] == 1 and e["tiles"] > 0 and 1 <= e["tenants"] <= 3 for e in ev)
+    assert all(0 < e["device_ms"] and e["start_ns"] < e["end_ns"] for e in ev)
+    assert [e["start_ns"] for e in ev] == sorted(e["start_ns"] for e in ev)
+    assert sum(e["queries"] for e in ev) == s["dispatched_queries"]
 
 
 def test_poisson_low_rate_dispatches_singletons_after_max_wait():
