@@ -907,6 +907,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       for (;;) {
         const int t = claim();
+        if (t >= 0) {  // pull the claimed tile's entry and member descriptor toward the SM
+          const char* p0 = reinterpret_cast<const char*>(slots + tiles[t].member);
+#pragma unroll
+          for (int i = 0; i < static_cast<int>(sizeof(MemberDesc)); i += 128)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(p0 + i));
+        }
         mbar_wait(&sq_empty[sslot], sphase ^ 1);
         sq[sslot] = t;
         mbar_arrive(&sq_full[sslot]);
