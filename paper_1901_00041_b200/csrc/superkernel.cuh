@@ -912,6 +912,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < static_cast<int>(sizeof(MemberDesc)); i += 128)
             asm volatile("prefetch.global.L1 [%0];" ::"l"(p0 + i));
+          prefetch_tmap(&reinterpret_cast<const MemberDesc*>(p0)->c);  // the epilogue's store map
         }
         mbar_wait(&sq_empty[sslot], sphase ^ 1);
         sq[sslot] = t;
