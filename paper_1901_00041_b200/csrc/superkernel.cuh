@@ -686,14 +686,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           kb = kb_lo + pre;
         } else if (te.dep >= 0) {
-          wait_free();
-          mbar_expect_tx(&full[stage], tx);
-          load_b(kb_lo, stage);
+          // weights do not wait on the dependency: stream B into the next
+          // stages (up to the ring depth, as slots free up), then gate, then
+          // the activations into the same stages
+          const int pre = min(k_blocks - kb_lo, static_cast<int>(nslots) - 1);
+          uint32_t st = stage;
+          for (int j = 0; j < pre; ++j) {
+            mbar_wait(&empty[st], ((ubits >> st) & 1u) ^ 1u);
+            mbar_expect_tx(&full[st], tx);
+            load_b(kb_lo + j, st);
+            st = st + 1 == nslots ? 0 : st + 1;
+          }
           gate();
           if (trace) trace[6 * t + 1] = globaltimer();
-          load_a(kb_lo, stage);
-          advance();
-          kb = kb_lo + 1;
+          for (int j = 0; j < pre; ++j) {
+            load_a(kb_lo + j, stage);
+            advance();
+          }
+          kb = kb_lo + pre;
         } else if (trace) {
           trace[6 * t + 1] = globaltimer();  // no gate
         }
