@@ -189,50 +189,31 @@ def time_graph(torch, graph, stream, steps, flush=None, isolate=False):
     return per, t0.elapsed_time(t1)
 
 
-class CpuPort:
-    """The numpy fp32 port (oracle/cpu_conv.py) over one tenant's operators."""
+def graph_name(args):
+    return f"{args.model}_{args.image}"
 
-    def __init__(self, layers, batch, seed=42):
-        import numpy as np
-        sys.path.insert(0, os.path.join(HERE, "oracle"))
-        import cpu_conv  # test infra: CPU baseline / reference arm only
-        self.cpu_conv = cpu_conv
-        rng = np.random.default_rng(seed)
-        self.tensors = []
-        for L in layers:
-            s = L.gemm_shape(batch)
-            if L.kind == "dwconv":
-                c = L.conv
-                x = rng.uniform(-1, 1, (batch, c.image_h, c.image_w, c.in_channels)).astype(np.float32)
-                w = rng.uniform(-1, 1, (c.out_channels, c.kernel_h, c.kernel_w)).astype(np.float32)
-            elif L.kind == "conv":
-                c = L.conv
-                x = rng.uniform(-1, 1, (batch, c.image_h, c.image_w, c.in_channels)).astype(np.float32)
-                w = rng.uniform(-1, 1, (c.out_channels, c.kernel_h, c.kernel_w, c.in_channels)).astype(np.float32)
-            else:
-                x = rng.uniform(-1, 1, (s.m, s.k)).astype(np.float32)
-                w = rng.uniform(-1, 1, (s.n, s.k)).astype(np.float32)
-            self.tensors.append((L, x, w))
-        self.flops_pass = sum(L.flops(batch) for L in layers)
-        self.cores = cpu_conv.threads()
 
-    def run_pass(self):
-        for L, x, w in self.tensors:
-            if L.kind == "dwconv":
-                self.cpu_conv.dwconv2d_nhwc(x, w, L.conv.stride, L.conv.padding)
-            elif L.kind == "conv":
-                self.cpu_conv.conv2d_nhwc(x, w, L.conv.stride, L.conv.padding)
-            else:
-                self.cpu_conv.gemm_nt(x, w)
+def load_graph(args):
+    """The tenant graph as plain data (oracle/graphs/*.json, exported from the
+    product's workload builders and pinned to them by tests/test_workload.py):
+    the reference arm and the CPU baseline read it without importing the
+    product package."""
+    sys.path.insert(0, os.path.join(HERE, "oracle"))
+    import cpu_conv  # test infra: CPU baseline / reference arm only
+    return cpu_conv.load_graph(graph_name(args))
 
-    def sample(self, seconds):
-        done, t0 = 0, time.perf_counter()
-        while True:
-            self.run_pass()
-            done += 1
-            el = time.perf_counter() - t0
-            if el >= seconds:
-                return done * self.flops_pass / el / 1e12, done, el
+
+def workload_desc(args, graph):
+    """config.workload, identical in both arms (same_config)."""
+    convs = sum(L["kind"] == "conv" for L in graph)
+    return (f"{args.tenants} tenants/GPU x {args.model}@{args.image} dataflow graph ({len(graph)} ops: {convs} convs, "
+            f"pools, residual adds, fc), batch {args.batch} per tenant query (BASELINE configs[1])")
+
+
+def cpu_graph(args, graph):
+    sys.path.insert(0, os.path.join(HERE, "oracle"))
+    import cpu_conv  # test infra: CPU baseline / reference arm only
+    return cpu_conv.CpuGraph(graph, args.batch), cpu_conv.threads()
 
 
 # ------------------------------------------------------------------ reference arm
@@ -242,49 +223,61 @@ def run_reference(args):
     The reference artifact computes no tensors (it is a roofline simulator),
     so its CPU implementation of the path is: the reference planner
     (oracle/_ref/libgpumux_ref.so, the unmodified gpumux_core) forming the
-    round's super-kernels, plus the fp32 CPU port of the members' conv/GEMM
-    math (oracle/cpu_conv.py) on all host threads.  Each step is a bounded
-    sample: one tenant's full pass at the configured batch, cycling tenants.
+    round's super-kernels over the tenant graph's GEMM shapes (the reference's
+    own im2col lowering, gemm.hpp:44-56), plus the fp32 CPU port of the
+    members' math (oracle/cpu_conv.py CpuGraph: the same dataflow graph) on all
+    host threads.  Each step is a bounded sample: one tenant's full pass at the
+    configured batch.  Nothing here imports the product package.
     """
     import ctypes
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    layers = model_layers(args.model, args.image)
-    flops_pass = sum(L.flops(args.batch) for L in layers)
+    graph = load_graph(args)
     ref_path = os.path.join(HERE, "oracle", "_ref", "libgpumux_ref.so")
     planner_ok = os.path.exists(ref_path)
     if planner_ok:
         ref = ctypes.CDLL(ref_path)
         ref.gm_ref_call.restype = ctypes.c_char_p
         ref.gm_ref_call.argtypes = [ctypes.c_char_p]
-        shapes = [list(L.gemm_shape(args.batch).__dict__.values()) for L in layers]
-    port = CpuPort(layers, args.batch)
-    cores = port.cores
+
+        def call(req):
+            return json.loads(ref.gm_ref_call(json.dumps(req).encode()))
+
+        shapes = []
+        for L in graph:
+            if L["kind"] == "gemm":
+                shapes.append([L["rows"] * args.batch, L["n"], L["k"]])
+                continue
+            H, W_, R, S, Cin, Cout, st, pad = L["conv"]
+            m, n, k = call({"op": "im2col", "conv": [H, W_, R, S, Cin, Cout, st, pad]})["shape"]
+            if L["kind"] != "conv":
+                k = R * S  # per-channel ops: the reference's K = R*S model (workload.cpp:66)
+            shapes.append([m * args.batch, n, k])  # batch_inputs (gemm.hpp:54-56)
+    port, cores = cpu_graph(args, graph)
     steps = []
     total = args.warmup + args.steps
     for i in range(total):
         t0 = time.perf_counter()
         if planner_ok:  # one round of the reference planner over the configured tenants
-            req = {"op": "run_space_time", "tenants": args.tenants * args.gpus, "layers": shapes,
-                   "duration": 1e-3, "microbench": False, "scheduler": {"target_batch": 0}}
-            ref.gm_ref_call(json.dumps(req).encode())
+            call({"op": "run_space_time", "tenants": args.tenants * args.gpus, "layers": shapes,
+                  "duration": 1e-3, "microbench": False, "scheduler": {"target_batch": 0}})
         port.run_pass()
         if i >= args.warmup:
             steps.append(time.perf_counter() - t0)
     mean_s = sum(steps) / len(steps)
-    value = flops_pass / mean_s / 1e12
+    value = port.flops_pass / mean_s / 1e12
     kind = "reference" if planner_ok else "port"
     line = {
         "impl": "reference", "metric": "packed multi-tenant conv TFLOP/s vs time-/space-only; p99 query latency",
         "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": mean_s * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.tenants} tenants x {args.model}@{args.image} conv layers + fc, batch "
-                               f"{args.batch} (configs[1]); CPU sample per step: 1 tenant pass"},
+        "config": {"workload": workload_desc(args, graph)},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": kind,
                          "sample": f"one {args.model}@{args.image} b{args.batch} tenant pass per step "
-                                   f"({flops_pass / 1e9:.1f} GFLOP) + reference planner round"},
+                                   f"({port.flops_pass / 1e9:.1f} GFLOP, numpy fp32 dataflow graph) + reference "
+                                   f"planner round (oracle/_ref run_space_time)"},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -331,6 +324,7 @@ def run_ours(args):
     # headline: the round program (all of the round's super-kernels in one
     # persistent launch, per-tenant layer dependencies on device)
     g_packed = eng.capture_round(rnd)
+    tile_info = rnd.tile_info()
     # the reference's literal dispatch unit: one launch per formed super-kernel
     g_parity = eng.capture_packed(rnd)
     g_timed = eng.capture_round(rnd, timed=True)  # event pair around the round kernel
@@ -444,13 +438,13 @@ def run_ours(args):
     attain_s = sum(max(L.flops(args.batch) / (burst * 1e12), L.compulsory_bytes(args.batch) / (hbm * 1e9))
                    for L in layers) * T
     cpu = None
+    graph = load_graph(args)
     if world == 1:
-        port = CpuPort(layers, args.batch)
+        port, cores = cpu_graph(args, graph)
         cpu_tf, reps_cpu, el = port.sample(args.cpu_seconds)
-        cores = port.cores
         cpu = {"value": cpu_tf, "unit": "TFLOP/s", "cores": cores, "kind": "port",
                "sample": f"{reps_cpu} x one {args.model}@{args.image} b{args.batch} tenant pass "
-                         f"(numpy fp32 im2col+BLAS, oracle/cpu_conv.py), {el:.1f} s"}
+                         f"(numpy fp32 dataflow graph, im2col+BLAS, oracle/cpu_conv.py), {el:.1f} s"}
     line = {
         "metric": "packed multi-tenant conv TFLOP/s vs time-/space-only; p99 query latency",
         "value": value,
@@ -465,14 +459,18 @@ def run_ours(args):
         "dtype": "bf16",
         "data": "synthetic (U(-1,1) inputs, Kaiming-normal weights, seed 42)",
         "config": {
-            "workload": f"{T} tenants/GPU x {args.model}@{args.image} ({len(layers)} ops: convs + fc), "
-                        f"batch {args.batch} per tenant query (BASELINE configs[1])",
+            "workload": workload_desc(args, graph),
             "tenants_per_gpu": T, "batch": args.batch, "placement": "tenant-sharded, no collective",
             "planner": f"space-time form_batches (max_waves={args.max_waves}; 1 = reference plan parity); "
                        f"packed = round program (1 persistent launch/round), modes.packed_per_plan = 1 launch "
                        f"per formed super-kernel",
-            "superkernels_per_round": len(rnd.kernels), "tiles_per_round": sum(k.planned_cost.blocks
-                                                                             for k in rnd.kernels),
+            "superkernels_per_round": len(rnd.kernels),
+            "planner_tiles_per_round": sum(k.planned_cost.blocks for k in rnd.kernels),
+            "tiles_executed_per_round": len(tile_info),
+            "executed_tile_variants": {"tall_256_rows": sum(t["rows"] == 256 for t in tile_info),
+                                       "narrow_n": sum(t["cols"] < 256 and t["rows"] != 32 for t in tile_info),
+                                       "split_k": sum(t["splits"] > 1 for t in tile_info),
+                                       "cuda_core": sum(t["rows"] == 32 for t in tile_info)},
             "l2": f"inputs larger than L2 ({bytes_round / 1e6:.0f} MB compulsory/round)",
         },
         "modes": {
@@ -491,9 +489,10 @@ def run_ours(args):
             "peak_source": f"{peak_src} HBM copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
             "kernel": "gmb::dev::superkernel<256> (round program)", "launches_per_round": 1,
             "avg_launch_us": round_s * 1e6, "timing": f"CUDA events around the round kernel, {len(round_ms)} replays",
-            "tensor_view": {"achieved_tflops": achieved, "peak_tflops": sustained,
-                            "frac_of_dense_bf16": achieved / sustained,
-                            "peak_source": f"{peak_src} bf16 sustained (MEASURED_PEAKS.json)"},
+            "tensor_view": {"achieved_tflops": achieved, "peak_tflops": burst,
+                            "frac_of_dense_bf16": achieved / burst,
+                            "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json bf16_tflops; the round "
+                                           f"kernel is timed alone)"},
             "attainable_tflops": flops_round / attain_s / 1e12 if attain_s else None,
             "frac_of_attainable": achieved / (flops_round / attain_s / 1e12) if attain_s else None,
             "attainable_note": "per-layer max(F/P_burst, B/BW) summed over the round",

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define GM_ABI_VERSION 1
+#define GM_ABI_VERSION 2
 
 enum gm_status {
   GM_OK = 0,
@@ -275,12 +275,39 @@ int gm_sim_trace_evictions(const gm_sim_trace* t, int32_t* tenants, int64_t* tim
 int gm_sim_trace_flops(const gm_sim_trace* t, int64_t* dispatched, int64_t* completed);
 void gm_sim_trace_destroy(gm_sim_trace* t);
 
+/* One closed-loop space-time round on the virtual clock, host only (no GPU):
+ * every listed tenant submits one forward pass at `start` and the
+ * run_space_time loop (proj/src/sim.cpp:452-576: dispatch FIFO, formation only
+ * when the FIFO is empty, completion fan-out of the next layer, wake timer)
+ * runs until every pass has completed.  This is the planner behind
+ * gm_plan_round (which reads the layer lists from registered tenants); for a
+ * homogeneous tenant set its dispatches equal the reference engine's first-pass
+ * dispatches (tests/test_round_parity.py).  `cache` (nullable) and `next_id`
+ * (nullable, in/out) persist across rounds like a gm_ctx's. */
+typedef struct gm_round_tenant {
+  int32_t tenant;
+  int32_t reserved;
+  const gm_gemm_shape* layers;
+  size_t n_layers;
+  int64_t slo_ns;                   /* pass deadline = start + slo_ns */
+} gm_round_tenant;
+int gm_plan_round_shapes(const gm_round_tenant* tenants, size_t n, int64_t start, const gm_batch_policy* p,
+                         const gm_device_spec* d, gm_cache* cache, uint64_t* next_id, gm_plans** out);
+
 /* ---- B200 runtime: tenants, super-kernel dispatch ------------------------ */
 
 /* DWCONV: depthwise conv (groups = channels; MobileNet-v2).  The planner sees
  * the reference's model of it, a K = R*S GEMM (proj/src/workload.cpp:66):
  * (b*P*Q, C, R*S); w is [C, ldw] with R*S taps per row; R*S <= 9, C % 4 == 0. */
-enum gm_layer_kind { GM_LAYER_GEMM = 0, GM_LAYER_CONV = 1, GM_LAYER_DWCONV = 2 };
+enum gm_layer_kind { GM_LAYER_GEMM = 0, GM_LAYER_CONV = 1, GM_LAYER_DWCONV = 2, GM_LAYER_MAXPOOL = 3,
+                     GM_LAYER_AVGPOOL = 4 };
+/* MAXPOOL / AVGPOOL: conv = the window (kernel_h/w, stride, padding; in ==
+ * out channels), w unused (may be null); planned like a depthwise conv, a
+ * K = R*S GEMM; executed as CUDA-core tiles of the same persistent launch.
+ * Pool FLOPs are not tensor work and are not counted by the benchmarks. */
+
+/* Fused epilogue activations (after the residual add). */
+enum gm_activation { GM_ACT_NONE = 0, GM_ACT_RELU = 1, GM_ACT_RELU6 = 2, GM_ACT_GELU = 3 };
 
 /* One operator of a tenant's graph, with its device buffers (bf16).
  *   CONV: x = NHWC [batch, H, W, Cin]; w = KRSC [Cout, R, S, Cin] with a row
@@ -298,7 +325,19 @@ typedef struct gm_layer_desc {
   void* y;
   int64_t ldx;                      /* 0 = dense */
   int64_t ldw;                      /* 0 = dense */
-  int32_t relu;                     /* fuse max(0, .) into the epilogue */
+  int32_t act;                      /* gm_activation fused into the epilogue */
+  /* Dataflow: the layer of this tenant whose output y is this layer's x
+   * (-1 = an external input, e.g. the tenant's query batch).  x must then
+   * point into that layer's y.  In a round program the layer runs after its
+   * source by the tenant's dependency chain (a tenant's layers run in order,
+   * proj/src/sim.cpp:482-488). */
+  int32_t src;
+  /* Fused residual add: y = act(x * W + res), res [M, N] bf16 row-major with
+   * row stride ldr (0 = N; 16-byte aligned rows), null = none.  res_src: the
+   * earlier layer of this tenant whose y it is (-1 = external). */
+  const void* res;
+  int64_t ldr;
+  int32_t res_src;
   int32_t reserved0;
 } gm_layer_desc;
 
@@ -409,6 +448,21 @@ int gm_graph_capture_round(gm_ctx* ctx, const gm_plans* p, int timed, gm_graph**
  * (member = registered slot, flags = plan index). */
 int gm_trace_round(gm_ctx* ctx, const gm_plans* p, uint64_t stream, uint64_t* out, size_t cap, size_t* n_tiles);
 int gm_round_tiles(gm_ctx* ctx, const gm_plans* p, gm_tile* out, size_t cap, size_t* n);
+/* The executed tile table of a round program, one entry per tile in launch
+ * order: which operator, which output tile, the tile variant the runtime
+ * chose (tall 256-row, N width, split-K slice) and its device-side
+ * dependency edge (done = counter it publishes to, dep = counter it waits on,
+ * -1 = none).  Differs from gm_build_tile_table (the planner's tile count,
+ * thread_blocks under the b200 profile) by those variants. */
+typedef struct gm_round_tile {
+  int32_t tenant, layer;
+  int32_t m_tile, n_tile;
+  int32_t rows, cols;               /* output rows per tile (128 / 256 / 32) and N width */
+  int32_t splits, kb_begin, kb_end; /* split-K slice (splits 1: the whole K, kb_end 0) */
+  int32_t done, dep;
+  int32_t plan;                     /* index of the formed super-kernel it came from */
+} gm_round_tile;
+int gm_round_tile_info(gm_ctx* ctx, const gm_plans* p, gm_round_tile* out, size_t cap, size_t* n);
 /* End-to-end round program (the serving call with host buffers): per tenant
  * i, an H2D copy h_in[i] -> d_in[i] (its query batch) and its layer-0
  * pre-pass run on a copy branch that then opens the tenant's input gate; the

@@ -136,3 +136,138 @@ void oracle_dwconv2d_nhwc(const float* x, const float* w, float* y, int64_t batc
     }
   }
 }
+
+/* ---------------------------------------------------------------------------
+ * Dataflow operators (a tenant graph where each layer reads an earlier
+ * layer's output): fused residual add and activation, pooling, and row
+ * sampling for the large configurations.
+ *
+ *   y[m, o] = act(sum(...) + res[m * ldr + o])   (res == NULL: no add)
+ *   act: 0 none, 1 relu, 2 relu6 (MobileNet-v2), 3 gelu (erf form, BERT FFN)
+ *   rows: the output rows m to compute (y then holds n_rows rows, in order);
+ *         rows == NULL computes every row (y holds all M rows).
+ * The residual add and activation are the torchvision block semantics
+ * (ResNet: relu(conv3(x) + identity/downsample); MobileNet-v2: project(x) + x);
+ * pooling is torch.nn.MaxPool2d (padded taps ignored) / AvgPool2d (global, no
+ * padding).  The reference models none of these (it has no tensors). */
+
+static float oracle_act(double v, int32_t act) {
+  if (act == 1) return v < 0.0 ? 0.0f : (float)v;
+  if (act == 2) return v < 0.0 ? 0.0f : (v > 6.0 ? 6.0f : (float)v);
+  if (act == 3) return (float)(0.5 * v * (1.0 + erf(v * 0.70710678118654752440)));
+  return (float)v;
+}
+
+void oracle_conv2d_ex(const float* x, const float* w, const float* res, int64_t ldr, float* y, const int64_t* rows,
+                      int64_t n_rows, int64_t batch, int64_t H, int64_t W, int64_t Cin, int64_t Cout, int64_t R,
+                      int64_t S, int64_t stride, int64_t pad, int64_t ldw, int32_t act) {
+  const int64_t P = (H + 2 * pad - R) / stride + 1;
+  const int64_t Q = (W + 2 * pad - S) / stride + 1;
+  const int64_t M = batch * P * Q;
+  if (ldw <= 0) ldw = R * S * Cin;
+  if (ldr <= 0) ldr = Cout;
+  const int64_t n = rows ? n_rows : M;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t m = rows ? rows[i] : i;
+    const int64_t b = m / (P * Q), p = (m / Q) % P, q = m % Q;
+    float* out = y + i * Cout;
+    for (int64_t o = 0; o < Cout; ++o) {
+      double acc = 0.0;
+      const float* wo = w + o * ldw;
+      for (int64_t r = 0; r < R; ++r) {
+        const int64_t ih = p * stride - pad + r;
+        if (ih < 0 || ih >= H) continue;
+        for (int64_t s = 0; s < S; ++s) {
+          const int64_t iw = q * stride - pad + s;
+          if (iw < 0 || iw >= W) continue;
+          const float* xi = x + ((b * H + ih) * W + iw) * Cin;
+          const float* wi = wo + (r * S + s) * Cin;
+          for (int64_t c = 0; c < Cin; ++c) acc += (double)xi[c] * (double)wi[c];
+        }
+      }
+      if (res) acc += (double)res[m * ldr + o];
+      out[o] = oracle_act(acc, act);
+    }
+  }
+}
+
+void oracle_gemm_ex(const float* a, const float* b, const float* res, int64_t ldr, float* c, const int64_t* rows,
+                    int64_t n_rows, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int32_t act) {
+  if (lda <= 0) lda = K;
+  if (ldb <= 0) ldb = K;
+  if (ldr <= 0) ldr = N;
+  const int64_t n = rows ? n_rows : M;
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t m = rows ? rows[i] : i;
+    const float* am = a + m * lda;
+    for (int64_t j = 0; j < N; ++j) {
+      double acc = 0.0;
+      const float* bn = b + j * ldb;
+      for (int64_t k = 0; k < K; ++k) acc += (double)am[k] * (double)bn[k];
+      if (res) acc += (double)res[m * ldr + j];
+      c[i * N + j] = oracle_act(acc, act);
+    }
+  }
+}
+
+void oracle_dwconv2d_ex(const float* x, const float* w, float* y, const int64_t* rows, int64_t n_rows, int64_t batch,
+                        int64_t H, int64_t W, int64_t C, int64_t R, int64_t S, int64_t stride, int64_t pad,
+                        int64_t ldw, int32_t act) {
+  const int64_t P = (H + 2 * pad - R) / stride + 1;
+  const int64_t Q = (W + 2 * pad - S) / stride + 1;
+  const int64_t M = batch * P * Q;
+  if (ldw <= 0) ldw = R * S;
+  const int64_t n = rows ? n_rows : M;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t m = rows ? rows[i] : i;
+    const int64_t b = m / (P * Q), p = (m / Q) % P, q = m % Q;
+    for (int64_t c = 0; c < C; ++c) {
+      double acc = 0.0;
+      for (int64_t r = 0; r < R; ++r) {
+        const int64_t ih = p * stride - pad + r;
+        if (ih < 0 || ih >= H) continue;
+        for (int64_t s = 0; s < S; ++s) {
+          const int64_t iw = q * stride - pad + s;
+          if (iw < 0 || iw >= W) continue;
+          acc += (double)x[((b * H + ih) * W + iw) * C + c] * (double)w[c * ldw + r * S + s];
+        }
+      }
+      y[i * C + c] = oracle_act(acc, act);
+    }
+  }
+}
+
+/* is_max: torch MaxPool2d (padded taps never win); else AvgPool2d over the
+ * full R x S window (count_include_pad: divisor R*S). */
+void oracle_pool2d(const float* x, float* y, const int64_t* rows, int64_t n_rows, int64_t batch, int64_t H, int64_t W,
+                   int64_t C, int64_t R, int64_t S, int64_t stride, int64_t pad, int32_t is_max) {
+  const int64_t P = (H + 2 * pad - R) / stride + 1;
+  const int64_t Q = (W + 2 * pad - S) / stride + 1;
+  const int64_t M = batch * P * Q;
+  const int64_t n = rows ? n_rows : M;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t m = rows ? rows[i] : i;
+    const int64_t b = m / (P * Q), p = (m / Q) % P, q = m % Q;
+    for (int64_t c = 0; c < C; ++c) {
+      double acc = is_max ? -INFINITY : 0.0;
+      for (int64_t r = 0; r < R; ++r) {
+        const int64_t ih = p * stride - pad + r;
+        if (ih < 0 || ih >= H) continue;
+        for (int64_t s = 0; s < S; ++s) {
+          const int64_t iw = q * stride - pad + s;
+          if (iw < 0 || iw >= W) continue;
+          const double v = (double)x[((b * H + ih) * W + iw) * C + c];
+          if (is_max)
+            acc = v > acc ? v : acc;
+          else
+            acc += v;
+        }
+      }
+      y[i * C + c] = is_max ? (float)acc : (float)(acc / (double)(R * S));
+    }
+  }
+}

@@ -13,7 +13,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GM_LIB_PATH") or os.path.join(_HERE, "_lib", "libgpumux_b200.so")
 
 GM_OK, GM_EINVAL, GM_ECONFIG, GM_EOOM, GM_EINTERNAL, GM_ECUDA, GM_ERANGE, GM_ENODEV = range(8)
-GM_LAYER_GEMM, GM_LAYER_CONV, GM_LAYER_DWCONV = 0, 1, 2
+GM_LAYER_GEMM, GM_LAYER_CONV, GM_LAYER_DWCONV, GM_LAYER_MAXPOOL, GM_LAYER_AVGPOOL = 0, 1, 2, 3, 4
+GM_ACT_NONE, GM_ACT_RELU, GM_ACT_RELU6, GM_ACT_GELU = 0, 1, 2, 3
 GM_MODE_PACKED, GM_MODE_TIME_ONLY, GM_MODE_SPACE_ONLY = 0, 1, 2
 
 
@@ -49,6 +50,16 @@ class gm_kernel_request(C.Structure):
     _fields_ = [("request_id", C.c_uint64), ("tenant_index", C.c_int32), ("layer_index", C.c_int32),
                 ("shape", gm_gemm_shape), ("enqueue_time", C.c_int64), ("slo_deadline", C.c_int64),
                 ("pass_index", C.c_uint32), ("batch", C.c_uint32)]
+
+
+class gm_round_tenant(C.Structure):
+    _fields_ = [("tenant", C.c_int32), ("reserved", C.c_int32), ("layers", C.POINTER(gm_gemm_shape)),
+                ("n_layers", C.c_size_t), ("slo_ns", C.c_int64)]
+
+
+class gm_round_tile(C.Structure):
+    _fields_ = [(f, C.c_int32) for f in ("tenant", "layer", "m_tile", "n_tile", "rows", "cols", "splits",
+                                          "kb_begin", "kb_end", "done", "dep", "plan")]
 
 
 class gm_batch_policy(C.Structure):
@@ -97,7 +108,8 @@ class gm_sim_completion(C.Structure):
 class gm_layer_desc(C.Structure):
     _fields_ = [("kind", C.c_int32), ("batch", C.c_int32), ("conv", gm_conv_spec), ("gemm", gm_gemm_shape),
                 ("x", C.c_void_p), ("w", C.c_void_p), ("y", C.c_void_p), ("ldx", C.c_int64), ("ldw", C.c_int64),
-                ("relu", C.c_int32), ("reserved0", C.c_int32)]
+                ("act", C.c_int32), ("src", C.c_int32), ("res", C.c_void_p), ("ldr", C.c_int64),
+                ("res_src", C.c_int32), ("reserved0", C.c_int32)]
 
 
 class gm_tenant_desc(C.Structure):
@@ -207,6 +219,8 @@ _SIGS = {
     "gm_members_launch_count": (C.c_int, [C.c_void_p, P(C.c_int32), P(C.c_int32), C.c_size_t, P(C.c_int32)]),
     "gm_plan_round": (C.c_int, [C.c_void_p, P(C.c_int32), C.c_size_t, C.c_int64, P(C.c_void_p)]),
     "gm_plans_times": (C.c_int, [C.c_void_p, C.c_size_t, P(C.c_int64), P(C.c_int64)]),
+    "gm_plan_round_shapes": (C.c_int, [P(gm_round_tenant), C.c_size_t, C.c_int64, P(gm_batch_policy),
+                                       P(gm_device_spec), C.c_void_p, P(C.c_uint64), P(C.c_void_p)]),
     "gm_prepare_plans": (C.c_int, [C.c_void_p, C.c_void_p]),
     "gm_dispatch_plans": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, P(C.c_int32)]),
     "gm_graph_capture_plans": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, P(C.c_void_p)]),
@@ -216,6 +230,7 @@ _SIGS = {
     "gm_graph_capture_round": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, P(C.c_void_p)]),
     "gm_trace_round": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, P(C.c_uint64), C.c_size_t, P(C.c_size_t)]),
     "gm_round_tiles": (C.c_int, [C.c_void_p, C.c_void_p, P(gm_tile), C.c_size_t, P(C.c_size_t)]),
+    "gm_round_tile_info": (C.c_int, [C.c_void_p, C.c_void_p, P(gm_round_tile), C.c_size_t, P(C.c_size_t)]),
     "gm_graph_capture_round_e2e": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, P(C.c_int32), P(C.c_void_p),
                                              P(C.c_void_p), P(C.c_size_t), P(C.c_void_p), P(C.c_void_p),
                                              P(C.c_size_t), P(C.c_void_p)]),

@@ -465,6 +465,38 @@ int gm_geomean(const double* v, size_t n, double* out) {
 
 // ---- virtual-clock driver --------------------------------------------------
 
+int gm_plan_round_shapes(const gm_round_tenant* tenants, size_t n, int64_t start, const gm_batch_policy* p,
+                         const gm_device_spec* d, gm_cache* cache, uint64_t* next_id, gm_plans** out) {
+  GM_API_BEGIN
+  need(out, "out");
+  need(p, "policy");
+  need(d, "device");
+  if (n && !tenants) throw std::invalid_argument("null argument: tenants");
+  std::vector<RoundTenant> round;
+  round.reserve(n);
+  for (size_t j = 0; j < n; ++j) {
+    RoundTenant rt;
+    rt.tenant = tenants[j].tenant;
+    if (tenants[j].n_layers && !tenants[j].layers) throw std::invalid_argument("null argument: layers");
+    for (size_t l = 0; l < tenants[j].n_layers; ++l) rt.layers.push_back(to_shape(tenants[j].layers[l]));
+    rt.slo_ns = tenants[j].slo_ns;
+    round.push_back(std::move(rt));
+  }
+  const Device dev = to_device(*d);
+  dev.check();
+  SignatureCache local;
+  std::uint64_t id = next_id ? *next_id : 1;
+  RoundResult res = plan_round(round, start, to_policy(*p), dev, cache ? cache->c : local, id);
+  if (next_id) *next_id = id;
+  auto* plans = new gm_plans();
+  for (RoundDispatch& r : res.dispatches) {
+    plans->plans.push_back(std::move(r.plan));
+    plans->times.emplace_back(r.start, r.end);
+  }
+  *out = plans;
+  GM_API_END
+}
+
 int gm_simulate_space_time(const gm_sim_config* cfg, gm_sim_trace** out) {
   GM_API_BEGIN
   need(cfg, "config");

@@ -57,6 +57,11 @@ int b_box_rows(int64_t n, int bn) { return static_cast<int>(std::min<int64_t>(bn
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// Operators computed on CUDA cores inside the persistent kernel (no tensor-core tile).
+bool cuda_core_kind(int kind) {
+  return kind == GM_LAYER_DWCONV || kind == GM_LAYER_MAXPOOL || kind == GM_LAYER_AVGPOOL;
+}
+
 
 }  // namespace
 
@@ -83,6 +88,11 @@ struct Operator {
   int64_t ldk = 0;
   void* wpad = nullptr;     // narrow-channel conv: weights repacked to 8 channels per tap
   int64_t kernel_k = 0;     // K the kernel iterates (0 = shape.k)
+  // dataflow (gm_layer_desc.src / res_src): producing layers of x and of the
+  // residual within the tenant (-1 = external), and this layer's output range
+  int src = -1, res_src = -1;
+  const char* y = nullptr;
+  int64_t y_bytes = 0;
 };
 
 struct Prepared {
@@ -309,8 +319,29 @@ struct Runtime {
       op.x = L.x;
       op.tenant = static_cast<int>(tenant_ops.size());
       op.layer = static_cast<int>(i);
-      if (!L.x || !L.w || !L.y) throw std::invalid_argument("register_tenant: null operand pointer");
+      const bool pool = L.kind == GM_LAYER_MAXPOOL || L.kind == GM_LAYER_AVGPOOL;
+      if (!L.x || (!L.w && !pool) || !L.y) throw std::invalid_argument("register_tenant: null operand pointer");
       if (!aligned16(L.y)) throw std::invalid_argument("register_tenant: output must be 16-byte aligned");
+      if (L.act < GM_ACT_NONE || L.act > GM_ACT_GELU) throw std::invalid_argument("register_tenant: unknown activation");
+      // dataflow: x (and the residual) must lie inside the named earlier layer's output
+      auto inside = [&](int j, const void* p, const char* what) {
+        if (j < 0) return;
+        if (j >= static_cast<int>(i))
+          throw std::invalid_argument(std::string("register_tenant: ") + what + " must name an earlier layer");
+        const Operator& pr = fresh[j];
+        const char* c = static_cast<const char*>(p);
+        if (c < pr.y || c >= pr.y + pr.y_bytes)
+          throw std::invalid_argument(std::string("register_tenant: ") + what + " does not point into layer " +
+                                      std::to_string(j) + "'s output");
+      };
+      inside(L.src, L.x, "src");
+      op.src = L.src < 0 ? -1 : L.src;
+      if (L.res) {
+        inside(L.res_src, L.res, "res_src");
+        op.res_src = L.res_src < 0 ? -1 : L.res_src;
+      } else if (L.res_src >= 0) {
+        throw std::invalid_argument("register_tenant: res_src without a residual pointer");
+      }
       if (L.kind == GM_LAYER_CONV) {
         op.conv = to_conv(L.conv);
         op.batch = L.batch < 1 ? 1 : L.batch;
@@ -405,6 +436,36 @@ struct Runtime {
           cuda_check(cudaMalloc(&op.scratch, static_cast<size_t>(op.shape.m * op.ldk * 2)), "cudaMalloc(im2col)");
           tiled_map(&md.a, op.scratch, op.shape.m, K, op.ldk, a_box_rows(op.shape.m));
         }
+      } else if (pool) {
+        // max / average pool: CUDA-core tile type; planned as a K = R*S GEMM
+        // like a depthwise conv (the reference's model of per-channel ops,
+        // proj/src/workload.cpp:66)
+        op.conv = to_conv(L.conv);
+        op.batch = L.batch < 1 ? 1 : L.batch;
+        const Conv& c = op.conv;
+        if (c.in_channels != c.out_channels) throw std::invalid_argument("register_tenant: pool needs Cin == Cout");
+        if (c.in_channels % 4 != 0) throw std::invalid_argument("register_tenant: pool channels must be a multiple of 4");
+        if (!aligned16(L.x)) throw std::invalid_argument("pool input must be 16-byte aligned");
+        if (L.res) throw std::invalid_argument("register_tenant: pools take no residual");
+        const int64_t P = (c.image_h + 2 * c.padding - c.kernel_h) / c.stride + 1;
+        const int64_t Q = (c.image_w + 2 * c.padding - c.kernel_w) / c.stride + 1;
+        if (P < 1 || Q < 1 || c.kernel_h < 1 || c.kernel_w < 1 || c.stride < 1 || c.padding < 0)
+          throw std::invalid_argument("conv output dims must be positive");
+        op.shape = Shape{op.batch * P * Q, c.out_channels, c.kernel_h * c.kernel_w};
+        op.n_tile = dev::kDwTileC;
+        md.a_mode = L.kind == GM_LAYER_MAXPOOL ? dev::kMaxPool : dev::kAvgPool;
+        md.dx = static_cast<const __nv_bfloat16*>(L.x);
+        md.dy = static_cast<__nv_bfloat16*>(L.y);
+        md.h_in = static_cast<int32_t>(c.image_h);
+        md.w_in = static_cast<int32_t>(c.image_w);
+        md.ch = static_cast<int32_t>(c.in_channels);
+        md.r_taps = static_cast<int32_t>(c.kernel_h * c.kernel_w);
+        md.s_taps = static_cast<int32_t>(c.kernel_w);
+        md.stride = static_cast<int32_t>(c.stride);
+        md.pad = static_cast<int32_t>(c.padding);
+        md.pq = static_cast<int32_t>(P * Q);
+        md.q = static_cast<int32_t>(Q);
+        md.images = op.batch;
       } else if (L.kind == GM_LAYER_DWCONV) {
         // depthwise conv: the reference models it as a K = R*S GEMM
         // (proj/src/workload.cpp:66); executed as the super-kernel's CUDA-core
@@ -456,7 +517,7 @@ struct Runtime {
         throw std::invalid_argument("register_tenant: unknown layer kind");
       }
       if (op.shape.n % 8 != 0) throw std::invalid_argument("register_tenant: output channels must be a multiple of 8");
-      if (op.shape.m > int64_t(0xFFFF) * (op.kind == GM_LAYER_DWCONV ? dev::kDwTileM : dev::kBM) ||
+      if (op.shape.m > int64_t(0xFFFF) * (cuda_core_kind(op.kind) ? dev::kDwTileM : dev::kBM) ||
           op.shape.m > INT32_MAX)
         throw std::invalid_argument("register_tenant: M too large for the tile table");
       store_map(&md.c, L.y, op.shape.m, op.shape.n);
@@ -468,7 +529,17 @@ struct Runtime {
       // one k-block moves an A box (rows x 64 channels, or 8 tap columns of
       // rows x 8 channels: the same bytes) plus a B box
       md.tx_bytes = static_cast<uint32_t>((a_box_rows(op.shape.m) + b_box_rows(op.shape.n, op.n_tile)) * dev::kBK * 2);
-      md.relu = L.relu ? 1 : 0;
+      md.act = L.act;
+      if (L.res) {
+        if (cuda_core_kind(op.kind)) throw std::invalid_argument("register_tenant: residual add needs a conv / GEMM");
+        const int64_t ldr = L.ldr > 0 ? L.ldr : op.shape.n;
+        if (ldr < op.shape.n || ldr % 8 != 0 || !aligned16(L.res))
+          throw std::invalid_argument("register_tenant: residual rows must be 16-byte aligned (ldr % 8 == 0, ldr >= N)");
+        md.res = static_cast<const __nv_bfloat16*>(L.res);
+        md.ldr = static_cast<int32_t>(ldr);
+      }
+      op.y = static_cast<const char*>(L.y);
+      op.y_bytes = op.shape.m * op.shape.n * 2;
       md.n_tile = op.n_tile;
       md.ring_narrow = ring_narrow_of(md, b_box_rows(op.shape.n, op.n_tile));
       op.slot = static_cast<int>(host_desc.size() + descs.size());
@@ -476,7 +547,7 @@ struct Runtime {
       descs.push_back(md);
       slot_of_new.push_back(f_index);
       // narrower-N variants (same operands, smaller B box / UMMA N)
-      if (op.kind != GM_LAYER_DWCONV && op.b_ptr) {
+      if (!cuda_core_kind(op.kind) && op.b_ptr) {
         int v = 0;
         for (int w = bn / 2; w >= 64 && v < 2; w /= 2) {
           if (op.shape.n <= w) break;
@@ -494,9 +565,14 @@ struct Runtime {
         }
       }
       // tall variant: two 128-row halves per tile sharing the B box
-      if (op.kind != GM_LAYER_DWCONV && op.b_ptr && op.shape.m >= 2 * dev::kBM && op.shape.n <= 128 &&
+      // (needs the 256-column kernel: the second half's accumulator sits at
+      // column 128 of a BN-column buffer, and the stage holds 2 A boxes + a
+      // <= 128-row B box, which only the 48 KB BN = 256 ring slot fits)
+      if (bn == 256 && !cuda_core_kind(op.kind) && op.b_ptr && op.shape.m >= 2 * dev::kBM && op.shape.n <= 128 &&
           (md.a_mode == dev::kATiled || md.a_mode == dev::kAIm2col || md.a_mode == dev::kAIm2colFold) &&
           a_box_rows(op.shape.m) == dev::kBM) {
+        if (!dev::Cfg<256>::kTallFits || b_box_rows(op.shape.n, 128) > 128)
+          throw std::logic_error("tall variant does not fit the ring slot / accumulator");
         dev::MemberDesc md3 = md;
         md3.tall = 1;
         md3.ring_narrow = 0;  // two A boxes: a wide-layout stage
@@ -600,7 +676,7 @@ struct Runtime {
     for (int f : members) {
       const Operator& op = flat[f];
       const auto [slot, w] = variant(f, plan_tiles, plan_tiles);
-      const int64_t tm = op.kind == GM_LAYER_DWCONV ? dev::kDwTileM : dev::kBM << (is_tall(slot) ? 1 : 0);
+      const int64_t tm = cuda_core_kind(op.kind) ? dev::kDwTileM : dev::kBM << (is_tall(slot) ? 1 : 0);
       const int64_t mt = (op.shape.m + tm - 1) / tm;
       const int64_t nt = (op.shape.n + w - 1) / w;
       for (int64_t a = 0; a < mt; ++a)
@@ -659,7 +735,6 @@ struct Runtime {
           }
         }
         const bool tall = is_tall(slot);
-        const int inst = static_cast<int>(targets.size());
         int dep = -1;
         if (op.layer > 0) {
           auto prev = last_instance.find(tenant_ops[op.tenant][op.layer - 1]);
@@ -670,8 +745,12 @@ struct Runtime {
           targets.push_back(1);
           p.gates.emplace_back(op.tenant, dep);
         }
+        // the member instance's own completion counter comes after any gate
+        // counter pushed above (a tile never publishes to what it waits on)
+        const int inst = static_cast<int>(targets.size());
+        if (dep == inst) throw std::logic_error("round program: member instance waits on its own counter");
         last_instance[f] = inst;
-        const int64_t tm = op.kind == GM_LAYER_DWCONV ? dev::kDwTileM : dev::kBM << (tall ? 1 : 0);
+        const int64_t tm = cuda_core_kind(op.kind) ? dev::kDwTileM : dev::kBM << (tall ? 1 : 0);
         const int64_t mt = (op.shape.m + tm - 1) / tm;
         const int64_t nt = (op.shape.n + w - 1) / w;
         const int kb = static_cast<int>((op.shape.k + dev::kBK - 1) / dev::kBK);
@@ -689,7 +768,7 @@ struct Runtime {
           splits = (kb + chunk - 1) / chunk;
         }
         // 4 epilogue warps arrive per output tile (8 for a depthwise tile: all of them compute it)
-        targets.push_back(static_cast<uint32_t>(mt * nt * (op.kind == GM_LAYER_DWCONV ? 8 : 4)));
+        targets.push_back(static_cast<uint32_t>(mt * nt * (cuda_core_kind(op.kind) ? 8 : 4)));
         for (int64_t a = 0; a < mt; ++a)
           for (int64_t b = 0; b < nt; ++b) {
             if (splits == 1) {
@@ -706,6 +785,10 @@ struct Runtime {
                                              static_cast<uint16_t>(std::min(kbt, (s + 1) * chunk)), n_ws});
             ++n_ws;
           }
+        if (op.prepass && op.src >= 0 && last_instance.count(tenant_ops[op.tenant][op.src]))
+          throw std::invalid_argument("round program: operator " + std::to_string(op.layer) + " of tenant " +
+                                      std::to_string(op.tenant) +
+                                      " needs a pre-pass over an input produced inside the round");
         if (op.prepass) (gated && op.layer == 0 ? p.gated_prepass : p.prepass_ops).push_back(f);
       }
       p.tile_plan.resize(table.size(), static_cast<uint16_t>(&pl - plans.data()));
@@ -1396,6 +1479,39 @@ int gm_round_tiles(gm_ctx* ctx, const gm_plans* p, gm_tile* out, size_t cap, siz
   GM_API_END
 }
 
+int gm_round_tile_info(gm_ctx* ctx, const gm_plans* p, gm_round_tile* out, size_t cap, size_t* n) {
+  GM_API_BEGIN
+  if (!p) throw std::invalid_argument("null argument: plans");
+  Runtime& rt = runtime_of(ctx);
+  std::vector<std::vector<int>> plans;
+  for (const Plan& plan : p->plans) plans.push_back(members_of(rt, plan));
+  Prepared& pr = rt.prepare_round(plans);
+  std::vector<dev::TileEntry> table(pr.n_tiles);
+  cuda_check(cudaMemcpy(table.data(), pr.tiles, table.size() * sizeof(dev::TileEntry), cudaMemcpyDeviceToHost),
+             "read round tiles");
+  if (n) *n = table.size();
+  if (!out || cap < table.size()) throw RangeError("output buffer too small");
+  for (size_t i = 0; i < table.size(); ++i) {
+    const dev::TileEntry& te = table[i];
+    const Operator& op = rt.flat[rt.slot_op[te.member]];
+    const dev::MemberDesc& md = rt.host_desc[te.member];
+    gm_round_tile& o = out[i];
+    o.tenant = op.tenant;
+    o.layer = op.layer;
+    o.m_tile = te.m_tile;
+    o.n_tile = te.n_tile;
+    o.rows = dev::cuda_core_mode(md.a_mode) ? dev::kDwTileM : (md.tall ? 2 * dev::kBM : dev::kBM);
+    o.cols = dev::cuda_core_mode(md.a_mode) ? dev::kDwTileC : md.n_tile;
+    o.splits = te.splits > 1 ? te.splits : 1;
+    o.kb_begin = te.kb_begin;
+    o.kb_end = te.kb_end;
+    o.done = te.done;
+    o.dep = te.dep;
+    o.plan = pr.tile_plan[i];
+  }
+  GM_API_END
+}
+
 int gm_graph_capture_round(gm_ctx* ctx, const gm_plans* p, int timed, gm_graph** out) {
   GM_API_BEGIN
   if (!p || !out) throw std::invalid_argument("null argument");
@@ -1453,6 +1569,15 @@ int gm_graph_capture_round_e2e(gm_ctx* ctx, const gm_plans* p, size_t n, const i
     bool found = false;
     for (const auto& gt : pr->gates) found |= gt.first == tenants[i];
     if (!found) throw std::invalid_argument("e2e round: tenant " + std::to_string(tenants[i]) + " is not in the round");
+  }
+  // every gate of the round must be opened by this program, or the kernel
+  // would spin on it until the device-side watchdog traps
+  for (const auto& gt : pr->gates) {
+    bool covered = false;
+    for (size_t i = 0; i < n; ++i) covered |= gt.first == tenants[i];
+    if (!covered)
+      throw std::invalid_argument("e2e round: tenant " + std::to_string(gt.first) +
+                                  " of the round has no host input (every round tenant needs one)");
   }
   *out = capture(ctx, [&](cudaStream_t cs, gm_graph& g) {
     // copy branch: each tenant's H2D, its layer-0 pre-pass, then the gate

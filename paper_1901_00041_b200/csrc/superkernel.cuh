@@ -56,7 +56,11 @@ struct Cfg {
   static constexpr int kNarrowBytes = 32768;
   static constexpr int kNarrowSlots = kStages * kStageBytes / kNarrowBytes;
   static constexpr int kMaxSlots = kNarrowSlots > kStages ? kNarrowSlots : kStages;
+  // A tall tile's stage: two 128-row A boxes and a <= 128-row B box; its second
+  // accumulator half starts at column 128 of the tile's BN-column buffer.
+  static constexpr bool kTallFits = 2 * kABytes + 128 * kBK * 2 <= kStageBytes && 128 + 128 <= BN;
 };
+static_assert(Cfg<256>::kTallFits, "tall tiles need the 256-column ring slot");
 
 // A-operand modes: 2-D tiled box; TMA im2col (C_in % 64 == 0: one 128 B
 // channel block per k-block, SW128); narrow-channel TMA im2col (input pixel
@@ -65,7 +69,16 @@ struct Cfg {
 // each output column's horizontal window into one 32-channel "pixel"
 // (X'[b, h, q, s*C_in + c]); the conv becomes R x 1 with vertical stride,
 // two 64 B (SW64) TMA im2col columns per k-block.
-enum : int32_t { kATiled = 0, kAIm2col = 1, kAIm2colNarrow = 2, kAIm2colFold = 3, kDepthwise = 4 };
+enum : int32_t { kATiled = 0, kAIm2col = 1, kAIm2colNarrow = 2, kAIm2colFold = 3, kDepthwise = 4, kMaxPool = 5,
+                 kAvgPool = 6 };
+// Modes >= kDepthwise are CUDA-core tile types (no TMA / MMA pipeline): the
+// eight epilogue warps compute them.  Max / average pooling (ResNet's stem
+// maxpool and global avgpool, VGG's 2x2 pools, MobileNet-v2's avgpool) sit
+// between convs on a tenant's dataflow chain, so they are tiles of the same
+// persistent launch, gated on the same dependency counters.
+__host__ __device__ constexpr bool cuda_core_mode(int32_t m) { return m >= kDepthwise; }
+// Epilogue activations (applied after the residual add).
+enum : int32_t { kActNone = 0, kActRelu = 1, kActRelu6 = 2, kActGelu = 3 };
 // Depthwise conv (MobileNet-v2) is a CUDA-core tile type inside the same
 // persistent kernel (tensor cores do not apply: one filter per channel).  Its
 // tiles skip the TMA/MMA pipeline; the eight epilogue warps compute them
@@ -97,7 +110,7 @@ struct alignas(128) MemberDesc {
   int32_t stride, pad;
   int32_t s_taps;       // filter width S
   int32_t c_blocks;     // Cin / kBK
-  int32_t relu;
+  int32_t act;          // kAct*: fused activation
   int32_t n_tile;       // output columns per tile (<= BN): narrower for few-tile members
   int32_t taps;         // narrow im2col: R*S filter taps
   int32_t images;       // narrow im2col: batch (an out-of-range image zero-fills a box)
@@ -114,6 +127,12 @@ struct alignas(128) MemberDesc {
   const __nv_bfloat16* dw;
   __nv_bfloat16* dy;
   int32_t h_in, w_in, ch, r_taps, ldw;
+  // fused residual add (ResNet's identity / downsample add, MobileNet-v2's
+  // inverted-residual add, BERT's skip connections): y = act(acc + res), res
+  // [M, N] row-major bf16 with row stride ldr; null = none.  The residual is
+  // an earlier layer of the same tenant, complete by the dependency chain.
+  const __nv_bfloat16* res;
+  int32_t ldr;
 };
 
 // Device tile-table entry; `member` is the registered slot index.
@@ -326,14 +345,32 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ uint32_t pack_bf16(uint32_t lo_bits, uint32_t hi_bits, int relu) {
+__device__ __forceinline__ float activate(float v, int act) {
+  if (act == kActRelu) return fmaxf(v, 0.f);
+  if (act == kActRelu6) return fminf(fmaxf(v, 0.f), 6.f);
+  if (act == kActGelu) return 0.5f * v * (1.f + erff(v * 0.70710678118654752f));
+  return v;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(uint32_t lo_bits, uint32_t hi_bits, int act) {
   float lo = __uint_as_float(lo_bits), hi = __uint_as_float(hi_bits);
-  if (relu) {
-    lo = fmaxf(lo, 0.f);
-    hi = fmaxf(hi, 0.f);
+  if (act) {
+    lo = activate(lo, act);
+    hi = activate(hi, act);
   }
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// Adds 8 bf16 residual values (one 16-byte load) to 8 fp32 accumulators.
+__device__ __forceinline__ void add_residual8(uint32_t* v, uint4 r) {
+  const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __nv_bfloat162 p = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+    v[2 * i] = __float_as_uint(__uint_as_float(v[2 * i]) + __low2float(p));
+    v[2 * i + 1] = __float_as_uint(__uint_as_float(v[2 * i + 1]) + __high2float(p));
+  }
 }
 
 // Depthwise tile (CUDA cores): epilogue warp `ew` (0..7) computes output
@@ -404,10 +441,69 @@ __device__ __forceinline__ void depthwise_tile(const MemberDesc* __restrict__ md
     for (int j = 0; j < kG; ++j) {
       if (bb[j] < 0) continue;
       uint2 o;
-      o.x = pack_bf16(__float_as_uint(acc[j][0]), __float_as_uint(acc[j][1]), md->relu);
-      o.y = pack_bf16(__float_as_uint(acc[j][2]), __float_as_uint(acc[j][3]), md->relu);
+      o.x = pack_bf16(__float_as_uint(acc[j][0]), __float_as_uint(acc[j][1]), md->act);
+      o.y = pack_bf16(__float_as_uint(acc[j][2]), __float_as_uint(acc[j][3]), md->act);
       *reinterpret_cast<uint2*>(md->dy + static_cast<int64_t>(m_base + pp * (i0 + j)) * C + c) = o;
     }
+  }
+}
+
+// Pool tile (CUDA cores): max or average over an R x S window, same lane
+// mapping as the depthwise tile (epilogue warp `ew` owns kDwPixW output pixels,
+// each lane 4 channels: one 8-byte load per tap and pixel).  Max pooling skips
+// padded taps (torch MaxPool2d); average pooling divides by R*S (the global
+// pools it serves have no padding).
+__device__ __forceinline__ void pool_tile(const MemberDesc* __restrict__ md, const TileEntry& te, int ew, int lane) {
+  const int M = md->m, C = md->ch, H = md->h_in, W = md->w_in;
+  const int cbase = te.n_tile * kDwTileC;
+  const int g = min(kDwTileC, C - cbase) >> 2;
+  const int gp = g <= 8 ? 8 : (g <= 16 ? 16 : 32);
+  const int pp = 32 / gp;
+  const int cg = lane & (gp - 1), sub = lane / gp;
+  if (cg >= g) return;
+  const int c = cbase + cg * 4;
+  const int R = md->r_taps / md->s_taps, S = md->s_taps, st = md->stride, pad = md->pad, PQ = md->pq, Q = md->q;
+  const bool mx = md->a_mode == kMaxPool;
+  const float init = mx ? -INFINITY : 0.f;
+  const float scale = mx ? 1.f : 1.f / static_cast<float>(R * S);
+  const int m_base = te.m_tile * kDwTileM + ew * kDwPixW + sub;
+  const int npx = (kDwPixW + pp - 1) / pp;
+  for (int i = 0; i < npx; ++i) {
+    const int m = m_base + pp * i;
+    if (m >= M) break;
+    const int b = m / PQ;
+    const int rem = m - b * PQ;
+    const int p = rem / Q;
+    const int h0 = p * st - pad, w0 = (rem - p * Q) * st - pad;
+    float a0 = init, a1 = init, a2 = init, a3 = init;
+    for (int r = 0; r < R; ++r) {
+      const int ih = h0 + r;
+      if (ih < 0 || ih >= H) continue;
+      const __nv_bfloat16* row = md->dx + (static_cast<int64_t>(b) * H + ih) * W * C + c;
+#pragma unroll 4
+      for (int s = 0; s < S; ++s) {
+        const int iw = w0 + s;
+        if (iw < 0 || iw >= W) continue;
+        const uint2 raw = __ldcg(reinterpret_cast<const uint2*>(row + static_cast<int64_t>(iw) * C));
+        const __nv_bfloat162 x01 = *reinterpret_cast<const __nv_bfloat162*>(&raw.x);
+        const __nv_bfloat162 x23 = *reinterpret_cast<const __nv_bfloat162*>(&raw.y);
+        if (mx) {
+          a0 = fmaxf(a0, __low2float(x01));
+          a1 = fmaxf(a1, __high2float(x01));
+          a2 = fmaxf(a2, __low2float(x23));
+          a3 = fmaxf(a3, __high2float(x23));
+        } else {
+          a0 += __low2float(x01);
+          a1 += __high2float(x01);
+          a2 += __low2float(x23);
+          a3 += __high2float(x23);
+        }
+      }
+    }
+    uint2 o;
+    o.x = pack_bf16(__float_as_uint(a0 * scale), __float_as_uint(a1 * scale), md->act);
+    o.y = pack_bf16(__float_as_uint(a2 * scale), __float_as_uint(a3 * scale), md->act);
+    *reinterpret_cast<uint2*>(md->dy + static_cast<int64_t>(m) * C + c) = o;
   }
 }
 
@@ -539,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (t >= 0) {
           te = tiles[t];
           md = slots + te.member;
-          dw = md->a_mode == kDepthwise;
+          dw = cuda_core_mode(md->a_mode);
         }
         mbar_wait(&tq_empty[qslot], qphase ^ 1);
         tq[qslot] = dw ? (t | kDwTag) : t;  // consumers skip / route a depthwise tile without loading it
@@ -981,7 +1077,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t now = globaltimer();
           for (int j = 0; j < 5; ++j) trace[6 * t + j] = now;  // no load / MMA phases
         }
-        depthwise_tile(md, te, warp - 4, lane);
+        if (md->a_mode == kDepthwise)
+          depthwise_tile(md, te, warp - 4, lane);
+        else
+          pool_tile(md, te, warp - 4, lane);
         __syncwarp();
         if (trace && warp == 4 && lane == 0) trace[6 * t + 5] = globaltimer();
         if (te.done >= 0 && lane == 0) {
@@ -999,7 +1098,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m0 = te.m_tile * (kBM << tall) + quarter * 32;
       const int n0 = te.n_tile * md->n_tile;
       const int cols = min(md->n_tile, md->n - n0);
-      const int relu = md->relu;
+      const int act = md->act;
+      const __nv_bfloat16* res = md->res;
+      const int ldr = md->ldr, n_real = md->n, m_real = md->m;
+      if (res && lane == 0) {
+        // the residual is an earlier layer of this tenant, complete by the
+        // dependency chain the producer waited on; acquire it for this warp's
+        // generic-proxy loads (the producer's acquire ordered only its TMA).
+        // Outside a round program it comes from a prior launch: PDL wait.
+        if (te.dep >= 0) {
+          wait_counter(counters + te.dep, targets[te.dep], 32);
+        } else if (!dw_gated) {
+          asm volatile("griddepcontrol.wait;" ::: "memory");
+          dw_gated = true;
+        }
+      }
+      __syncwarp();
       const int sw = (lane >> 1) & 3;  // SWIZZLE_64B: 16B chunk j of a 64 B row -> j ^ row[2:1]
       // Claim the next staging buffer once the store issued from it two
       // chunks ago has finished reading it.
@@ -1013,16 +1127,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         buf ^= 1;
       };
       // 32 fp32 accumulators of this lane's row -> bf16 -> one 32x32 store box.
-      auto store_bf16 = [&](const uint32_t (&v)[32], int c, int mrow) {
+      auto store_bf16 = [&](uint32_t (&v)[32], int c, int mrow) {
+        if (res) {
+          // this lane's row, 32 columns: four 16-byte loads (each lane reads
+          // whole 32-byte sectors), clipped at the M / N edges
+          const int m = mrow + lane;
+          if (m < m_real) {
+            const __nv_bfloat16* rrow = res + static_cast<int64_t>(m) * ldr + n0 + c;
+            uint4 rv[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              rv[j] = n0 + c + 8 * j < n_real ? __ldcg(reinterpret_cast<const uint4*>(rrow + 8 * j))
+                                              : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) add_residual8(v + 8 * j, rv[j]);
+          }
+        }
         uint8_t* sbuf = claim();
         uint8_t* row = sbuf + lane * 64;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           uint4 pk;
-          pk.x = pack_bf16(v[8 * j + 0], v[8 * j + 1], relu);
-          pk.y = pack_bf16(v[8 * j + 2], v[8 * j + 3], relu);
-          pk.z = pack_bf16(v[8 * j + 4], v[8 * j + 5], relu);
-          pk.w = pack_bf16(v[8 * j + 6], v[8 * j + 7], relu);
+          pk.x = pack_bf16(v[8 * j + 0], v[8 * j + 1], act);
+          pk.y = pack_bf16(v[8 * j + 2], v[8 * j + 3], act);
+          pk.z = pack_bf16(v[8 * j + 4], v[8 * j + 5], act);
+          pk.w = pack_bf16(v[8 * j + 6], v[8 * j + 7], act);
           *reinterpret_cast<uint4*>(row + ((j ^ sw) << 4)) = pk;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -74,9 +74,14 @@ class Graph:
 class TenantModel:
     """Device buffers of one tenant's operator graph with synthetic data.
 
-    Inputs U(-1, 1), weights Kaiming-normal (std sqrt(2 / fan_in)); each tensor
-    from its own generator seeded by mix64(seed, tenant, layer, kind).  Weight
-    rows are padded to a multiple of 8 elements (16-byte TMA strides).
+    Dataflow: a layer with ``src`` reads that earlier layer's output buffer
+    (a view of it), and ``res`` adds that layer's output in the epilogue, so
+    the tenant's query input determines every activation down to its result.
+    A layer without ``src`` (the first, or every layer of a plain operator
+    list) gets its own input buffer.  Inputs U(-1, 1), weights Kaiming-normal
+    (std sqrt(2 / fan_in)); each tensor from its own generator seeded by
+    mix64(seed, tenant, layer, kind).  Weight rows are padded to a multiple of
+    8 elements (16-byte TMA strides).
     """
 
     def __init__(self, layers: Sequence[Layer], batch: int, seed: int, tenant: int, device: torch.device,
@@ -84,39 +89,54 @@ class TenantModel:
         self.layers = list(layers)
         self.batch = batch
         self.buffers: List[LayerBuffers] = []
+        ys: List[torch.Tensor] = []
         for li, L in enumerate(self.layers):
             s = L.gemm_shape(batch)
             g_in = torch.Generator(device=device).manual_seed(mix64(seed, tenant, li, KIND_INPUT))
             g_w = torch.Generator(device=device).manual_seed(mix64(seed, tenant, li, KIND_WEIGHT))
+            y = torch.empty(s.m, s.n, device=device, dtype=torch.bfloat16)
+            ys.append(y)
+            src = -1 if L.src is None else int(L.src)
+            res, res_src = None, -1
+            if L.res is not None:
+                res_src = int(L.res)
+                res = ys[res_src].view(s.m, s.n)  # same rows and columns as this layer's output
+            windowed = L.kind in ("conv", "dwconv", "maxpool", "avgpool")
+            if windowed:
+                c = L.conv
+                if src >= 0:
+                    x = ys[src].view(batch, c.image_h, c.image_w, c.in_channels)
+                else:
+                    x = (torch.rand(batch, c.image_h, c.image_w, c.in_channels, device=device, generator=g_in) * 2 - 1)
+                    x = x.to(torch.bfloat16)
+                    if narrow_inputs and L.kind == "conv" and c.in_channels < NARROW_C and c.kernel_h > 1:
+                        # narrow-channel input (RGB stem): stored with an 8-channel
+                        # pixel pitch, zero padded, for the narrow TMA im2col path
+                        # (opt-in: one 16 B TMA request per pixel and tap is slower
+                        # than the explicit pre-pass on B200)
+                        xp = torch.zeros(batch, c.image_h, c.image_w, NARROW_C, device=device, dtype=torch.bfloat16)
+                        xp[..., : c.in_channels] = x
+                        x = xp
+            if L.kind in ("maxpool", "avgpool"):
+                self.buffers.append(LayerBuffers(L.kind, x, None, y, conv=L.conv, batch=batch, act=L.act, src=src))
+                continue
+            if L.kind == "dwconv":
+                w = (torch.randn(s.n, s.k, device=device, generator=g_w) * (2.0 / s.k) ** 0.5).to(torch.bfloat16)
+                self.buffers.append(LayerBuffers("dwconv", x, w, y, conv=L.conv, batch=batch, act=L.act, src=src))
+                continue
             kpad = (s.k + 7) // 8 * 8
             w = torch.zeros(s.n, kpad, device=device, dtype=torch.bfloat16)
             w[:, : s.k] = (torch.randn(s.n, s.k, device=device, generator=g_w) * (2.0 / s.k) ** 0.5).to(torch.bfloat16)
-            if L.kind == "dwconv":
-                c = L.conv
-                x = (torch.rand(batch, c.image_h, c.image_w, c.in_channels, device=device, generator=g_in) * 2 - 1)
-                w = (torch.randn(s.n, s.k, device=device, generator=g_w) * (2.0 / s.k) ** 0.5).to(torch.bfloat16)
-                y = torch.empty(s.m, s.n, device=device, dtype=torch.bfloat16)
-                self.buffers.append(LayerBuffers("dwconv", x.to(torch.bfloat16), w, y, conv=c, batch=batch))
-                continue
             if L.kind == "conv":
-                c = L.conv
-                x = (torch.rand(batch, c.image_h, c.image_w, c.in_channels, device=device, generator=g_in) * 2 - 1)
-                x = x.to(torch.bfloat16)
-                if narrow_inputs and c.in_channels < NARROW_C and c.kernel_h > 1:
-                    # narrow-channel input (RGB stem): stored with an 8-channel
-                    # pixel pitch, zero padded, for the narrow TMA im2col path
-                    # (opt-in: one 16 B TMA request per pixel and tap is slower
-                    # than the explicit pre-pass on B200)
-                    xp = torch.zeros(batch, c.image_h, c.image_w, NARROW_C, device=device, dtype=torch.bfloat16)
-                    xp[..., : c.in_channels] = x
-                    x = xp
-                y = torch.empty(s.m, s.n, device=device, dtype=torch.bfloat16)
-                self.buffers.append(LayerBuffers("conv", x, w, y, conv=c, batch=batch))
+                self.buffers.append(LayerBuffers("conv", x, w, y, conv=L.conv, batch=batch, act=L.act, src=src,
+                                                 res=res, res_src=res_src))
+                continue
+            if src >= 0:
+                x = ys[src].view(s.m, -1)[:, L.src_col: L.src_col + s.k]  # strided view: ldx = the source's width
             else:
-                xfull = torch.zeros(s.m, kpad, device=device, dtype=torch.bfloat16)
-                xfull[:, : s.k] = (torch.rand(s.m, s.k, device=device, generator=g_in) * 2 - 1).to(torch.bfloat16)
-                y = torch.empty(s.m, s.n, device=device, dtype=torch.bfloat16)
-                self.buffers.append(LayerBuffers("gemm", xfull, w, y, gemm=s))
+                x = torch.zeros(s.m, kpad, device=device, dtype=torch.bfloat16)
+                x[:, : s.k] = (torch.rand(s.m, s.k, device=device, generator=g_in) * 2 - 1).to(torch.bfloat16)
+            self.buffers.append(LayerBuffers("gemm", x, w, y, gemm=s, act=L.act, src=src, res=res, res_src=res_src))
 
     @property
     def query_input(self) -> torch.Tensor:
@@ -343,11 +363,15 @@ class ServeResult:
 
 
 def _variant(buf: LayerBuffers, max_batch: int, b: int) -> LayerBuffers:
-    """The same device buffers viewed as a batch-b operator (the first b queries)."""
-    if buf.kind in ("conv", "dwconv"):
-        return LayerBuffers(buf.kind, buf.x, buf.w, buf.y, conv=buf.conv, batch=b, relu=buf.relu)
+    """The same device buffers viewed as a batch-b operator (the first b
+    queries: NHWC images and GEMM rows are query-major, so the batch-b views of
+    a dataflow chain still chain)."""
+    if buf.kind in ("conv", "dwconv", "maxpool", "avgpool"):
+        return LayerBuffers(buf.kind, buf.x, buf.w, buf.y, conv=buf.conv, batch=b, act=buf.activation, src=buf.src,
+                            res=buf.res, res_src=buf.res_src)
     g = buf.gemm
-    return LayerBuffers("gemm", buf.x, buf.w, buf.y, gemm=GemmShape(g.m // max_batch * b, g.n, g.k), relu=buf.relu)
+    return LayerBuffers("gemm", buf.x, buf.w, buf.y, gemm=GemmShape(g.m // max_batch * b, g.n, g.k),
+                        act=buf.activation, src=buf.src, res=buf.res, res_src=buf.res_src)
 
 
 class ServingEngine:

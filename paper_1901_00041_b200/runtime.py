@@ -24,7 +24,13 @@ class LayerBuffers:
 
     conv: x NHWC [b, H, W, Cin], w [Cout, ldw] (KRSC rows), y NHWC [b, P, Q, Cout]
     dwconv: x NHWC [b, H, W, C], w [C, ldw] (R*S taps per row), y NHWC [b, P, Q, C]
+    maxpool / avgpool: x NHWC [b, H, W, C], y NHWC [b, P, Q, C], w unused
     gemm: x [M, ldx], w [N, ldw], y [M, N]
+
+    ``act`` (gm_activation; ``relu=True`` is act 1) runs after the optional
+    residual add ``res`` ([M, N] rows, row stride ``res.stride(0)``).  ``src``
+    / ``res_src``: the tenant's earlier layer whose output ``x`` / ``res``
+    views (-1 = an external buffer).
     """
     kind: str
     x: object
@@ -34,6 +40,14 @@ class LayerBuffers:
     batch: int = 1
     gemm: Optional[GemmShape] = None
     relu: bool = False
+    act: Optional[int] = None
+    src: int = -1
+    res: object = None
+    res_src: int = -1
+
+    @property
+    def activation(self) -> int:
+        return self.act if self.act is not None else (1 if self.relu else 0)
 
 
 class Context:
@@ -78,9 +92,19 @@ class Context:
         descs = (N.gm_layer_desc * len(layers))()
         for i, L in enumerate(layers):
             d = descs[i]
-            d.x, d.w, d.y = L.x.data_ptr(), L.w.data_ptr(), L.y.data_ptr()
-            d.relu = int(bool(L.relu))
-            if L.kind == "conv":
+            d.x, d.y = L.x.data_ptr(), L.y.data_ptr()
+            d.w = L.w.data_ptr() if L.w is not None else None
+            d.act = L.activation
+            d.src = L.src
+            d.res_src = L.res_src
+            if L.res is not None:
+                d.res = L.res.data_ptr()
+                d.ldr = L.res.stride(0)
+            if L.kind in ("maxpool", "avgpool"):
+                d.kind = N.GM_LAYER_MAXPOOL if L.kind == "maxpool" else N.GM_LAYER_AVGPOOL
+                d.batch = L.batch
+                d.conv = L.conv._c()
+            elif L.kind == "conv":
                 d.kind = N.GM_LAYER_CONV
                 d.batch = L.batch
                 d.conv = L.conv._c()
@@ -196,6 +220,20 @@ class Round:
         out = C.c_int32()
         check(lib().gm_dispatch_plans(self.ctx.handle, self.handle, int(stream), C.byref(out)))
         return int(out.value)
+
+    def tile_info(self) -> List[dict]:
+        """The executed tile table of this round's program (gm_round_tile_info)."""
+        n = C.c_size_t()
+        arr = (N.gm_round_tile * max(1, self._n_round_tiles()))()
+        check(lib().gm_round_tile_info(self.ctx.handle, self.handle, arr, len(arr), C.byref(n)))
+        return [{f: getattr(arr[i], f) for f, _ in N.gm_round_tile._fields_} for i in range(n.value)]
+
+    def _n_round_tiles(self) -> int:
+        n = C.c_size_t()
+        st = lib().gm_round_tile_info(self.ctx.handle, self.handle, None, 0, C.byref(n))
+        if st not in (N.GM_OK, N.GM_ERANGE):
+            check(st)
+        return int(n.value)
 
     def launch_round(self, stream: int = 0) -> int:
         """The whole round as one persistent launch (round program)."""

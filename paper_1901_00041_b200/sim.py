@@ -131,3 +131,38 @@ def simulate_space_time(cfg: SpaceTimeConfig) -> Trace:
                      int(comp.value))
     finally:
         lib().gm_sim_trace_destroy(h)
+
+
+@dataclass
+class RoundDispatch:
+    """One dispatch of a planned round: the formed super-kernel and its
+    virtual [start, end)."""
+    kernel: object  # scheduler.SuperKernel
+    start: int
+    end: int
+
+
+def plan_round_shapes(tenants: Sequence[tuple], start: int, policy: BatchPolicy, device: DeviceSpec,
+                      cache=None) -> List[RoundDispatch]:
+    """gm_plan_round_shapes: one closed-loop round on the virtual clock, host
+    only.  ``tenants`` = [(tenant_index, [GemmShape, ...], slo_seconds), ...].
+    The run_space_time loop of proj/src/sim.cpp:452-576 for one pass per
+    tenant; heterogeneous layer lists are allowed (B200 extension)."""
+    from .scheduler import _Plans, _unpack_plans
+    keep = []
+    arr = (N.gm_round_tenant * max(1, len(tenants)))()
+    for i, (t, layers, slo) in enumerate(tenants):
+        ls = (N.gm_gemm_shape * max(1, len(layers)))(*[N.gm_gemm_shape(s.m, s.n, s.k) for s in layers])
+        keep.append(ls)
+        arr[i] = N.gm_round_tenant(int(t), 0, ls, len(layers), int(lib().gm_to_ns(float(slo))))
+    h = C.c_void_p()
+    check(lib().gm_plan_round_shapes(arr, len(tenants), int(start), C.byref(policy._c()), C.byref(device._c()),
+                                     cache.handle if cache is not None else None, None, C.byref(h)))
+    owner = _Plans(h.value)
+    kernels = _unpack_plans(h.value, owner)
+    out = []
+    for i, k in enumerate(kernels):
+        s_, e_ = C.c_int64(), C.c_int64()
+        check(lib().gm_plans_times(h.value, i, C.byref(s_), C.byref(e_)))
+        out.append(RoundDispatch(k, int(s_.value), int(e_.value)))
+    return out

@@ -73,13 +73,25 @@ def find_preset(name: str) -> Optional[WorkloadPreset]:
 
 # ---------------------------------------------------------------- real graphs
 
+ACT_NONE, ACT_RELU, ACT_RELU6, ACT_GELU = 0, 1, 2, 3  # gm_activation
+POOLS = ("maxpool", "avgpool")
+WINDOWED = ("conv", "dwconv") + POOLS
+
+
 @dataclass(frozen=True)
 class Layer:
     """One operator of a tenant graph.
 
-    conv/dwconv: ``conv`` holds the ConvSpec (per image).
+    conv/dwconv/maxpool/avgpool: ``conv`` holds the ConvSpec (per image; a
+          pool's kernel is its window, in == out channels).
     gemm: ``rows`` rows per query (1 for a classifier, seq_len for BERT),
           ``n`` outputs, ``k`` inner dimension.
+
+    Dataflow: ``src`` names the earlier layer whose output this layer reads
+    (None = its own input buffer, e.g. the tenant's query batch), starting at
+    column ``src_col`` of that output viewed as [rows, -1] (BERT's attention
+    output projection reads the V third of the qkv projection); ``res`` names
+    the earlier layer added before the activation ``act`` (residual blocks).
     """
     name: str
     kind: str
@@ -87,9 +99,14 @@ class Layer:
     rows: int = 0
     n: int = 0
     k: int = 0
+    act: int = ACT_NONE
+    src: Optional[int] = None
+    res: Optional[int] = None
+    src_col: int = 0
 
     def gemm_shape(self, batch: int = 1) -> GemmShape:
-        if self.kind == "dwconv":  # the reference's model of a depthwise conv: K = R*S (workload.cpp:66)
+        if self.kind == "dwconv" or self.kind in POOLS:
+            # the reference's model of a per-channel op: K = R*S (workload.cpp:66)
             s = batch_inputs(im2col_gemm_dims(self.conv), batch)
             return GemmShape(s.m, s.n, self.conv.kernel_h * self.conv.kernel_w)
         if self.kind == "conv":
@@ -97,90 +114,126 @@ class Layer:
         return GemmShape(self.rows * batch, self.n, self.k)
 
     def flops(self, batch: int = 1) -> int:
+        """Multiply-add FLOPs (2mnk); pools do no multiply-adds and count 0."""
+        if self.kind in POOLS:
+            return 0
         s = self.gemm_shape(batch)  # dwconv: per-channel filter, K = R*S
         return 2 * s.m * s.n * s.k
 
     def compulsory_bytes(self, batch: int = 1, elem: int = 2) -> int:
-        """Implicit-GEMM bf16 traffic: input + weights + output."""
-        if self.kind in ("conv", "dwconv"):
-            c = self.conv
-            s = self.gemm_shape(batch)
-            w = c.out_channels * c.kernel_h * c.kernel_w * (1 if self.kind == "dwconv" else c.in_channels)
-            return elem * (batch * c.image_h * c.image_w * c.in_channels + w + s.m * s.n)
+        """Implicit-GEMM bf16 traffic: input + weights + output (SURVEY §8(d));
+        plus the residual read when one is fused."""
         s = self.gemm_shape(batch)
-        return elem * (s.m * s.k + s.n * s.k + s.m * s.n)
+        extra = s.m * s.n if self.res is not None else 0
+        if self.kind in WINDOWED:
+            c = self.conv
+            if self.kind in POOLS:
+                w = 0
+            else:
+                w = c.out_channels * c.kernel_h * c.kernel_w * (1 if self.kind == "dwconv" else c.in_channels)
+            return elem * (batch * c.image_h * c.image_w * c.in_channels + w + s.m * s.n + extra)
+        return elem * (s.m * s.k + s.n * s.k + s.m * s.n + extra)
 
 
-def _conv(name, hw, cin, cout, r, stride, pad):
-    return Layer(name, "conv", ConvSpec(hw, hw, r, r, cin, cout, stride, pad))
+def _conv(name, hw, cin, cout, r, stride, pad, act=ACT_NONE, src=None, res=None):
+    return Layer(name, "conv", ConvSpec(hw, hw, r, r, cin, cout, stride, pad), act=act, src=src, res=res)
+
+
+def _pool(name, kind, hw, c, r, stride, pad, src):
+    return Layer(name, kind, ConvSpec(hw, hw, r, r, c, c, stride, pad), src=src)
 
 
 def resnet50(image: int = 224, classifier: bool = True) -> List[Layer]:
-    """torchvision resnet50 (v1.5: stride on the 3x3), 53 convs + fc."""
-    L = [_conv("conv1", image, 3, 64, 7, 2, 3)]
+    """torchvision resnet50 (v1.5: stride on the 3x3) as a dataflow graph:
+    stem conv + relu, maxpool 3x3/2, 16 bottlenecks (conv1/conv2 + relu;
+    relu(conv3 + identity), or relu(downsample + conv3) with the add fused into
+    the downsample, which is listed after conv3), global avgpool, fc.
+    BatchNorm is folded into the (synthetic) weights."""
+    L = [_conv("conv1", image, 3, 64, 7, 2, 3, act=ACT_RELU)]
     hw = (image + 6 - 7) // 2 + 1
-    hw = (hw + 2 - 3) // 2 + 1  # maxpool 3x3 s2 p1
-    cin = 64
+    L.append(_pool("maxpool", "maxpool", hw, 64, 3, 2, 1, src=0))
+    hw = (hw + 2 - 3) // 2 + 1
+    cin, block_in = 64, 1
     for stage, (width, blocks, stride) in enumerate([(64, 3, 1), (128, 4, 2), (256, 6, 2), (512, 3, 2)], start=1):
         out = width * 4
         for b in range(blocks):
             s = stride if b == 0 else 1
             p = f"layer{stage}.{b}"
-            L.append(_conv(p + ".conv1", hw, cin, width, 1, 1, 0))
-            L.append(_conv(p + ".conv2", hw, width, width, 3, s, 1))
+            L.append(_conv(p + ".conv1", hw, cin, width, 1, 1, 0, act=ACT_RELU, src=block_in))
+            L.append(_conv(p + ".conv2", hw, width, width, 3, s, 1, act=ACT_RELU, src=len(L) - 1))
             ohw = (hw + 2 - 3) // s + 1
-            L.append(_conv(p + ".conv3", ohw, width, out, 1, 1, 0))
             if b == 0:
-                L.append(_conv(p + ".downsample", hw, cin, out, 1, s, 0))
+                L.append(_conv(p + ".conv3", ohw, width, out, 1, 1, 0, src=len(L) - 1))
+                L.append(_conv(p + ".downsample", hw, cin, out, 1, s, 0, act=ACT_RELU, src=block_in, res=len(L) - 1))
+            else:
+                L.append(_conv(p + ".conv3", ohw, width, out, 1, 1, 0, act=ACT_RELU, src=len(L) - 1, res=block_in))
+            block_in = len(L) - 1
             hw, cin = ohw, out
     if classifier:
-        L.append(Layer("fc", "gemm", rows=1, n=1000, k=2048))
+        L.append(_pool("avgpool", "avgpool", hw, cin, hw, 1, 0, src=block_in))
+        L.append(Layer("fc", "gemm", rows=1, n=1000, k=2048, src=len(L) - 1))
     return L
 
 
 def resnet18(image: int = 224, classifier: bool = True) -> List[Layer]:
-    """torchvision resnet18; at image=128 layer2.* is the paper's conv2_2 (256,128,1152)."""
-    L = [_conv("conv1", image, 3, 64, 7, 2, 3)]
+    """torchvision resnet18 as a dataflow graph (basic blocks: relu(conv2 +
+    identity), or relu(downsample + conv2) fused into the downsample); at
+    image=128 layer2.* is the paper's conv2_2 (256,128,1152)."""
+    L = [_conv("conv1", image, 3, 64, 7, 2, 3, act=ACT_RELU)]
     hw = (image + 6 - 7) // 2 + 1
+    L.append(_pool("maxpool", "maxpool", hw, 64, 3, 2, 1, src=0))
     hw = (hw + 2 - 3) // 2 + 1
-    cin = 64
+    cin, block_in = 64, 1
     for stage, (width, stride) in enumerate([(64, 1), (128, 2), (256, 2), (512, 2)], start=1):
         for b in range(2):
             s = stride if b == 0 else 1
             p = f"layer{stage}.{b}"
-            L.append(_conv(p + ".conv1", hw, cin, width, 3, s, 1))
+            L.append(_conv(p + ".conv1", hw, cin, width, 3, s, 1, act=ACT_RELU, src=block_in))
             ohw = (hw + 2 - 3) // s + 1
-            L.append(_conv(p + ".conv2", ohw, width, width, 3, 1, 1))
             if b == 0 and (s != 1 or cin != width):
-                L.append(_conv(p + ".downsample", hw, cin, width, 1, s, 0))
+                L.append(_conv(p + ".conv2", ohw, width, width, 3, 1, 1, src=len(L) - 1))
+                L.append(_conv(p + ".downsample", hw, cin, width, 1, s, 0, act=ACT_RELU, src=block_in,
+                               res=len(L) - 1))
+            else:
+                L.append(_conv(p + ".conv2", ohw, width, width, 3, 1, 1, act=ACT_RELU, src=len(L) - 1,
+                               res=block_in))
+            block_in = len(L) - 1
             hw, cin = ohw, width
     if classifier:
-        L.append(Layer("fc", "gemm", rows=1, n=1000, k=512))
+        L.append(_pool("avgpool", "avgpool", hw, cin, hw, 1, 0, src=block_in))
+        L.append(Layer("fc", "gemm", rows=1, n=1000, k=512, src=len(L) - 1))
     return L
 
 
 def vgg16(image: int = 224, classifier: bool = True) -> List[Layer]:
-    """torchvision vgg16 (13 convs 3x3 p1 + 3 fc)."""
+    """torchvision vgg16: 13 convs 3x3 p1 + relu, 2x2 max pools, 3 fc (relu on
+    the first two; the flatten reads pool5's NHWC output, adaptive avgpool is
+    the identity at 224)."""
     cfg = [64, 64, "M", 128, 128, "M", 256, 256, 256, "M", 512, 512, 512, "M", 512, 512, 512, "M"]
     L, hw, cin, i = [], image, 3, 0
     for v in cfg:
+        src = len(L) - 1 if L else None
         if v == "M":
+            L.append(_pool(f"pool{len([x for x in L if x.kind == 'maxpool']) + 1}", "maxpool", hw, cin, 2, 2, 0, src))
             hw //= 2
             continue
-        L.append(_conv(f"features.{i}", hw, cin, v, 3, 1, 1))
+        L.append(_conv(f"features.{i}", hw, cin, v, 3, 1, 1, act=ACT_RELU, src=src))
         cin, i = v, i + 1
     if classifier:
-        L += [Layer("classifier.0", "gemm", rows=1, n=4096, k=512 * 7 * 7),
-              Layer("classifier.3", "gemm", rows=1, n=4096, k=4096),
-              Layer("classifier.6", "gemm", rows=1, n=1000, k=4096)]
+        L += [Layer("classifier.0", "gemm", rows=1, n=4096, k=512 * hw * hw, act=ACT_RELU, src=len(L) - 1),
+              Layer("classifier.3", "gemm", rows=1, n=4096, k=4096, act=ACT_RELU, src=len(L)),
+              Layer("classifier.6", "gemm", rows=1, n=1000, k=4096, src=len(L) + 1)]
     return L
 
 
 def mobilenet_v2(image: int = 224, classifier: bool = True) -> List[Layer]:
-    """torchvision mobilenet_v2 (width 1.0); depthwise 3x3 convs are ``dwconv``."""
-    L = [_conv("features.0", image, 3, 32, 3, 2, 1)]
+    """torchvision mobilenet_v2 (width 1.0) as a dataflow graph: inverted
+    residuals (expand 1x1 + relu6, depthwise 3x3 ``dwconv`` + relu6, linear
+    project 1x1, + input when stride 1 and in == out channels), features.18
+    1x1 + relu6, global avgpool, classifier."""
+    L = [_conv("features.0", image, 3, 32, 3, 2, 1, act=ACT_RELU6)]
     hw = (image + 2 - 3) // 2 + 1
-    cin = 32
+    cin, block_in = 32, 0
     settings = [(1, 16, 1, 1), (6, 24, 2, 2), (6, 32, 3, 2), (6, 64, 4, 2), (6, 96, 3, 1), (6, 160, 3, 2),
                 (6, 320, 1, 1)]
     idx = 1
@@ -189,27 +242,41 @@ def mobilenet_v2(image: int = 224, classifier: bool = True) -> List[Layer]:
             stride = s if b == 0 else 1
             hidden = cin * t
             p = f"features.{idx}"
+            src = block_in
             if t != 1:
-                L.append(_conv(p + ".expand", hw, cin, hidden, 1, 1, 0))
-            L.append(Layer(p + ".dw", "dwconv", ConvSpec(hw, hw, 3, 3, hidden, hidden, stride, 1)))
-            hw = (hw + 2 - 3) // stride + 1
-            L.append(_conv(p + ".project", hw, hidden, c, 1, 1, 0))
-            cin, idx = c, idx + 1
-    L.append(_conv("features.18", hw, cin, 1280, 1, 1, 0))
+                L.append(_conv(p + ".expand", hw, cin, hidden, 1, 1, 0, act=ACT_RELU6, src=src))
+                src = len(L) - 1
+            L.append(Layer(p + ".dw", "dwconv", ConvSpec(hw, hw, 3, 3, hidden, hidden, stride, 1), act=ACT_RELU6,
+                           src=src))
+            ohw = (hw + 2 - 3) // stride + 1
+            residual = block_in if stride == 1 and cin == c else None
+            L.append(_conv(p + ".project", ohw, hidden, c, 1, 1, 0, src=len(L) - 1, res=residual))
+            block_in = len(L) - 1
+            hw, cin, idx = ohw, c, idx + 1
+    L.append(_conv("features.18", hw, cin, 1280, 1, 1, 0, act=ACT_RELU6, src=block_in))
     if classifier:
-        L.append(Layer("classifier.1", "gemm", rows=1, n=1000, k=1280))
+        L.append(_pool("avgpool", "avgpool", hw, 1280, hw, 1, 0, src=len(L) - 1))
+        L.append(Layer("classifier.1", "gemm", rows=1, n=1000, k=1280, src=len(L) - 1))
     return L
 
 
 def bert_base_gemms(seq_len: int = 128, layers: int = 1) -> List[Layer]:
-    """BERT-base projection/FFN GEMMs per encoder layer (hidden 768, FFN 3072)."""
+    """BERT-base projection/FFN GEMMs per encoder layer (hidden 768, FFN 3072)
+    as a chain: qkv; attn_out reads the V third of qkv's output (the attention
+    core softmax(QK^T)V and LayerNorm are not GEMM-shaped tenant operators and
+    are out of scope) and adds the layer input; ffn1 + GELU; ffn2 adds
+    attn_out's output; the next layer reads ffn2."""
     out = []
+    layer_in = None
     for i in range(layers):
         p = f"encoder.{i}"
-        out += [Layer(p + ".qkv", "gemm", rows=seq_len, n=2304, k=768),
-                Layer(p + ".attn_out", "gemm", rows=seq_len, n=768, k=768),
-                Layer(p + ".ffn1", "gemm", rows=seq_len, n=3072, k=768),
-                Layer(p + ".ffn2", "gemm", rows=seq_len, n=768, k=3072)]
+        base = len(out)
+        out += [Layer(p + ".qkv", "gemm", rows=seq_len, n=2304, k=768, src=layer_in),
+                Layer(p + ".attn_out", "gemm", rows=seq_len, n=768, k=768, src=base, src_col=1536,
+                      res=layer_in),
+                Layer(p + ".ffn1", "gemm", rows=seq_len, n=3072, k=768, act=ACT_GELU, src=base + 1),
+                Layer(p + ".ffn2", "gemm", rows=seq_len, n=768, k=3072, src=base + 2, res=base + 1)]
+        layer_in = base + 3
     return out
 
 
@@ -240,6 +307,31 @@ def table1_flops(preset: str) -> int:
         return conv2_2()[0].flops(1)
     s = find_preset(preset).layers[0]
     return 2 * s.m * s.n * s.k
+
+
+def graph_json(layers: List[Layer]) -> List[dict]:
+    """The layer graph as plain data (oracle/graphs/*.json: the form the CPU
+    baseline and the reference arm read without importing this package)."""
+    out = []
+    for L in layers:
+        c = L.conv
+        out.append({"name": L.name, "kind": L.kind,
+                    "conv": None if c is None else [c.image_h, c.image_w, c.kernel_h, c.kernel_w, c.in_channels,
+                                                    c.out_channels, c.stride, c.padding],
+                    "rows": L.rows, "n": L.n, "k": L.k, "act": L.act, "src": L.src, "res": L.res,
+                    "src_col": L.src_col})
+    return out
+
+
+# graphs exported to oracle/graphs (tools/export_graphs.py; pinned by tests/test_workload.py)
+EXPORTED_GRAPHS = {
+    "resnet50_224": lambda: resnet50(224),
+    "vgg16_224": lambda: vgg16(224),
+    "mobilenet_v2_224": lambda: mobilenet_v2(224),
+    "bert_base_12": lambda: bert_base_gemms(128, layers=12),
+    "resnet18_128": lambda: resnet18(128, classifier=False),
+    "conv2_2": lambda: conv2_2(),
+}
 
 
 MODELS = {

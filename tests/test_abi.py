@@ -28,7 +28,7 @@ def test_ctypes_signatures_cover_the_header():
 
 def test_abi_version_and_host_only_context():
     lib = _native.lib()
-    assert lib.gm_abi_version() == 1
+    assert lib.gm_abi_version() == 2
     h = ctypes.c_void_p()
     assert lib.gm_create(None, None, None, -1, ctypes.byref(h)) == 0  # host-only: planner without a GPU
     q = ctypes.c_void_p()

@@ -196,17 +196,17 @@ def small_engine(tenants=3, batch=2, image=64, options=None):
     return SpaceTimeEngine([W.resnet18(image)] * tenants, [batch] * tenants, options=options or {})
 
 
-def check_engine(eng, oracle):
-    for m in eng.models:
-        for L, buf in zip(m.layers, m.buffers):
-            err = rel_err(buf, expect(oracle, buf))
-            assert err <= TOL, f"{L.name}: {err:.3e}"
+def check_engine(eng, oracle=None):
+    """Every layer of every tenant (dataflow graphs: each layer on the device's
+    own input, i.e. its producer's output) against the oracle, every row."""
+    import oracle_check
+    for i, m in enumerate(eng.models):
+        oracle_check.check_model(m, names=f"tenant {i}", sample=False)
 
 
 def clear(eng):
-    for m in eng.models:
-        for buf in m.buffers:
-            buf.y.fill_(float("nan"))
+    import oracle_check
+    oracle_check.poison(eng.models)
 
 
 def test_round_program_matches_oracle(oracle):
@@ -282,16 +282,73 @@ def test_execution_options_keep_results(oracle, options):
 
 
 def test_serve_round_e2e_host_buffers(oracle):
+    """The gated e2e program (per-tenant H2D opens that tenant's chain): the
+    host results are the dataflow chain of the host inputs."""
     eng = small_engine(tenants=2)
     s = torch.cuda.Stream()
     h_in = [m.query_input.cpu().pin_memory() for m in eng.models]
     h_out = [torch.empty_like(m.query_output, device="cpu").pin_memory() for m in eng.models]
+    clear(eng)
     for _ in range(3):
         rnd = eng.serve_round(h_in, h_out, s)
     assert len(eng._graphs) == 1  # steady state: one cached launch program
     for m, h in zip(eng.models, h_out):
         assert torch.equal(h, m.query_output.cpu())
     check_engine(eng, oracle)
+    # a new host batch through the cached program: new results, still the oracle's
+    first = [h.clone() for h in h_out]
+    g = torch.Generator().manual_seed(7)
+    for h in h_in:
+        h.copy_((torch.rand(h.shape, generator=g) * 2 - 1).to(h.dtype))
+    clear(eng)
+    eng.serve_round(h_in, h_out, s)
+    assert len(eng._graphs) == 1
+    for a, b, m, hi in zip(first, h_out, eng.models, h_in):
+        assert not torch.equal(a, b)
+        assert torch.equal(m.query_input.cpu(), hi)
+    check_engine(eng, oracle)
+
+
+def test_round_dependency_graph():
+    """Device tile table edges (gm_round_tile_info): every tile of a tenant's
+    layer l > 0 waits on the counter its layer l-1 tiles publish to, no tile
+    waits on its own counter, and the counters a tile waits on are published."""
+    from paper_1901_00041_b200 import workload as W
+    from paper_1901_00041_b200.engine import SpaceTimeEngine
+    eng = SpaceTimeEngine([W.resnet18(64), W.mobilenet_v2(64, classifier=False)], [2, 2])
+    rnd = eng.plan_round()
+    info = rnd.tile_info()
+    done = {}
+    for t in info:
+        done.setdefault((t["tenant"], t["layer"]), set()).add(t["done"])
+    for t in info:
+        assert t["dep"] < 0 or t["dep"] != t["done"]
+        if t["layer"] == 0:
+            assert t["dep"] == -1
+        else:
+            prev = done[(t["tenant"], t["layer"] - 1)]
+            assert prev == {t["dep"]}, (t, prev)
+    last = {(tn, max(l for (tt, l) in done if tt == tn)) for tn, _ in done}
+    for key, d in done.items():
+        assert (d == {-1}) == (key in last)  # only the chain tails skip the publish
+
+
+@pytest.mark.parametrize("options", [{}, {"greedy_schedule": 1}, {"dynamic_schedule": 1}, {"critical_order": 0},
+                                     {"split_k": 1, "narrow_min_tiles": 64}])
+def test_dataflow_chain_every_schedule(oracle, options):
+    """A chained ResNet-18 + MobileNet-v2 round (layer l reads layer l-1's
+    output, residual adds read earlier layers) under every tile schedule,
+    outputs poisoned first: results depend on dependency order."""
+    from paper_1901_00041_b200 import workload as W
+    from paper_1901_00041_b200.engine import SpaceTimeEngine
+    eng = SpaceTimeEngine([W.resnet18(64), W.mobilenet_v2(64)], [2, 3], options=options)
+    rnd = eng.plan_round()
+    s = torch.cuda.Stream()
+    for launch in (lambda: rnd.launch_round(s.cuda_stream), lambda: rnd.launch(s.cuda_stream)):
+        clear(eng)
+        launch()
+        torch.cuda.synchronize()
+        check_engine(eng, oracle)
 
 
 def test_serve_rounds_pipelined_matches_single_rounds():

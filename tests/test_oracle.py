@@ -141,3 +141,66 @@ def test_planner_oracle_pinned_to_reference_cost_goldens():
         except ValueError as e:
             got = {"error": str(e)}
         assert got == case["output"]
+
+
+# ------------------------------------------------------------------ dataflow operators
+
+def _torch_act(y, act):
+    if act == 1:
+        return torch.relu(y)
+    if act == 2:
+        return torch.clamp(y, 0.0, 6.0)
+    if act == 3:
+        return torch.nn.functional.gelu(y)  # erf form
+    return y
+
+
+@pytest.mark.parametrize("act", [0, 1, 2, 3])
+@pytest.mark.parametrize("with_res,with_rows", [(False, False), (True, False), (True, True)])
+def test_oracle_ex_ops_match_torch(act, with_res, with_rows):
+    """conv / GEMM with fused residual add and activation, depthwise, pools,
+    and row sampling (oracle_check.expect) == torch float64 on CPU."""
+    import oracle_check
+    from paper_1901_00041_b200.runtime import LayerBuffers
+    from paper_1901_00041_b200.scheduler import ConvSpec, GemmShape
+    g = torch.Generator().manual_seed(act * 7 + with_res)
+    b, hw, cin, cout = 2, 9, 16, 24
+    x = (torch.rand(b, hw, hw, cin, generator=g) * 2 - 1).to(torch.bfloat16)
+    w = (torch.randn(cout, 3 * 3 * cin, generator=g) * 0.2).to(torch.bfloat16)
+    M = b * 5 * 5  # 3x3 s2 p1: 9 -> 5
+    res = (torch.rand(M, cout, generator=g) * 2 - 1).to(torch.bfloat16) if with_res else None
+    buf = LayerBuffers("conv", x, w, torch.empty(M, cout, dtype=torch.bfloat16),
+                       conv=ConvSpec(hw, hw, 3, 3, cin, cout, 2, 1), batch=b, act=act, res=res)
+    rows = np.array([0, 7, 13, M - 1], dtype=np.int64) if with_rows else None
+    got = oracle_check.expect(buf, rows)
+    ref = torch.nn.functional.conv2d(x.double().permute(0, 3, 1, 2), w.double().reshape(cout, 3, 3, cin)
+                                     .permute(0, 3, 1, 2), stride=2, padding=1).permute(0, 2, 3, 1).reshape(M, cout)
+    if res is not None:
+        ref = ref + res.double()
+    ref = _torch_act(ref, act).numpy()
+    if rows is not None:
+        ref = ref[rows]
+    np.testing.assert_allclose(got, ref, rtol=1e-5, atol=1e-5)
+    # GEMM with a strided (column-slice) input, like BERT's attn_out reading V
+    a = (torch.rand(10, 48, generator=g) * 2 - 1).to(torch.bfloat16)[:, 16:40]
+    wb = (torch.randn(8, 24, generator=g) * 0.3).to(torch.bfloat16)
+    r2 = (torch.rand(10, 8, generator=g) * 2 - 1).to(torch.bfloat16) if with_res else None
+    gb = LayerBuffers("gemm", a, wb, torch.empty(10, 8, dtype=torch.bfloat16), gemm=GemmShape(10, 8, 24), act=act,
+                      res=r2)
+    ref2 = a.double() @ wb.double().T + (r2.double() if r2 is not None else 0)
+    np.testing.assert_allclose(oracle_check.expect(gb), _torch_act(ref2, act).numpy(), rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("kind,r,stride,pad", [("maxpool", 3, 2, 1), ("maxpool", 2, 2, 0), ("avgpool", 7, 1, 0)])
+def test_oracle_pools_match_torch(kind, r, stride, pad):
+    import oracle_check
+    from paper_1901_00041_b200.runtime import LayerBuffers
+    from paper_1901_00041_b200.scheduler import ConvSpec
+    hw = 7 if kind == "avgpool" else 12
+    x = (torch.randn(2, hw, hw, 8) * 3).to(torch.bfloat16)
+    P = (hw + 2 * pad - r) // stride + 1
+    buf = LayerBuffers(kind, x, None, None, conv=ConvSpec(hw, hw, r, r, 8, 8, stride, pad), batch=2)
+    xt = x.double().permute(0, 3, 1, 2)
+    f = torch.nn.functional.max_pool2d if kind == "maxpool" else torch.nn.functional.avg_pool2d
+    ref = f(xt, r, stride, pad).permute(0, 2, 3, 1).reshape(2 * P * P, 8).numpy()
+    np.testing.assert_allclose(oracle_check.expect(buf), ref, rtol=1e-6, atol=1e-6)
