@@ -468,9 +468,9 @@ def run_ours(args):
             "planner_tiles_per_round": sum(k.planned_cost.blocks for k in rnd.kernels),
             "tiles_executed_per_round": len(tile_info),
             "executed_tile_variants": {"tall_256_rows": sum(t["rows"] == 256 for t in tile_info),
-                                       "narrow_n": sum(t["cols"] < 256 and t["rows"] != 32 for t in tile_info),
+                                       "narrow_n": sum(t["cols"] < 256 and not t["cuda_core"] for t in tile_info),
                                        "split_k": sum(t["splits"] > 1 for t in tile_info),
-                                       "cuda_core": sum(t["rows"] == 32 for t in tile_info)},
+                                       "cuda_core": sum(t["cuda_core"] for t in tile_info)},
             "l2": f"inputs larger than L2 ({bytes_round / 1e6:.0f} MB compulsory/round)",
         },
         "modes": {

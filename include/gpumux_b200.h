@@ -461,6 +461,8 @@ typedef struct gm_round_tile {
   int32_t splits, kb_begin, kb_end; /* split-K slice (splits 1: the whole K, kb_end 0) */
   int32_t done, dep;
   int32_t plan;                     /* index of the formed super-kernel it came from */
+  int32_t cuda_core;                /* 1: depthwise / pool tile computed on CUDA cores */
+  int32_t reserved0;
 } gm_round_tile;
 int gm_round_tile_info(gm_ctx* ctx, const gm_plans* p, gm_round_tile* out, size_t cap, size_t* n);
 /* End-to-end round program (the serving call with host buffers): per tenant

@@ -61,6 +61,8 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 bool cuda_core_kind(int kind) {
   return kind == GM_LAYER_DWCONV || kind == GM_LAYER_MAXPOOL || kind == GM_LAYER_AVGPOOL;
 }
+// Output rows per tile of a CUDA-core operator.
+int64_t cuda_core_rows(int kind) { return kind == GM_LAYER_DWCONV ? dev::kDwTileM : dev::kPoolTileM; }
 
 
 }  // namespace
@@ -444,7 +446,7 @@ struct Runtime {
         op.batch = L.batch < 1 ? 1 : L.batch;
         const Conv& c = op.conv;
         if (c.in_channels != c.out_channels) throw std::invalid_argument("register_tenant: pool needs Cin == Cout");
-        if (c.in_channels % 4 != 0) throw std::invalid_argument("register_tenant: pool channels must be a multiple of 4");
+        if (c.in_channels % 8 != 0) throw std::invalid_argument("register_tenant: pool channels must be a multiple of 8");
         if (!aligned16(L.x)) throw std::invalid_argument("pool input must be 16-byte aligned");
         if (L.res) throw std::invalid_argument("register_tenant: pools take no residual");
         const int64_t P = (c.image_h + 2 * c.padding - c.kernel_h) / c.stride + 1;
@@ -517,7 +519,7 @@ struct Runtime {
         throw std::invalid_argument("register_tenant: unknown layer kind");
       }
       if (op.shape.n % 8 != 0) throw std::invalid_argument("register_tenant: output channels must be a multiple of 8");
-      if (op.shape.m > int64_t(0xFFFF) * (cuda_core_kind(op.kind) ? dev::kDwTileM : dev::kBM) ||
+      if (op.shape.m > int64_t(0xFFFF) * (cuda_core_kind(op.kind) ? cuda_core_rows(op.kind) : dev::kBM) ||
           op.shape.m > INT32_MAX)
         throw std::invalid_argument("register_tenant: M too large for the tile table");
       store_map(&md.c, L.y, op.shape.m, op.shape.n);
@@ -537,6 +539,17 @@ struct Runtime {
           throw std::invalid_argument("register_tenant: residual rows must be 16-byte aligned (ldr % 8 == 0, ldr >= N)");
         md.res = static_cast<const __nv_bfloat16*>(L.res);
         md.ldr = static_cast<int32_t>(ldr);
+        {
+          const cuuint64_t dims[2] = {static_cast<cuuint64_t>(op.shape.n), static_cast<cuuint64_t>(op.shape.m)};
+          const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldr * 2)};
+          const cuuint32_t box[2] = {64, 128};
+          const cuuint32_t estr[2] = {1, 1};
+          const CUresult r = encode_tiled(&md.r, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(L.res), dims,
+                                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+          if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled(residual) failed (" + std::to_string(int(r)) + ")");
+        }
       }
       op.y = static_cast<const char*>(L.y);
       op.y_bytes = op.shape.m * op.shape.n * 2;
@@ -676,7 +689,7 @@ struct Runtime {
     for (int f : members) {
       const Operator& op = flat[f];
       const auto [slot, w] = variant(f, plan_tiles, plan_tiles);
-      const int64_t tm = cuda_core_kind(op.kind) ? dev::kDwTileM : dev::kBM << (is_tall(slot) ? 1 : 0);
+      const int64_t tm = cuda_core_kind(op.kind) ? cuda_core_rows(op.kind) : dev::kBM << (is_tall(slot) ? 1 : 0);
       const int64_t mt = (op.shape.m + tm - 1) / tm;
       const int64_t nt = (op.shape.n + w - 1) / w;
       for (int64_t a = 0; a < mt; ++a)
@@ -750,7 +763,7 @@ struct Runtime {
         const int inst = static_cast<int>(targets.size());
         if (dep == inst) throw std::logic_error("round program: member instance waits on its own counter");
         last_instance[f] = inst;
-        const int64_t tm = cuda_core_kind(op.kind) ? dev::kDwTileM : dev::kBM << (tall ? 1 : 0);
+        const int64_t tm = cuda_core_kind(op.kind) ? cuda_core_rows(op.kind) : dev::kBM << (tall ? 1 : 0);
         const int64_t mt = (op.shape.m + tm - 1) / tm;
         const int64_t nt = (op.shape.n + w - 1) / w;
         const int kb = static_cast<int>((op.shape.k + dev::kBK - 1) / dev::kBK);
@@ -1500,7 +1513,9 @@ int gm_round_tile_info(gm_ctx* ctx, const gm_plans* p, gm_round_tile* out, size_
     o.layer = op.layer;
     o.m_tile = te.m_tile;
     o.n_tile = te.n_tile;
-    o.rows = dev::cuda_core_mode(md.a_mode) ? dev::kDwTileM : (md.tall ? 2 * dev::kBM : dev::kBM);
+    o.rows = md.a_mode == dev::kDepthwise ? dev::kDwTileM
+             : dev::cuda_core_mode(md.a_mode) ? dev::kPoolTileM
+                                              : (md.tall ? 2 * dev::kBM : dev::kBM);
     o.cols = dev::cuda_core_mode(md.a_mode) ? dev::kDwTileC : md.n_tile;
     o.splits = te.splits > 1 ? te.splits : 1;
     o.kb_begin = te.kb_begin;
@@ -1508,6 +1523,8 @@ int gm_round_tile_info(gm_ctx* ctx, const gm_plans* p, gm_round_tile* out, size_
     o.done = te.done;
     o.dep = te.dep;
     o.plan = pr.tile_plan[i];
+    o.cuda_core = dev::cuda_core_mode(md.a_mode) ? 1 : 0;
+    o.reserved0 = 0;
   }
   GM_API_END
 }

@@ -101,6 +101,7 @@ struct alignas(128) MemberDesc {
   CUtensorMap a;        // A operand: [M, K] tiled, or NHWC im2col
   CUtensorMap b;        // B operand: weights [N, K], K-major
   CUtensorMap c;        // output [M, N] row-major, store box 32 x 32
+  CUtensorMap r;        // residual [M, N] (row stride ldr), box 64 x 128: L2 prefetch only
   int32_t m, n;
   int32_t k_blocks;     // ceil(K / kBK)
   uint32_t idesc;       // tcgen05 instruction descriptor (N = B box rows)
@@ -272,6 +273,14 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
                "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+
+// Bulk L2 prefetch of one tensor box (no smem destination, no completion).
+__device__ __forceinline__ void prefetch_box_l2(const CUtensorMap* map, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
                : "memory");
 }
 
@@ -448,62 +457,92 @@ __device__ __forceinline__ void depthwise_tile(const MemberDesc* __restrict__ md
   }
 }
 
-// Pool tile (CUDA cores): max or average over an R x S window, same lane
-// mapping as the depthwise tile (epilogue warp `ew` owns kDwPixW output pixels,
-// each lane 4 channels: one 8-byte load per tap and pixel).  Max pooling skips
-// padded taps (torch MaxPool2d); average pooling divides by R*S (the global
-// pools it serves have no padding).
+// Pool tile (CUDA cores): max or average over an R x S window, kPoolTileM
+// output pixels x kDwTileC channels.  Each lane owns 8 channels (16-byte
+// loads); a warp pass covers 32 / (channel groups) pixels, spread over the 8
+// epilogue warps first (a global pool's few pixels still use every warp).
+// Two pixels per lane are processed together with up to 9 taps each
+// unrolled, so 18 independent loads are in flight per lane: the op is
+// load-latency bound.  Max pooling skips padded taps (torch MaxPool2d, via a
+// -inf fill); average pooling divides by R*S (the global pools it serves have
+// no padding).
+constexpr int kPoolTileM = 128;
+constexpr int kPoolTapChunk = 9;
+
 __device__ __forceinline__ void pool_tile(const MemberDesc* __restrict__ md, const TileEntry& te, int ew, int lane) {
   const int M = md->m, C = md->ch, H = md->h_in, W = md->w_in;
   const int cbase = te.n_tile * kDwTileC;
-  const int g = min(kDwTileC, C - cbase) >> 2;
-  const int gp = g <= 8 ? 8 : (g <= 16 ? 16 : 32);
-  const int pp = 32 / gp;
+  const int g = min(kDwTileC, C - cbase) >> 3;  // 8-channel groups in this tile
+  const int gp = g <= 4 ? 4 : (g <= 8 ? 8 : 16);
+  const int pp = 32 / gp;  // pixels per warp pass
   const int cg = lane & (gp - 1), sub = lane / gp;
   if (cg >= g) return;
-  const int c = cbase + cg * 4;
-  const int R = md->r_taps / md->s_taps, S = md->s_taps, st = md->stride, pad = md->pad, PQ = md->pq, Q = md->q;
+  const int c = cbase + cg * 8;
+  const int taps = md->r_taps, S = md->s_taps, st = md->stride, pad = md->pad, PQ = md->pq, Q = md->q;
   const bool mx = md->a_mode == kMaxPool;
-  const float init = mx ? -INFINITY : 0.f;
-  const float scale = mx ? 1.f : 1.f / static_cast<float>(R * S);
-  const int m_base = te.m_tile * kDwTileM + ew * kDwPixW + sub;
-  const int npx = (kDwPixW + pp - 1) / pp;
-  for (int i = 0; i < npx; ++i) {
-    const int m = m_base + pp * i;
-    if (m >= M) break;
-    const int b = m / PQ;
-    const int rem = m - b * PQ;
-    const int p = rem / Q;
-    const int h0 = p * st - pad, w0 = (rem - p * Q) * st - pad;
-    float a0 = init, a1 = init, a2 = init, a3 = init;
-    for (int r = 0; r < R; ++r) {
-      const int ih = h0 + r;
-      if (ih < 0 || ih >= H) continue;
-      const __nv_bfloat16* row = md->dx + (static_cast<int64_t>(b) * H + ih) * W * C + c;
-#pragma unroll 4
-      for (int s = 0; s < S; ++s) {
-        const int iw = w0 + s;
-        if (iw < 0 || iw >= W) continue;
-        const uint2 raw = __ldcg(reinterpret_cast<const uint2*>(row + static_cast<int64_t>(iw) * C));
-        const __nv_bfloat162 x01 = *reinterpret_cast<const __nv_bfloat162*>(&raw.x);
-        const __nv_bfloat162 x23 = *reinterpret_cast<const __nv_bfloat162*>(&raw.y);
-        if (mx) {
-          a0 = fmaxf(a0, __low2float(x01));
-          a1 = fmaxf(a1, __high2float(x01));
-          a2 = fmaxf(a2, __low2float(x23));
-          a3 = fmaxf(a3, __high2float(x23));
-        } else {
-          a0 += __low2float(x01);
-          a1 += __high2float(x01);
-          a2 += __low2float(x23);
-          a3 += __high2float(x23);
+  const uint32_t fill = mx ? 0xFF80FF80u : 0u;  // bf16x2 -inf (max) or 0 (sum)
+  const float scale = mx ? 1.f : 1.f / static_cast<float>(taps);
+  const int passes = kPoolTileM / (8 * pp);
+  for (int ps = 0; ps < passes; ps += 2) {
+    int mm[2], bb[2], hh[2], ww[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      mm[j] = te.m_tile * kPoolTileM + ((ps + j) * 8 + ew) * pp + sub;
+      const bool ok = ps + j < passes && mm[j] < M;
+      bb[j] = ok ? mm[j] / PQ : -1;
+      const int rem = mm[j] - bb[j] * PQ;
+      const int p = rem / Q;
+      hh[j] = p * st - pad;
+      ww[j] = (rem - p * Q) * st - pad;
+    }
+    if (bb[0] < 0 && bb[1] < 0) break;
+    float acc[2][8];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[j][e] = mx ? -INFINITY : 0.f;
+    for (int t0 = 0; t0 < taps; t0 += kPoolTapChunk) {
+      uint4 raw[2][kPoolTapChunk];
+#pragma unroll
+      for (int k = 0; k < kPoolTapChunk; ++k) {
+        const int tap = t0 + k;
+        const int r = tap / S, s = tap - (tap / S) * S;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int ih = hh[j] + r, iw = ww[j] + s;
+          raw[j][k] = make_uint4(fill, fill, fill, fill);
+          if (tap < taps && bb[j] >= 0 && ih >= 0 && ih < H && iw >= 0 && iw < W)
+            raw[j][k] = __ldcg(reinterpret_cast<const uint4*>(md->dx + ((static_cast<int64_t>(bb[j]) * H + ih) * W + iw) * C + c));
         }
       }
+#pragma unroll
+      for (int k = 0; k < kPoolTapChunk; ++k)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const uint32_t w4[4] = {raw[j][k].x, raw[j][k].y, raw[j][k].z, raw[j][k].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(&w4[e]);
+            if (mx) {
+              acc[j][2 * e] = fmaxf(acc[j][2 * e], __low2float(v));
+              acc[j][2 * e + 1] = fmaxf(acc[j][2 * e + 1], __high2float(v));
+            } else {
+              acc[j][2 * e] += __low2float(v);
+              acc[j][2 * e + 1] += __high2float(v);
+            }
+          }
+        }
     }
-    uint2 o;
-    o.x = pack_bf16(__float_as_uint(a0 * scale), __float_as_uint(a1 * scale), md->act);
-    o.y = pack_bf16(__float_as_uint(a2 * scale), __float_as_uint(a3 * scale), md->act);
-    *reinterpret_cast<uint2*>(md->dy + static_cast<int64_t>(m) * C + c) = o;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (bb[j] < 0) continue;
+      uint4 o;
+      o.x = pack_bf16(__float_as_uint(acc[j][0] * scale), __float_as_uint(acc[j][1] * scale), md->act);
+      o.y = pack_bf16(__float_as_uint(acc[j][2] * scale), __float_as_uint(acc[j][3] * scale), md->act);
+      o.z = pack_bf16(__float_as_uint(acc[j][4] * scale), __float_as_uint(acc[j][5] * scale), md->act);
+      o.w = pack_bf16(__float_as_uint(acc[j][6] * scale), __float_as_uint(acc[j][7] * scale), md->act);
+      *reinterpret_cast<uint4*>(md->dy + static_cast<int64_t>(mm[j]) * C + c) = o;
+    }
   }
 }
 
@@ -707,6 +746,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int taps = md->taps, images = md->images;
         const CUtensorMap* amap = &md->a;
+        if (md->res) {
+          // the epilogue adds this tile's residual rows several tiles from
+          // now: pull them into L2 while the operands stream
+          const int rcols = min(md->n_tile, md->n - n0);
+          for (int cc = 0; cc < rcols; cc += 64) {
+            prefetch_box_l2(&md->r, n0 + cc, m0);
+            if (tall) prefetch_box_l2(&md->r, n0 + cc, m0 + kBM);
+          }
+        }
         auto load_a = [&](int kb, uint32_t st) {
           uint8_t* a_dst = ring + st * sbytes;
           if (fold) {
@@ -1126,22 +1174,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++issued;
         buf ^= 1;
       };
-      // 32 fp32 accumulators of this lane's row -> bf16 -> one 32x32 store box.
-      auto store_bf16 = [&](uint32_t (&v)[32], int c, int mrow) {
+      // Residual of this lane's row, 32 columns from column c: four 16-byte
+      // loads (each lane reads whole 32-byte sectors), zero past the M / N
+      // edges.  Loaded one chunk ahead of its use (and the first chunk before
+      // the accumulator wait), so a chunk's load latency overlaps the
+      // previous chunk's drain; the producer pulled the tile's rows into L2.
+      auto load_res = [&](uint4 (&rv)[4], int c, int mrow) {
+        const int m = mrow + lane;
+        const bool ok = res && m < m_real && c < cols;
+        const __nv_bfloat16* rrow = res + static_cast<int64_t>(ok ? m : 0) * ldr + n0 + c;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          rv[j] = ok && n0 + c + 8 * j < n_real ? __ldcg(reinterpret_cast<const uint4*>(rrow + 8 * j))
+                                                : make_uint4(0u, 0u, 0u, 0u);
+      };
+      // 32 fp32 accumulators of this lane's row (+ residual) -> bf16 -> one
+      // 32x32 store box.
+      auto store_bf16 = [&](uint32_t (&v)[32], int c, int mrow, const uint4 (&rv)[4]) {
         if (res) {
-          // this lane's row, 32 columns: four 16-byte loads (each lane reads
-          // whole 32-byte sectors), clipped at the M / N edges
-          const int m = mrow + lane;
-          if (m < m_real) {
-            const __nv_bfloat16* rrow = res + static_cast<int64_t>(m) * ldr + n0 + c;
-            uint4 rv[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-              rv[j] = n0 + c + 8 * j < n_real ? __ldcg(reinterpret_cast<const uint4*>(rrow + 8 * j))
-                                              : make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) add_residual8(v + 8 * j, rv[j]);
-          }
+          for (int j = 0; j < 4; ++j) add_residual8(v + 8 * j, rv[j]);
         }
         uint8_t* sbuf = claim();
         uint8_t* row = sbuf + lane * 64;
@@ -1162,6 +1214,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         issue();
       };
+      uint4 rcur[4], rnxt[4];
+      if (res && te.splits <= 1) load_res(rcur, 0, m0);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       if (trace && quarter == 0 && lane == 0) trace[6 * t + 4] = globaltimer();
@@ -1211,7 +1265,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + f.w);
               __stcg(src + j * 32, make_float4(0.f, 0.f, 0.f, 0.f));
             }
-            if (m0 < md->m) store_bf16(v, c, m0);
+            if (m0 < md->m) {
+              load_res(rcur, c, m0);
+              store_bf16(v, c, m0, rcur);
+            }
           }
           tc_fence_before();
           mbar_arrive(&acc_empty[acc]);
@@ -1223,14 +1280,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c = 0; c < cols; c += kEpiChunk) {
             uint32_t v[32];
             tmem_ld32(taddr + c, v);
-            store_bf16(v, c, m0);
+            if (res && (c + kEpiChunk < cols || tall))
+              load_res(rnxt, c + kEpiChunk < cols ? c + kEpiChunk : 0, c + kEpiChunk < cols ? m0 : m0 + kBM);
+            store_bf16(v, c, m0, rcur);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) rcur[j] = rnxt[j];
           }
         }
         if (tall && m0 + kBM < md->m) {  // tall tile: the second 128-row half
           for (int c = 0; c < cols; c += kEpiChunk) {
             uint32_t v[32];
             tmem_ld32(taddr + md->n_tile + c, v);
-            store_bf16(v, c, m0 + kBM);
+            if (res && c + kEpiChunk < cols) load_res(rnxt, c + kEpiChunk, m0 + kBM);
+            store_bf16(v, c, m0 + kBM, rcur);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) rcur[j] = rnxt[j];
           }
         }
         tc_fence_before();

@@ -57,8 +57,8 @@ def check(model, name, full, extra, seed):
 def variants(rnd):
     info = rnd.tile_info()
     return {"tiles": len(info), "tall": sum(t["rows"] == 256 for t in info),
-            "narrow": sum(t["cols"] < 256 and t["rows"] != 32 for t in info),
-            "split": sum(t["splits"] > 1 for t in info), "cuda_core": sum(t["rows"] == 32 for t in info)}
+            "narrow": sum(t["cols"] < 256 and not t["cuda_core"] for t in info),
+            "split": sum(t["splits"] > 1 for t in info), "cuda_core": sum(t["cuda_core"] for t in info)}
 
 
 def assert_plan_matches_host_planner(eng, rnd, policy):
@@ -112,5 +112,5 @@ def test_mix_config_224(batch):
     info = rnd.tile_info()
     fc6 = [t for t in info if t["tenant"] == 1 and t["layer"] == len(W.vgg16(224)) - 3]
     assert fc6 and all(t["splits"] > 1 for t in fc6), "VGG fc6 should run split over K by default"
-    assert any(t["rows"] == 32 for t in info)
+    assert any(t["cuda_core"] for t in info)
     run_and_check(eng, rnd, full_tenants=(2,), extra=8)
