@@ -172,6 +172,7 @@ struct Runtime {
   int64_t tall_min_tiles = 0;     // concurrent same-shape tiles that make a member "throughput-bound" (0 = 2 x SMs)
   int bn = 256;     // N tile of the super-kernel (== DeviceSpec.tile_n)
   uint32_t* host_one = nullptr;  // pinned 4-byte 1: DMA source that opens an input gate
+  void* ident = nullptr;         // bf16 identity [kIdentN, kIdentN]: B operand of residual k-blocks
   int smem_bytes = 0;
   const void* kernel = nullptr;
 
@@ -186,6 +187,7 @@ struct Runtime {
       cudaFree(op.wpad);
     }
     cudaFree(d_desc);
+    cudaFree(ident);
     cudaFreeHost(host_one);
   }
 
@@ -218,6 +220,12 @@ struct Runtime {
                "cudaFuncSetAttribute");
     cuda_check(cudaHostAlloc(&host_one, sizeof(uint32_t), cudaHostAllocDefault), "cudaHostAlloc");
     *host_one = 1;
+    {
+      std::vector<uint16_t> eye(static_cast<size_t>(dev::kIdentN) * dev::kIdentN, 0);
+      for (int i = 0; i < dev::kIdentN; ++i) eye[static_cast<size_t>(i) * dev::kIdentN + i] = 0x3F80;  // bf16 1.0
+      cuda_check(cudaMalloc(&ident, eye.size() * 2), "cudaMalloc(identity)");
+      cuda_check(cudaMemcpy(ident, eye.data(), eye.size() * 2, cudaMemcpyHostToDevice), "upload identity");
+    }
   }
 
   // A member's k-block stage (A region + B box) fits a 32 KB narrow-layout slot.
@@ -537,19 +545,15 @@ struct Runtime {
         const int64_t ldr = L.ldr > 0 ? L.ldr : op.shape.n;
         if (ldr < op.shape.n || ldr % 8 != 0 || !aligned16(L.res))
           throw std::invalid_argument("register_tenant: residual rows must be 16-byte aligned (ldr % 8 == 0, ldr >= N)");
+        // the add runs on the tensor core as extra k-blocks (A = residual
+        // columns, B = identity): the member's A operand must be the SW128
+        // K-major layout the residual box lands in
+        if (md.a_mode != dev::kATiled && md.a_mode != dev::kAIm2col)
+          throw std::invalid_argument("register_tenant: residual add needs a tiled or im2col A operand");
         md.res = static_cast<const __nv_bfloat16*>(L.res);
         md.ldr = static_cast<int32_t>(ldr);
-        {
-          const cuuint64_t dims[2] = {static_cast<cuuint64_t>(op.shape.n), static_cast<cuuint64_t>(op.shape.m)};
-          const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldr * 2)};
-          const cuuint32_t box[2] = {64, 128};
-          const cuuint32_t estr[2] = {1, 1};
-          const CUresult r = encode_tiled(&md.r, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(L.res), dims,
-                                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-          if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled(residual) failed (" + std::to_string(int(r)) + ")");
-        }
+        tiled_map(&md.r, L.res, op.shape.m, op.shape.n, ldr, a_box_rows(op.shape.m));
+        tiled_map(&md.id, ident, dev::kIdentN, dev::kIdentN, dev::kIdentN, b_box_rows(op.shape.n, op.n_tile));
       }
       op.y = static_cast<const char*>(L.y);
       op.y_bytes = op.shape.m * op.shape.n * 2;
@@ -567,6 +571,7 @@ struct Runtime {
           dev::MemberDesc md2 = md;
           tiled_map(&md2.b, op.b_ptr, op.shape.n, op.b_k, op.b_ld, b_box_rows(op.shape.n, w));
           md2.idesc = make_idesc(b_box_rows(op.shape.n, w));
+          if (md2.res) tiled_map(&md2.id, ident, dev::kIdentN, dev::kIdentN, dev::kIdentN, b_box_rows(op.shape.n, w));
           md2.tx_bytes = static_cast<uint32_t>((a_box_rows(op.shape.m) + b_box_rows(op.shape.n, w)) * dev::kBK * 2);
           md2.n_tile = w;
           md2.ring_narrow = ring_narrow_of(md2, b_box_rows(op.shape.n, w));

@@ -34,6 +34,7 @@ namespace gmb {
 namespace dev {
 
 constexpr int kBM = 128;  // UMMA M; == b200 DeviceSpec.tile_m
+constexpr int kIdentN = 256;  // identity matrix side (the widest N tile): residual k-blocks' B operand
 constexpr int kBK = 64;   // 64 bf16 = 128 B = one SWIZZLE_128B row
 constexpr int kThreads = 384;  // 4 control warps + 2 epilogue warpgroups
 constexpr int kABytes = kBM * kBK * 2;
@@ -101,7 +102,13 @@ struct alignas(128) MemberDesc {
   CUtensorMap a;        // A operand: [M, K] tiled, or NHWC im2col
   CUtensorMap b;        // B operand: weights [N, K], K-major
   CUtensorMap c;        // output [M, N] row-major, store box 32 x 32
-  CUtensorMap r;        // residual [M, N] (row stride ldr), box 64 x 128: L2 prefetch only
+  // Fused residual add as extra k-blocks of the same MMA: y = [A | R] [W ; I]
+  // over the tile's columns.  r: the residual [M, N] as an A operand (box 64
+  // columns x A-box rows, SW128); id: a bf16 identity as the B operand (box 64
+  // x B-box rows).  ceil(cols / 64) extra k-blocks per tile add R exactly in
+  // the fp32 accumulator, streamed by TMA through the operand ring.
+  CUtensorMap r;
+  CUtensorMap id;
   int32_t m, n;
   int32_t k_blocks;     // ceil(K / kBK)
   uint32_t idesc;       // tcgen05 instruction descriptor (N = B box rows)
@@ -131,7 +138,8 @@ struct alignas(128) MemberDesc {
   // fused residual add (ResNet's identity / downsample add, MobileNet-v2's
   // inverted-residual add, BERT's skip connections): y = act(acc + res), res
   // [M, N] row-major bf16 with row stride ldr; null = none.  The residual is
-  // an earlier layer of the same tenant, complete by the dependency chain.
+  // an earlier layer of the same tenant, complete by the dependency chain the
+  // producer gates on; it enters the accumulator through maps r / id.
   const __nv_bfloat16* res;
   int32_t ldr;
 };
@@ -354,33 +362,26 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ float activate(float v, int act) {
-  if (act == kActRelu) return fmaxf(v, 0.f);
-  if (act == kActRelu6) return fminf(fmaxf(v, 0.f), 6.f);
-  if (act == kActGelu) return 0.5f * v * (1.f + erff(v * 0.70710678118654752f));
-  return v;
+// Activations: relu / relu6 are a clamp [lo, hi] applied while packing
+// (branch-free, two instructions); GELU runs out of line over a whole chunk
+// before packing (its erf would otherwise be inlined into every unrolled
+// packing site and bloat the kernel's instruction footprint).
+struct Clamp {
+  float lo, hi;
+};
+__device__ __forceinline__ Clamp clamp_of(int act) {
+  return Clamp{act == kActRelu || act == kActRelu6 ? 0.f : -INFINITY, act == kActRelu6 ? 6.f : INFINITY};
 }
 
-__device__ __forceinline__ uint32_t pack_bf16(uint32_t lo_bits, uint32_t hi_bits, int act) {
-  float lo = __uint_as_float(lo_bits), hi = __uint_as_float(hi_bits);
-  if (act) {
-    lo = activate(lo, act);
-    hi = activate(hi, act);
-  }
+__device__ __noinline__ float gelu_f(float x) { return 0.5f * x * (1.f + erff(x * 0.70710678118654752f)); }
+
+__device__ __forceinline__ uint32_t pack_bf16(uint32_t lo_bits, uint32_t hi_bits, Clamp k) {
+  const float lo = fminf(fmaxf(__uint_as_float(lo_bits), k.lo), k.hi);
+  const float hi = fminf(fmaxf(__uint_as_float(hi_bits), k.lo), k.hi);
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-// Adds 8 bf16 residual values (one 16-byte load) to 8 fp32 accumulators.
-__device__ __forceinline__ void add_residual8(uint32_t* v, uint4 r) {
-  const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const __nv_bfloat162 p = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
-    v[2 * i] = __float_as_uint(__uint_as_float(v[2 * i]) + __low2float(p));
-    v[2 * i + 1] = __float_as_uint(__uint_as_float(v[2 * i + 1]) + __high2float(p));
-  }
-}
 
 // Depthwise tile (CUDA cores): epilogue warp `ew` (0..7) computes output
 // pixels [m_tile*128 + ew*16, +16) x channels [n_tile*kDwTileC + 4*lane, +4)
@@ -398,6 +399,7 @@ __device__ __forceinline__ void depthwise_tile(const MemberDesc* __restrict__ md
   if (cg >= g) return;
   const int c = cbase + cg * 4;
   const int taps = md->r_taps, S = md->s_taps, st = md->stride, pad = md->pad, PQ = md->pq, Q = md->q;
+  const Clamp ck = clamp_of(md->act);  // depthwise activations: none / relu / relu6
   float wv[4][kDwMaxTaps];
 #pragma unroll
   for (int j = 0; j < 4; ++j)
@@ -450,8 +452,8 @@ __device__ __forceinline__ void depthwise_tile(const MemberDesc* __restrict__ md
     for (int j = 0; j < kG; ++j) {
       if (bb[j] < 0) continue;
       uint2 o;
-      o.x = pack_bf16(__float_as_uint(acc[j][0]), __float_as_uint(acc[j][1]), md->act);
-      o.y = pack_bf16(__float_as_uint(acc[j][2]), __float_as_uint(acc[j][3]), md->act);
+      o.x = pack_bf16(__float_as_uint(acc[j][0]), __float_as_uint(acc[j][1]), ck);
+      o.y = pack_bf16(__float_as_uint(acc[j][2]), __float_as_uint(acc[j][3]), ck);
       *reinterpret_cast<uint2*>(md->dy + static_cast<int64_t>(m_base + pp * (i0 + j)) * C + c) = o;
     }
   }
@@ -537,10 +539,11 @@ __device__ __forceinline__ void pool_tile(const MemberDesc* __restrict__ md, con
     for (int j = 0; j < 2; ++j) {
       if (bb[j] < 0) continue;
       uint4 o;
-      o.x = pack_bf16(__float_as_uint(acc[j][0] * scale), __float_as_uint(acc[j][1] * scale), md->act);
-      o.y = pack_bf16(__float_as_uint(acc[j][2] * scale), __float_as_uint(acc[j][3] * scale), md->act);
-      o.z = pack_bf16(__float_as_uint(acc[j][4] * scale), __float_as_uint(acc[j][5] * scale), md->act);
-      o.w = pack_bf16(__float_as_uint(acc[j][6] * scale), __float_as_uint(acc[j][7] * scale), md->act);
+      const Clamp ck = clamp_of(md->act);
+      o.x = pack_bf16(__float_as_uint(acc[j][0] * scale), __float_as_uint(acc[j][1] * scale), ck);
+      o.y = pack_bf16(__float_as_uint(acc[j][2] * scale), __float_as_uint(acc[j][3] * scale), ck);
+      o.z = pack_bf16(__float_as_uint(acc[j][4] * scale), __float_as_uint(acc[j][5] * scale), ck);
+      o.w = pack_bf16(__float_as_uint(acc[j][6] * scale), __float_as_uint(acc[j][7] * scale), ck);
       *reinterpret_cast<uint4*>(md->dy + static_cast<int64_t>(mm[j]) * C + c) = o;
     }
   }
@@ -746,15 +749,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int taps = md->taps, images = md->images;
         const CUtensorMap* amap = &md->a;
-        if (md->res) {
-          // the epilogue adds this tile's residual rows several tiles from
-          // now: pull them into L2 while the operands stream
-          const int rcols = min(md->n_tile, md->n - n0);
-          for (int cc = 0; cc < rcols; cc += 64) {
-            prefetch_box_l2(&md->r, n0 + cc, m0);
-            if (tall) prefetch_box_l2(&md->r, n0 + cc, m0 + kBM);
-          }
-        }
+
         auto load_a = [&](int kb, uint32_t st) {
           uint8_t* a_dst = ring + st * sbytes;
           if (fold) {
@@ -919,6 +914,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             advance();
           }
         }
+        if (md->res && k_blocks == md->k_blocks) {
+          // residual k-blocks (the tile, or the split holding the K tail):
+          // A = residual columns [n0 + 64 j, +64) of the tile's rows, B = the
+          // matching 64 columns of the identity
+          const int rk = (min(md->n_tile, md->n - n0) + kBK - 1) / kBK;
+          for (int j = 0; j < rk; ++j) {
+            wait_free();
+            uint64_t* bar = &full[stage];
+            mbar_expect_tx(bar, tx);
+            uint8_t* a_dst = ring + stage * sbytes;
+            tma_load_2d(a_dst, &md->r, bar, n0 + j * kBK, m0);
+            if (tall) tma_load_2d(a_dst + kABytes, &md->r, bar, n0 + j * kBK, m0 + kBM);
+            tma_load_2d(a_dst + b_off, &md->id, bar, j * kBK, 0);
+            advance();
+          }
+        }
       }
       if (first) asm volatile("griddepcontrol.wait;" ::: "memory");
     }
@@ -945,7 +956,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const TileEntry te = tiles[t];
       const MemberDesc* md = slots + te.member;
       const int kb_lo = __shfl_sync(0xffffffffu, te.kb_end ? te.kb_begin : 0, 0);
-      const int k_blocks = __shfl_sync(0xffffffffu, te.kb_end ? te.kb_end : md->k_blocks, 0);
+      const int k_tail = te.kb_end ? te.kb_end : md->k_blocks;
+      // residual k-blocks ride on the tile (or split) holding the K tail
+      const int k_res = md->res && k_tail == md->k_blocks
+                            ? (min(md->n_tile, md->n - te.n_tile * md->n_tile) + kBK - 1) / kBK
+                            : 0;
+      const int k_blocks = __shfl_sync(0xffffffffu, k_tail + k_res, 0);
       const uint32_t idesc = __shfl_sync(0xffffffffu, md->idesc, 0);
       const int lay = __shfl_sync(0xffffffffu, md->ring_narrow, 0);
       if (lay != layout) {  // the producer drained the ring before switching
@@ -1147,21 +1163,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int n0 = te.n_tile * md->n_tile;
       const int cols = min(md->n_tile, md->n - n0);
       const int act = md->act;
-      const __nv_bfloat16* res = md->res;
-      const int ldr = md->ldr, n_real = md->n, m_real = md->m;
-      if (res && lane == 0) {
-        // the residual is an earlier layer of this tenant, complete by the
-        // dependency chain the producer waited on; acquire it for this warp's
-        // generic-proxy loads (the producer's acquire ordered only its TMA).
-        // Outside a round program it comes from a prior launch: PDL wait.
-        if (te.dep >= 0) {
-          wait_counter(counters + te.dep, targets[te.dep], 32);
-        } else if (!dw_gated) {
-          asm volatile("griddepcontrol.wait;" ::: "memory");
-          dw_gated = true;
-        }
-      }
-      __syncwarp();
+      const Clamp ck = clamp_of(act);
       const int sw = (lane >> 1) & 3;  // SWIZZLE_64B: 16B chunk j of a 64 B row -> j ^ row[2:1]
       // Claim the next staging buffer once the store issued from it two
       // chunks ago has finished reading it.
@@ -1174,36 +1176,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++issued;
         buf ^= 1;
       };
-      // Residual of this lane's row, 32 columns from column c: four 16-byte
-      // loads (each lane reads whole 32-byte sectors), zero past the M / N
-      // edges.  Loaded one chunk ahead of its use (and the first chunk before
-      // the accumulator wait), so a chunk's load latency overlaps the
-      // previous chunk's drain; the producer pulled the tile's rows into L2.
-      auto load_res = [&](uint4 (&rv)[4], int c, int mrow) {
-        const int m = mrow + lane;
-        const bool ok = res && m < m_real && c < cols;
-        const __nv_bfloat16* rrow = res + static_cast<int64_t>(ok ? m : 0) * ldr + n0 + c;
+      // 32 fp32 accumulators of this lane's row (residual already added by
+      // the MMA) -> activation -> bf16 -> one 32x32 store box.
+      auto store_bf16 = [&](uint32_t (&v)[32], int c, int mrow) {
+        if (act == kActGelu) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          rv[j] = ok && n0 + c + 8 * j < n_real ? __ldcg(reinterpret_cast<const uint4*>(rrow + 8 * j))
-                                                : make_uint4(0u, 0u, 0u, 0u);
-      };
-      // 32 fp32 accumulators of this lane's row (+ residual) -> bf16 -> one
-      // 32x32 store box.
-      auto store_bf16 = [&](uint32_t (&v)[32], int c, int mrow, const uint4 (&rv)[4]) {
-        if (res) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) add_residual8(v + 8 * j, rv[j]);
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(gelu_f(__uint_as_float(v[i])));
         }
         uint8_t* sbuf = claim();
         uint8_t* row = sbuf + lane * 64;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           uint4 pk;
-          pk.x = pack_bf16(v[8 * j + 0], v[8 * j + 1], act);
-          pk.y = pack_bf16(v[8 * j + 2], v[8 * j + 3], act);
-          pk.z = pack_bf16(v[8 * j + 4], v[8 * j + 5], act);
-          pk.w = pack_bf16(v[8 * j + 6], v[8 * j + 7], act);
+          pk.x = pack_bf16(v[8 * j + 0], v[8 * j + 1], ck);
+          pk.y = pack_bf16(v[8 * j + 2], v[8 * j + 3], ck);
+          pk.z = pack_bf16(v[8 * j + 4], v[8 * j + 5], ck);
+          pk.w = pack_bf16(v[8 * j + 6], v[8 * j + 7], ck);
           *reinterpret_cast<uint4*>(row + ((j ^ sw) << 4)) = pk;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1214,8 +1202,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         issue();
       };
-      uint4 rcur[4], rnxt[4];
-      if (res && te.splits <= 1) load_res(rcur, 0, m0);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       if (trace && quarter == 0 && lane == 0) trace[6 * t + 4] = globaltimer();
@@ -1265,10 +1251,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + f.w);
               __stcg(src + j * 32, make_float4(0.f, 0.f, 0.f, 0.f));
             }
-            if (m0 < md->m) {
-              load_res(rcur, c, m0);
-              store_bf16(v, c, m0, rcur);
-            }
+            if (m0 < md->m) store_bf16(v, c, m0);
           }
           tc_fence_before();
           mbar_arrive(&acc_empty[acc]);
@@ -1276,25 +1259,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) *ctr = 0;  // next round (kernel boundary orders it)
         }
       } else {
-        if (m0 < md->m) {  // warp-uniform: this quarter holds at least one real row
+        // one or two (tall tile) 128-row halves; this warp's 32 rows of each
+        for (int h = 0; h <= tall; ++h) {
+          const int mrow = m0 + h * kBM;
+          if (mrow >= md->m) break;  // warp-uniform: no real row left in this quarter
+          const uint32_t tcol = taddr + h * md->n_tile;
           for (int c = 0; c < cols; c += kEpiChunk) {
             uint32_t v[32];
-            tmem_ld32(taddr + c, v);
-            if (res && (c + kEpiChunk < cols || tall))
-              load_res(rnxt, c + kEpiChunk < cols ? c + kEpiChunk : 0, c + kEpiChunk < cols ? m0 : m0 + kBM);
-            store_bf16(v, c, m0, rcur);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) rcur[j] = rnxt[j];
-          }
-        }
-        if (tall && m0 + kBM < md->m) {  // tall tile: the second 128-row half
-          for (int c = 0; c < cols; c += kEpiChunk) {
-            uint32_t v[32];
-            tmem_ld32(taddr + md->n_tile + c, v);
-            if (res && c + kEpiChunk < cols) load_res(rnxt, c + kEpiChunk, m0 + kBM);
-            store_bf16(v, c, m0 + kBM, rcur);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) rcur[j] = rnxt[j];
+            tmem_ld32(tcol + c, v);
+            store_bf16(v, c, mrow);
           }
         }
         tc_fence_before();
