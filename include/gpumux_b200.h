@@ -451,18 +451,20 @@ int gm_round_tiles(gm_ctx* ctx, const gm_plans* p, gm_tile* out, size_t cap, siz
 /* The executed tile table of a round program, one entry per tile in launch
  * order: which operator, which output tile, the tile variant the runtime
  * chose (tall 256-row, N width, split-K slice) and its device-side
- * dependency edge (done = counter it publishes to, dep = counter it waits on,
- * -1 = none).  Differs from gm_build_tile_table (the planner's tile count,
+ * dependency edges: one counter per output row block of a member instance;
+ * a tile waits for the producer row blocks its input rows (and residual
+ * rows) come from, -1 = none.  Differs from gm_build_tile_table (the planner's tile count,
  * thread_blocks under the b200 profile) by those variants. */
 typedef struct gm_round_tile {
   int32_t tenant, layer;
   int32_t m_tile, n_tile;
   int32_t rows, cols;               /* output rows per tile (128 / 256 / 32) and N width */
   int32_t splits, kb_begin, kb_end; /* split-K slice (splits 1: the whole K, kb_end 0) */
-  int32_t done, dep;
+  int32_t done;                     /* the tile's row-block counter (-1: nothing waits on it) */
+  int32_t dep, dep_n;               /* waits on counters [dep, dep + dep_n): its input's row blocks */
+  int32_t rdep, rdep_n;             /* and [rdep, rdep + rdep_n): its residual's row blocks */
   int32_t plan;                     /* index of the formed super-kernel it came from */
   int32_t cuda_core;                /* 1: depthwise / pool tile computed on CUDA cores */
-  int32_t reserved0;
 } gm_round_tile;
 int gm_round_tile_info(gm_ctx* ctx, const gm_plans* p, gm_round_tile* out, size_t cap, size_t* n);
 /* End-to-end round program (the serving call with host buffers): per tenant

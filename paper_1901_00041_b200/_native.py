@@ -59,7 +59,8 @@ class gm_round_tenant(C.Structure):
 
 class gm_round_tile(C.Structure):
     _fields_ = [(f, C.c_int32) for f in ("tenant", "layer", "m_tile", "n_tile", "rows", "cols", "splits",
-                                          "kb_begin", "kb_end", "done", "dep", "plan", "cuda_core", "reserved0")]
+                                          "kb_begin", "kb_end", "done", "dep", "dep_n", "rdep", "rdep_n", "plan",
+                                          "cuda_core")]
 
 
 class gm_batch_policy(C.Structure):

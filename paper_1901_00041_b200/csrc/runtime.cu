@@ -95,6 +95,9 @@ struct Operator {
   int src = -1, res_src = -1;
   const char* y = nullptr;
   int64_t y_bytes = 0;
+  int64_t x_pitch = 0;           // elements per input row (GEMM) or pixel (windowed ops)
+  const char* res = nullptr;     // residual base and row stride (elements)
+  int64_t ldr = 0;
 };
 
 struct Prepared {
@@ -557,6 +560,11 @@ struct Runtime {
       }
       op.y = static_cast<const char*>(L.y);
       op.y_bytes = op.shape.m * op.shape.n * 2;
+      op.x_pitch = L.ldx > 0 ? L.ldx : (L.kind == GM_LAYER_GEMM ? op.shape.k : op.conv.in_channels);
+      if (L.res) {
+        op.res = static_cast<const char*>(L.res);
+        op.ldr = L.ldr > 0 ? L.ldr : op.shape.n;
+      }
       md.n_tile = op.n_tile;
       md.ring_narrow = ring_narrow_of(md, b_box_rows(op.shape.n, op.n_tile));
       op.slot = static_cast<int>(host_desc.size() + descs.size());
@@ -700,7 +708,7 @@ struct Runtime {
       for (int64_t a = 0; a < mt; ++a)
         for (int64_t b = 0; b < nt; ++b)
           table.push_back(dev::TileEntry{static_cast<uint16_t>(slot), 0, static_cast<uint16_t>(a),
-                                         static_cast<uint16_t>(b), -1, -1, 0, 0, -1});
+                                         static_cast<uint16_t>(b), -1, -1, 0, 0, -1, -1, 0, 0});
       if (op.prepass) p.prepass_ops.push_back(f);
     }
     p.n_tiles = static_cast<int>(table.size());
@@ -708,6 +716,40 @@ struct Runtime {
     cuda_check(cudaMemcpy(p.tiles, table.data(), table.size() * sizeof(dev::TileEntry), cudaMemcpyHostToDevice),
                "upload tile table");
     return prepared.emplace(key, std::move(p)).first->second;
+  }
+
+  // Rows [lo, hi] of producer `pr`'s output that consumer `c`'s output rows
+  // [r0, r1) read: through its input x (a view into pr's y: a windowed op's
+  // receptive field, or a GEMM's row slice) or, with `residual`, through its
+  // residual (the same rows).  Conservative for windowed ops: whole input
+  // image rows from the first output pixel's window to the last one's.
+  std::pair<int64_t, int64_t> producer_rows(const Operator& c, const Operator& pr, bool residual, int64_t r0,
+                                            int64_t r1) const {
+    const int64_t np = pr.shape.n;
+    int64_t lo, hi;
+    if (residual) {
+      const int64_t off = (c.res - pr.y) / 2;
+      lo = (off + r0 * c.ldr) / np;
+      hi = (off + (r1 - 1) * c.ldr + c.shape.n - 1) / np;
+    } else if (c.kind == GM_LAYER_GEMM) {
+      const int64_t off = (static_cast<const char*>(c.x) - pr.y) / 2;
+      lo = (off + r0 * c.x_pitch) / np;
+      hi = (off + (r1 - 1) * c.x_pitch + c.shape.k - 1) / np;
+    } else {
+      const Conv& v = c.conv;
+      const int64_t P = (v.image_h + 2 * v.padding - v.kernel_h) / v.stride + 1;
+      const int64_t Q = (v.image_w + 2 * v.padding - v.kernel_w) / v.stride + 1;
+      auto pixel_row = [&](int64_t m, bool last) {
+        const int64_t b = m / (P * Q), p = (m % (P * Q)) / Q;
+        const int64_t ih = last ? std::min(v.image_h - 1, p * v.stride - v.padding + v.kernel_h - 1)
+                                : std::max<int64_t>(0, p * v.stride - v.padding);
+        return (b * v.image_h + ih) * v.image_w + (last ? v.image_w - 1 : 0);
+      };
+      const int64_t off = (static_cast<const char*>(c.x) - pr.y) / 2;
+      lo = (off + pixel_row(r0, false) * c.x_pitch) / np;
+      hi = (off + pixel_row(r1 - 1, true) * c.x_pitch + c.x_pitch - 1) / np;
+    }
+    return {std::max<int64_t>(0, lo), std::min(pr.shape.m - 1, hi)};
   }
 
   // Round program: every plan of a round, in plan order, as ONE persistent
@@ -727,7 +769,13 @@ struct Runtime {
     Prepared p;
     std::vector<dev::TileEntry> table;
     std::vector<uint32_t> targets;
-    std::unordered_map<int, int> last_instance;  // flat op -> instance id
+    // flat op -> its instance in this round: counters [base, base + mt), one
+    // per output row block of `rows` rows
+    struct Instance {
+      int base;
+      int64_t rows, mt;
+    };
+    std::unordered_map<int, Instance> last_instance;
     int n_ws = 0;
     // Concurrency estimate per shape: tenants run their chains in step, so
     // all members of a shape across the round's plans are in flight together.
@@ -753,24 +801,59 @@ struct Runtime {
           }
         }
         const bool tall = is_tall(slot);
-        int dep = -1;
-        if (op.layer > 0) {
-          auto prev = last_instance.find(tenant_ops[op.tenant][op.layer - 1]);
-          if (prev != last_instance.end()) dep = prev->second;
+        // Dependencies.  Dataflow layers wait on the producer row blocks
+        // their rows read (input and residual); a layer without a producer in
+        // the round but with an earlier layer in it (an operator list without
+        // dataflow) waits on that whole layer, keeping the tenant's layer order
+        // (sim.cpp:482-488); the first layer of a gated (e2e) round waits on
+        // the tenant's input gate (target 1), opened after its H2D copy.
+        const Instance* src_inst = nullptr;
+        const Instance* res_inst = nullptr;
+        const Operator* src_op = nullptr;
+        const Operator* res_op = nullptr;
+        const Instance* chain = nullptr;
+        int gate = -1;
+        if (op.src >= 0) {
+          auto it2 = last_instance.find(tenant_ops[op.tenant][op.src]);
+          if (it2 != last_instance.end()) {
+            src_inst = &it2->second;
+            src_op = &flat[it2->first];
+          }
+        } else if (op.layer > 0) {
+          auto it2 = last_instance.find(tenant_ops[op.tenant][op.layer - 1]);
+          if (it2 != last_instance.end()) chain = &it2->second;
         } else if (gated) {
-          // the tenant's query input: gate counter (target 1), set after its H2D
-          dep = static_cast<int>(targets.size());
+          gate = static_cast<int>(targets.size());
           targets.push_back(1);
-          p.gates.emplace_back(op.tenant, dep);
+          p.gates.emplace_back(op.tenant, gate);
         }
-        // the member instance's own completion counter comes after any gate
-        // counter pushed above (a tile never publishes to what it waits on)
-        const int inst = static_cast<int>(targets.size());
-        if (dep == inst) throw std::logic_error("round program: member instance waits on its own counter");
-        last_instance[f] = inst;
+        if (op.res_src >= 0) {
+          auto it2 = last_instance.find(tenant_ops[op.tenant][op.res_src]);
+          if (it2 != last_instance.end()) {
+            res_inst = &it2->second;
+            res_op = &flat[it2->first];
+          }
+        }
         const int64_t tm = cuda_core_kind(op.kind) ? cuda_core_rows(op.kind) : dev::kBM << (tall ? 1 : 0);
         const int64_t mt = (op.shape.m + tm - 1) / tm;
         const int64_t nt = (op.shape.n + w - 1) / w;
+        // this instance's counters come after any gate counter pushed above
+        // (a tile never publishes to what it waits on)
+        const int inst = static_cast<int>(targets.size());
+        auto deps_of = [&](int64_t a, bool residual) -> std::pair<int32_t, uint16_t> {
+          const Instance* in = residual ? res_inst : src_inst;
+          if (!residual && !in) {
+            if (chain) return {chain->base, static_cast<uint16_t>(chain->mt)};
+            if (gate >= 0) return {gate, 1};
+            return {-1, 0};
+          }
+          if (!in) return {-1, 0};
+          const int64_t r0 = a * tm, r1 = std::min(op.shape.m, r0 + tm);
+          const auto [lo, hi] = producer_rows(op, residual ? *res_op : *src_op, residual, r0, r1);
+          const int64_t first = lo / in->rows, last = hi / in->rows;
+          if (last - first + 1 > 0xFFFF) throw std::logic_error("round program: dependency range too long");
+          return {static_cast<int32_t>(in->base + first), static_cast<uint16_t>(last - first + 1)};
+        };
         const int kb = static_cast<int>((op.shape.k + dev::kBK - 1) / dev::kBK);
         // Split-K when the plan cannot fill the SMs and the K loop is long:
         // about two waves of tiles, at least 4 k-blocks per split.
@@ -785,25 +868,35 @@ struct Runtime {
           const int chunk = (kb + splits - 1) / splits;
           splits = (kb + chunk - 1) / chunk;
         }
-        // 4 epilogue warps arrive per output tile (8 for a depthwise tile: all of them compute it)
-        targets.push_back(static_cast<uint32_t>(mt * nt * (cuda_core_kind(op.kind) ? 8 : 4)));
+        // one counter per row block: 4 epilogue warps arrive per output tile
+        // (8 for a CUDA-core tile: all of them compute it), nt tiles per block
         for (int64_t a = 0; a < mt; ++a)
+          targets.push_back(static_cast<uint32_t>(nt * (cuda_core_kind(op.kind) ? 8 : 4)));
+        for (int64_t a = 0; a < mt; ++a) {
+          const auto [dep, dep_n] = deps_of(a, false);
+          const auto [rdep, rdep_n] = deps_of(a, true);
+          const int32_t done = inst + static_cast<int32_t>(a);
+          if ((dep >= 0 && done >= dep && done < dep + dep_n) || (rdep >= 0 && done >= rdep && done < rdep + rdep_n))
+            throw std::logic_error("round program: a tile waits on its own counter");
           for (int64_t b = 0; b < nt; ++b) {
             if (splits == 1) {
               table.push_back(dev::TileEntry{static_cast<uint16_t>(slot), 1, static_cast<uint16_t>(a),
-                                             static_cast<uint16_t>(b), inst, dep, 0, 0, -1});
+                                             static_cast<uint16_t>(b), done, dep, 0, 0, -1, rdep, dep_n, rdep_n});
               continue;
             }
             const int kbt = host_desc[slot].k_blocks;  // the kernel's K loop (padded channels included)
             const int chunk = (kbt + splits - 1) / splits;
             for (int s = 0; s < splits; ++s)
               table.push_back(dev::TileEntry{static_cast<uint16_t>(slot), static_cast<uint16_t>(splits),
-                                             static_cast<uint16_t>(a), static_cast<uint16_t>(b), inst, dep,
+                                             static_cast<uint16_t>(a), static_cast<uint16_t>(b), done, dep,
                                              static_cast<uint16_t>(s * chunk),
-                                             static_cast<uint16_t>(std::min(kbt, (s + 1) * chunk)), n_ws});
+                                             static_cast<uint16_t>(std::min(kbt, (s + 1) * chunk)), n_ws, rdep,
+                                             dep_n, rdep_n});
             ++n_ws;
           }
-        if (op.prepass && op.src >= 0 && last_instance.count(tenant_ops[op.tenant][op.src]))
+        }
+        last_instance[f] = Instance{inst, tm, mt};
+        if (op.prepass && src_inst)
           throw std::invalid_argument("round program: operator " + std::to_string(op.layer) + " of tenant " +
                                       std::to_string(op.tenant) +
                                       " needs a pre-pass over an input produced inside the round");
@@ -899,12 +992,14 @@ struct Runtime {
     // launch also skips the last-CTA reset (the exit counter).
     {
       std::vector<char> needed(targets.size(), 0);
-      for (const auto& te : table)
-        if (te.dep >= 0) needed[te.dep] = 1;
+      for (const auto& te : table) {
+        for (int i = 0; te.dep >= 0 && i < te.dep_n; ++i) needed[te.dep + i] = 1;
+        for (int i = 0; te.rdep >= 0 && i < te.rdep_n; ++i) needed[te.rdep + i] = 1;
+      }
       bool used = greedy_schedule || p.nq > 0;
       for (auto& te : table) {
         if (te.splits <= 1 && te.done >= 0 && !needed[te.done]) te.done = -1;
-        used = used || te.done >= 0 || te.dep >= 0;
+        used = used || te.done >= 0 || te.dep >= 0 || te.rdep >= 0;
       }
       p.self_reset = used;
     }
@@ -1527,9 +1622,11 @@ int gm_round_tile_info(gm_ctx* ctx, const gm_plans* p, gm_round_tile* out, size_
     o.kb_end = te.kb_end;
     o.done = te.done;
     o.dep = te.dep;
+    o.dep_n = te.dep >= 0 ? te.dep_n : 0;
+    o.rdep = te.rdep;
+    o.rdep_n = te.rdep >= 0 ? te.rdep_n : 0;
     o.plan = pr.tile_plan[i];
     o.cuda_core = dev::cuda_core_mode(md.a_mode) ? 1 : 0;
-    o.reserved0 = 0;
   }
   GM_API_END
 }

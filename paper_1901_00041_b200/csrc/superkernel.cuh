@@ -146,9 +146,12 @@ struct alignas(128) MemberDesc {
 
 // Device tile-table entry; `member` is the registered slot index.
 // In a round program (one persistent launch for a whole space-time round),
-// `done` names the completion counter of the tile's member instance and
-// `dep` the counter of the same tenant's previous layer (-1 = none): a tile's
-// activations are loaded only once every tile of its dependency is stored.
+// every output row block (m-tile) of a member instance has a completion
+// counter: `done` is the tile's.  A tile's activations are loaded only once
+// the producer m-tiles holding its input rows are stored: counters
+// [dep, dep + dep_n) (its input's producing layer) and [rdep, rdep + rdep_n)
+// (its residual's), -1 = none.  So consecutive layers overlap row block by
+// row block instead of meeting at a per-layer barrier.
 //
 // Split-K (round programs, few-tile long-K members): `splits` > 1 tiles each
 // cover k-blocks [kb_begin, kb_end) of output tile `ws`; they reduce-add fp32
@@ -159,7 +162,15 @@ struct TileEntry {
   int32_t done, dep;
   uint16_t kb_begin, kb_end;  // kb_end == 0: the whole K
   int32_t ws;                 // split workspace tile (-1 = not split)
+  int32_t rdep;
+  uint16_t dep_n, rdep_n;
 };
+
+// Wait until every counter of [first, first + n) reached its target (acquire).
+__device__ __forceinline__ void wait_range(const uint32_t* counters, const uint32_t* targets, int32_t first, int n,
+                                           uint32_t sleep_ns);
+// Whether every counter of [first, first + n) reached its target (no wait).
+__device__ __forceinline__ bool range_ready(const uint32_t* counters, const uint32_t* targets, int32_t first, int n);
 
 // Round-program side state (all null for a plain super-kernel launch).
 //
@@ -223,6 +234,17 @@ __device__ __forceinline__ void wait_counter(const uint32_t* ctr, uint32_t want,
         __trap();
     }
   }
+}
+
+__device__ __forceinline__ void wait_range(const uint32_t* counters, const uint32_t* targets, int32_t first, int n,
+                                           uint32_t sleep_ns) {
+  for (int i = 0; i < n; ++i) wait_counter(counters + first + i, targets[first + i], sleep_ns);
+}
+
+__device__ __forceinline__ bool range_ready(const uint32_t* counters, const uint32_t* targets, int32_t first, int n) {
+  for (int i = 0; i < n; ++i)
+    if (ld_acquire(counters + first + i) < targets[first + i]) return false;
+  return true;
 }
 
 // ---------------------------------------------------------------- PTX helpers
@@ -801,8 +823,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // stored).  Weights never wait on either.
         auto gate = [&]() {
           if (first) asm volatile("griddepcontrol.wait;" ::: "memory");
-          if (te.dep >= 0) {
-            wait_counter(counters + te.dep, targets[te.dep], 32);
+          if (te.dep >= 0 || te.rdep >= 0) {
+            if (te.dep >= 0) wait_range(counters, targets, te.dep, te.dep_n, 32);
+            if (te.rdep >= 0) wait_range(counters, targets, te.rdep, te.rdep_n, 32);
             asm volatile("fence.proxy.async.global;" ::: "memory");
           }
         };
@@ -824,7 +847,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             advance();
           }
           kb = kb_lo + pre;
-        } else if (te.dep >= 0) {
+        } else if (te.dep >= 0 || te.rdep >= 0) {
           // weights do not wait on the dependency: stream B into the next
           // stages (up to the ring depth, as slots free up), then gate, then
           // the activations into the same stages
@@ -1060,8 +1083,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (h >= len) continue;
             pending = true;
             // peek (no contention): skip a queue whose head is still blocked
-            const int dep = tiles[ra.qbeg[q] + static_cast<int>(h)].dep;
-            if (dep >= 0 && ld_acquire(counters + dep) < targets[dep]) continue;
+            const TileEntry& head = tiles[ra.qbeg[q] + static_cast<int>(h)];
+            if (head.dep >= 0 && !range_ready(counters, targets, head.dep, head.dep_n)) continue;
+            if (head.rdep >= 0 && !range_ready(counters, targets, head.rdep, head.rdep_n)) continue;
             // claim with one fetch-and-add; a claim that overtook the peeked
             // head may land on a not-yet-ready tile, which the gate waits for
             // (queue order is a topological order, so this cannot deadlock)
@@ -1133,8 +1157,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           dw_gated = true;
         }
         if (te.dep >= 0) {
-          if (lane == 0)
-            wait_counter(counters + te.dep, targets[te.dep], 32);
+          if (lane == 0) wait_range(counters, targets, te.dep, te.dep_n, 32);
           __syncwarp();
         }
         if (trace && warp == 4 && lane == 0) {

@@ -309,28 +309,72 @@ def test_serve_round_e2e_host_buffers(oracle):
     check_engine(eng, oracle)
 
 
+def _producer_rows(L, P, b, r0, r1, residual):
+    """Python restatement of Runtime::producer_rows for the test: rows of
+    producer layer P's output that consumer L's output rows [r0, r1) read."""
+    np_ = P.gemm_shape(b).n
+    mp = P.gemm_shape(b).m
+    if residual:
+        n = L.gemm_shape(b).n
+        lo, hi = r0 * n // np_, ((r1 - 1) * n + n - 1) // np_
+    elif L.kind == "gemm":
+        s = L.gemm_shape(b)
+        pitch = np_ * mp // s.m  # the source viewed as [rows, -1]
+        lo = (L.src_col + r0 * pitch) // np_
+        hi = (L.src_col + (r1 - 1) * pitch + s.k - 1) // np_
+    else:
+        c = L.conv
+        P_ = (c.image_h + 2 * c.padding - c.kernel_h) // c.stride + 1
+        Q_ = (c.image_w + 2 * c.padding - c.kernel_w) // c.stride + 1
+
+        def row(m, last):
+            bb, p = m // (P_ * Q_), (m % (P_ * Q_)) // Q_
+            ih = min(c.image_h - 1, p * c.stride - c.padding + c.kernel_h - 1) if last else \
+                max(0, p * c.stride - c.padding)
+            return (bb * c.image_h + ih) * c.image_w + (c.image_w - 1 if last else 0)
+        lo, hi = row(r0, False), row(r1 - 1, True)
+    return max(0, lo), min(mp - 1, hi)
+
+
 def test_round_dependency_graph():
-    """Device tile table edges (gm_round_tile_info): every tile of a tenant's
-    layer l > 0 waits on the counter its layer l-1 tiles publish to, no tile
-    waits on its own counter, and the counters a tile waits on are published."""
+    """Device tile table edges (gm_round_tile_info): every tile waits on
+    exactly the producer row blocks its input rows and residual rows come
+    from (re-derived here from the layer geometry), never on its own counter,
+    and the counters anything waits on are published."""
     from paper_1901_00041_b200 import workload as W
     from paper_1901_00041_b200.engine import SpaceTimeEngine
-    eng = SpaceTimeEngine([W.resnet18(64), W.mobilenet_v2(64, classifier=False)], [2, 2])
+    models = [W.resnet18(64), W.mobilenet_v2(64, classifier=False), W.bert_base_gemms(16, 2)]
+    eng = SpaceTimeEngine(models, [2, 2, 2])
     rnd = eng.plan_round()
     info = rnd.tile_info()
-    done = {}
+    base, rows = {}, {}
     for t in info:
-        done.setdefault((t["tenant"], t["layer"]), set()).add(t["done"])
+        key = (t["tenant"], t["layer"])
+        rows[key] = t["rows"]
+        if t["m_tile"] == 0 and t["done"] >= 0:
+            base[key] = t["done"]
+    needed = set()
     for t in info:
-        assert t["dep"] < 0 or t["dep"] != t["done"]
-        if t["layer"] == 0:
-            assert t["dep"] == -1
-        else:
-            prev = done[(t["tenant"], t["layer"] - 1)]
-            assert prev == {t["dep"]}, (t, prev)
-    last = {(tn, max(l for (tt, l) in done if tt == tn)) for tn, _ in done}
-    for key, d in done.items():
-        assert (d == {-1}) == (key in last)  # only the chain tails skip the publish
+        L = models[t["tenant"]][t["layer"]]
+        for d, n in ((t["dep"], t["dep_n"]), (t["rdep"], t["rdep_n"])):
+            if d >= 0:
+                needed.update(range(d, d + n))
+                assert not (d <= t["done"] < d + n)
+        r0 = t["m_tile"] * t["rows"]
+        r1 = min(L.gemm_shape(2).m, r0 + t["rows"])
+        for which, (d, n) in (("src", (t["dep"], t["dep_n"])), ("res", (t["rdep"], t["rdep_n"]))):
+            j = L.src if which == "src" else L.res
+            if j is None:
+                assert which == "res" or t["layer"] == 0 or d == base[(t["tenant"], t["layer"] - 1)]
+                if which == "res":
+                    assert d == -1
+                continue
+            P = models[t["tenant"]][j]
+            lo, hi = _producer_rows(L, P, 2, r0, r1, which == "res")
+            pr = rows[(t["tenant"], j)]
+            assert (d, n) == (base[(t["tenant"], j)] + lo // pr, hi // pr - lo // pr + 1), (t, which)
+    published = {t["done"] for t in info if t["done"] >= 0}
+    assert needed <= published
 
 
 @pytest.mark.parametrize("options", [{}, {"greedy_schedule": 1}, {"dynamic_schedule": 1}, {"critical_order": 0},
