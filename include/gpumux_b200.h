@@ -8,8 +8,9 @@
  *
  *   - plain C types only: POD structs, pointers, sizes; no torch, no STL
  *   - every function returns an int status (GM_OK == 0); the message of the
- *     last failure is gm_last_error() (per-thread) — messages equal the
- *     reference's std::invalid_argument::what() texts
+ *     last failure is gm_last_error(ctx) for calls on a context, and
+ *     gm_last_error(NULL) for the calling thread's last failure of any call —
+ *     messages equal the reference's std::invalid_argument::what() texts
  *   - objects (queue, plans, cache, ctx) are opaque handles; a handle is a
  *     single logical actor and is not thread-safe; use one
  *     gm_ctx per GPU on one host thread (tenant-sharded placement)
@@ -27,7 +28,7 @@
 extern "C" {
 #endif
 
-#define GM_ABI_VERSION 2
+#define GM_ABI_VERSION 3
 
 enum gm_status {
   GM_OK = 0,
@@ -141,7 +142,11 @@ typedef struct gm_plan_info {
 
 /* ---- defaults and profiles ---------------------------------------------- */
 
-const char* gm_last_error(void);
+typedef struct gm_ctx gm_ctx;       /* one per GPU (see below) */
+
+/* Message of the last failed call on ctx (NULL: of this thread's last failed
+ * call).  The reference throws; its what() text is this string. */
+const char* gm_last_error(const gm_ctx* ctx);
 int gm_abi_version(void);
 
 void gm_device_spec_default(gm_device_spec* out);  /* DeviceSpec{} defaults   */
@@ -350,8 +355,6 @@ typedef struct gm_tenant_desc {     /* Tenant, workload.hpp:14-22 */
   int32_t reserved0;
 } gm_tenant_desc;
 
-typedef struct gm_ctx gm_ctx;       /* one per GPU */
-
 /* cuda_device < 0 creates a host-only context (planner, no launches). */
 int gm_create(const gm_device_spec* d, const gm_batch_policy* p, const gm_detector* det,
               int cuda_device, gm_ctx** out);
@@ -393,11 +396,80 @@ int gm_tenant_count(const gm_ctx* ctx, int32_t* n);
 /* Prepare (host→device upload on a miss, never inside graph capture) and
  * launch the super-kernel of plan i on `stream` (a cudaStream_t; 0 = legacy
  * default).  planned_s/cache_hit follow dispatch_cost (scheduler.cpp:201-212)
- * against the ctx's SuperKernelCache.  Launches are CUDA-graph capturable once
- * prepared. */
+ * against the ctx's SuperKernelCache.  Members enqueued with gm_enqueue I/O
+ * get their copies around the launch, and the dispatch is tracked for
+ * gm_poll_completions (outside stream capture).  Launches are CUDA-graph
+ * capturable once prepared. */
 int gm_prepare(gm_ctx* ctx, const gm_plans* p, size_t i);
 int gm_dispatch(gm_ctx* ctx, const gm_plans* p, size_t i, uint64_t stream, double* planned_s,
                 int* cache_hit);
+/* ---- host-driven loop over one ctx (the reference run_space_time shape,
+ * proj/src/sim.cpp:452-576): gm_enqueue -> gm_ctx_form_batches ->
+ * gm_dispatch -> gm_poll_completions -> gm_ctx_record_latency ->
+ * gm_ctx_detect_stragglers -> gm_ctx_evict.  An external scheduler drives the
+ * GPU asynchronously through these; gm_serve is the same loop run natively. */
+
+/* I/O of one request (B200 extension of KernelRequest): host (pinned or
+ * pageable) or device pointers.  x: copied into the layer's registered input
+ * on the dispatch stream right before the super-kernel that runs the request
+ * (a query batch arriving at layer 0); y: the layer's output copied out right
+ * after it.  Either may be NULL / 0 bytes.  Sizes must not exceed the
+ * registered buffers. */
+typedef struct gm_request_io {
+  const void* x;
+  size_t x_bytes;
+  void* y;
+  size_t y_bytes;
+} gm_request_io;
+
+/* RequestQueue::enqueue (scheduler.cpp:8-16) on the ctx's queue, plus the
+ * request's I/O (nullable).  On a device ctx the (tenant, layer) must be
+ * registered and the request's shape equal its GEMM shape.  Errors keep the
+ * reference texts ("enqueue: duplicate request id N", "enqueue: invalid shape"). */
+int gm_enqueue(gm_ctx* ctx, const gm_kernel_request* r, const gm_request_io* io);
+/* form_batches (scheduler.cpp:96-199) over the ctx's queue, policy and device. */
+int gm_ctx_form_batches(gm_ctx* ctx, int64_t now, gm_plans** out);
+/* Nanoseconds on the ctx's steady clock (origin: gm_create); the clock of
+ * gm_completion's dispatch/complete stamps. */
+int64_t gm_ctx_now_ns(const gm_ctx* ctx);
+
+/* One completed member request of a dispatched super-kernel: the per-member
+ * completion fan-out of run_space_time (sim.cpp:466-476). */
+typedef struct gm_completion {
+  uint64_t request_id;
+  int32_t tenant_index;
+  int32_t layer_index;
+  uint32_t pass_index;
+  uint32_t batch;
+  int64_t enqueue_time;             /* as enqueued (caller's clock) */
+  int64_t slo_deadline;
+  int64_t dispatch_ns;              /* gm_ctx_now_ns at gm_dispatch */
+  int64_t complete_ns;              /* gm_ctx_now_ns when the poll first saw it complete */
+  double exec_seconds;              /* the super-kernel's device time (CUDA events): the
+                                       execution time record_latency takes (sim.cpp:475-476) */
+  int32_t plan_members;             /* members of its super-kernel */
+  int32_t reserved0;
+} gm_completion;
+
+/* Non-blocking: appends the member completions of every dispatch whose work
+ * (copy-in, super-kernel, copy-out) has finished, in dispatch order, whole
+ * dispatches only; *n = completions written.  GM_ERANGE if the oldest
+ * finished dispatch has more members than cap. */
+int gm_poll_completions(gm_ctx* ctx, gm_completion* out, size_t cap, size_t* n);
+/* Dispatches issued by gm_dispatch that gm_poll_completions has not yet returned. */
+int gm_ctx_in_flight(const gm_ctx* ctx, size_t* n);
+/* Blocks until every dispatch in flight has finished on the device. */
+int gm_ctx_synchronize(gm_ctx* ctx);
+
+/* The ctx's TenantHealth vector (one per registered tenant; on a host-only
+ * ctx, one per tenant index seen by gm_enqueue):
+ * record_latency / detect_stragglers / evict, scheduler.cpp:214-271, with the
+ * ctx's DetectorParams.  gm_ctx_evict also drops the cancelled requests' I/O. */
+int gm_ctx_record_latency(gm_ctx* ctx, int32_t tenant, double observed_seconds);
+int gm_ctx_detect_stragglers(gm_ctx* ctx, int32_t* out, size_t cap, size_t* n);
+int gm_ctx_evict(gm_ctx* ctx, int32_t tenant, uint64_t* cancelled_ids, size_t cap, size_t* n);
+int gm_ctx_health(const gm_ctx* ctx, int32_t tenant, gm_tenant_health* out);
+
 /* Launch an explicit member list (tenant, layer pairs) as one super-kernel;
  * n == 1 is the single-problem kernel used by the time-only / space-only
  * baseline modes.  Returns the number of kernels launched in *launches. */

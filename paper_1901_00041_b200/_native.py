@@ -141,13 +141,24 @@ class gm_serve_stats(C.Structure):
                 ("evicted", C.c_int32), ("reserved0", C.c_int32), ("evicted_mask", C.c_uint64)]
 
 
+class gm_request_io(C.Structure):
+    _fields_ = [("x", C.c_void_p), ("x_bytes", C.c_size_t), ("y", C.c_void_p), ("y_bytes", C.c_size_t)]
+
+
+class gm_completion(C.Structure):
+    _fields_ = [("request_id", C.c_uint64), ("tenant_index", C.c_int32), ("layer_index", C.c_int32),
+                ("pass_index", C.c_uint32), ("batch", C.c_uint32), ("enqueue_time", C.c_int64),
+                ("slo_deadline", C.c_int64), ("dispatch_ns", C.c_int64), ("complete_ns", C.c_int64),
+                ("exec_seconds", C.c_double), ("plan_members", C.c_int32), ("reserved0", C.c_int32)]
+
+
 class gm_dispatch_event(C.Structure):
     _fields_ = [("start_ns", C.c_int64), ("end_ns", C.c_int64), ("device_ms", C.c_double), ("flops", C.c_double),
                 ("queries", C.c_int32), ("tenants", C.c_int32), ("launches", C.c_int32), ("tiles", C.c_int32)]
 
 
 _SIGS = {
-    "gm_last_error": (C.c_char_p, []),
+    "gm_last_error": (C.c_char_p, [C.c_void_p]),
     "gm_abi_version": (C.c_int, []),
     "gm_device_spec_default": (None, [P(gm_device_spec)]),
     "gm_device_spec_v100": (None, [P(gm_device_spec)]),
@@ -215,6 +226,16 @@ _SIGS = {
     "gm_tenant_count": (C.c_int, [C.c_void_p, P(C.c_int32)]),
     "gm_prepare": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
     "gm_dispatch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint64, P(C.c_double), P(C.c_int)]),
+    "gm_enqueue": (C.c_int, [C.c_void_p, P(gm_kernel_request), P(gm_request_io)]),
+    "gm_ctx_form_batches": (C.c_int, [C.c_void_p, C.c_int64, P(C.c_void_p)]),
+    "gm_ctx_now_ns": (C.c_int64, [C.c_void_p]),
+    "gm_poll_completions": (C.c_int, [C.c_void_p, P(gm_completion), C.c_size_t, P(C.c_size_t)]),
+    "gm_ctx_in_flight": (C.c_int, [C.c_void_p, P(C.c_size_t)]),
+    "gm_ctx_synchronize": (C.c_int, [C.c_void_p]),
+    "gm_ctx_record_latency": (C.c_int, [C.c_void_p, C.c_int32, C.c_double]),
+    "gm_ctx_detect_stragglers": (C.c_int, [C.c_void_p, P(C.c_int32), C.c_size_t, P(C.c_size_t)]),
+    "gm_ctx_evict": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_uint64), C.c_size_t, P(C.c_size_t)]),
+    "gm_ctx_health": (C.c_int, [C.c_void_p, C.c_int32, P(gm_tenant_health)]),
     "gm_launch_members": (C.c_int, [C.c_void_p, P(C.c_int32), P(C.c_int32), C.c_size_t, C.c_uint64,
                                     P(C.c_int32)]),
     "gm_members_launch_count": (C.c_int, [C.c_void_p, P(C.c_int32), P(C.c_int32), C.c_size_t, P(C.c_int32)]),
@@ -281,7 +302,7 @@ def check(status: int) -> None:
     """Map a gm_status to the Python exception of the matching reference class."""
     if status == GM_OK:
         return
-    msg = lib().gm_last_error().decode()
+    msg = lib().gm_last_error(None).decode()
     if status == GM_EINVAL:
         raise ValueError(msg)  # std::invalid_argument
     if status == GM_ENODEV:

@@ -5,11 +5,14 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/gpumux_b200.h"
 #include "planner.hpp"
 #include "sim.hpp"
+
+struct gm_ctx;
 
 namespace gmb {
 
@@ -30,6 +33,10 @@ struct RangeError : std::runtime_error {
 
 void set_error(const std::string& msg);
 int fail(int code, const char* what);
+// Classifies the in-flight exception (call inside a catch block) into a
+// gm_status, records its message as this thread's last error and, when ctx
+// is given, as that context's last error (gm_last_error(ctx)).
+int fail_current(const gm_ctx* ctx);
 
 inline Shape to_shape(const gm_gemm_shape& s) { return Shape{s.m, s.n, s.k}; }
 inline gm_gemm_shape from_shape(const Shape& s) { return gm_gemm_shape{s.m, s.n, s.k}; }
@@ -76,17 +83,19 @@ struct gm_ctx {
   int cuda_device = -1;
   std::uint64_t next_request_id = 1;
   gmb::Runtime* rt = nullptr;
+  std::int64_t clock0_ns = 0;           // steady-clock origin of gm_ctx_now_ns
+  std::unordered_map<std::uint64_t, gm_request_io> io;  // gm_enqueue I/O by request id
+  mutable std::string last_error;       // gm_last_error(ctx)
 };
 
 // Wraps an API body: maps C++ exceptions to status codes + gm_last_error().
+// GM_CTX_API_END(ctx) also records the message on that context.
 #define GM_API_BEGIN try {
-#define GM_API_END                                                        \
-  }                                                                       \
-  catch (const std::invalid_argument& e) { return gmb::fail(GM_EINVAL, e.what()); } \
-  catch (const gmb::RangeError& e) { return gmb::fail(GM_ERANGE, e.what()); }       \
-  catch (const gmb::CudaError& e) { return gmb::fail(GM_ECUDA, e.what()); }         \
-  catch (const gmb::NoDevice& e) { return gmb::fail(GM_ENODEV, e.what()); }         \
-  catch (const std::bad_alloc& e) { return gmb::fail(GM_EOOM, e.what()); }          \
-  catch (const std::exception& e) { return gmb::fail(GM_EINTERNAL, e.what()); }     \
-  catch (...) { return gmb::fail(GM_EINTERNAL, "unknown error"); }                  \
+#define GM_API_END                                         \
+  }                                                        \
+  catch (...) { return gmb::fail_current(nullptr); }       \
+  return GM_OK;
+#define GM_CTX_API_END(CTX)                                \
+  }                                                        \
+  catch (...) { return gmb::fail_current(CTX); }           \
   return GM_OK;

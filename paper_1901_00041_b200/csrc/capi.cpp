@@ -1,6 +1,7 @@
 // extern "C" boundary for the host-side planner, cost model, monitor, metrics
 // and the virtual-clock driver.  Device-side entry points live in runtime.cu.
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 
 #include "abi.hpp"
@@ -14,6 +15,29 @@ thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
 int fail(int code, const char* what) {
   g_last_error = what ? what : "";
+  return code;
+}
+
+int fail_current(const gm_ctx* ctx) {
+  int code = GM_EINTERNAL;
+  try {
+    throw;
+  } catch (const std::invalid_argument& e) {
+    code = fail(GM_EINVAL, e.what());
+  } catch (const RangeError& e) {
+    code = fail(GM_ERANGE, e.what());
+  } catch (const CudaError& e) {
+    code = fail(GM_ECUDA, e.what());
+  } catch (const NoDevice& e) {
+    code = fail(GM_ENODEV, e.what());
+  } catch (const std::bad_alloc& e) {
+    code = fail(GM_EOOM, e.what());
+  } catch (const std::exception& e) {
+    code = fail(GM_EINTERNAL, e.what());
+  } catch (...) {
+    code = fail(GM_EINTERNAL, "unknown error");
+  }
+  if (ctx) ctx->last_error = g_last_error;
   return code;
 }
 
@@ -143,7 +167,7 @@ using namespace gmb;
 
 extern "C" {
 
-const char* gm_last_error(void) { return g_last_error.c_str(); }
+const char* gm_last_error(const gm_ctx* ctx) { return ctx ? ctx->last_error.c_str() : g_last_error.c_str(); }
 int gm_abi_version(void) { return GM_ABI_VERSION; }
 
 void gm_device_spec_default(gm_device_spec* out) {
@@ -588,5 +612,73 @@ int gm_sim_trace_flops(const gm_sim_trace* t, int64_t* dispatched, int64_t* comp
 }
 
 void gm_sim_trace_destroy(gm_sim_trace* t) { delete t; }
+
+
+// ---- host-driven loop over one ctx (header: gm_enqueue .. gm_ctx_health) ----
+
+namespace {
+gmb::Health& health_of(gm_ctx* ctx, int32_t tenant, const char* who) {
+  if (tenant < 0 || tenant >= static_cast<int32_t>(ctx->health.size()))
+    throw std::invalid_argument(std::string(who) + ": unknown tenant " + std::to_string(tenant));
+  return ctx->health[static_cast<size_t>(tenant)];
+}
+}  // namespace
+
+int gm_ctx_form_batches(gm_ctx* ctx, int64_t now, gm_plans** out) {
+  GM_API_BEGIN
+  if (!ctx || !out) throw std::invalid_argument("null argument");
+  auto* p = new gm_plans();
+  try {
+    p->plans = form_plans(ctx->queue.q, now, ctx->pol, ctx->dev);
+  } catch (...) {
+    delete p;
+    throw;
+  }
+  *out = p;
+  GM_CTX_API_END(ctx)
+}
+
+int64_t gm_ctx_now_ns(const gm_ctx* ctx) {
+  const int64_t t = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                        std::chrono::steady_clock::now().time_since_epoch()).count();
+  return ctx ? t - ctx->clock0_ns : t;
+}
+
+int gm_ctx_record_latency(gm_ctx* ctx, int32_t tenant, double observed_seconds) {
+  GM_API_BEGIN
+  if (!ctx) throw std::invalid_argument("null context");
+  observe(health_of(ctx, tenant, "record_latency"), observed_seconds);  // scheduler.cpp:214-223
+  GM_CTX_API_END(ctx)
+}
+
+int gm_ctx_detect_stragglers(gm_ctx* ctx, int32_t* out, size_t cap, size_t* n) {
+  GM_API_BEGIN
+  if (!ctx || !n) throw std::invalid_argument("null argument");
+  const std::vector<int> s = stragglers(ctx->health, ctx->det.threshold_ratio, ctx->det.min_observations);  // :246-271
+  if (s.size() > cap) throw RangeError("detect_stragglers: " + std::to_string(s.size()) + " stragglers, cap " +
+                                       std::to_string(cap));
+  for (size_t i = 0; i < s.size(); ++i) out[i] = s[i];
+  *n = s.size();
+  GM_CTX_API_END(ctx)
+}
+
+int gm_ctx_evict(gm_ctx* ctx, int32_t tenant, uint64_t* cancelled_ids, size_t cap, size_t* n) {
+  GM_API_BEGIN
+  if (!ctx) throw std::invalid_argument("null context");
+  const std::vector<Request> gone = evict_tenant(ctx->health, ctx->queue.q, tenant);  // scheduler.cpp:225-244
+  for (size_t i = 0; i < gone.size(); ++i) {
+    ctx->io.erase(gone[i].id);
+    if (cancelled_ids && i < cap) cancelled_ids[i] = gone[i].id;
+  }
+  if (n) *n = gone.size();  // the eviction stands even when cap < *n (ids past cap are not written)
+  GM_CTX_API_END(ctx)
+}
+
+int gm_ctx_health(const gm_ctx* ctx, int32_t tenant, gm_tenant_health* out) {
+  GM_API_BEGIN
+  if (!ctx || !out) throw std::invalid_argument("null argument");
+  *out = from_health(health_of(const_cast<gm_ctx*>(ctx), tenant, "health"));
+  GM_CTX_API_END(ctx)
+}
 
 }  // extern "C"

@@ -95,6 +95,7 @@ struct Operator {
   int src = -1, res_src = -1;
   const char* y = nullptr;
   int64_t y_bytes = 0;
+  int64_t x_bytes = 0;           // extent of the input x (gm_request_io copies)
   int64_t x_pitch = 0;           // elements per input row (GEMM) or pixel (windowed ops)
   const char* res = nullptr;     // residual base and row stride (elements)
   int64_t ldr = 0;
@@ -137,8 +138,18 @@ struct Prepared {
   }
 };
 
+// One gm_dispatch awaiting gm_poll_completions: events bracket the
+// super-kernel (execution time) and the whole dispatch (copy-out included).
+struct InFlight {
+  cudaEvent_t exec0 = nullptr, exec1 = nullptr, done = nullptr;
+  std::vector<Request> members;
+  int64_t dispatch_ns = 0;
+};
+
 struct Runtime {
-  std::vector<gm_dispatch_event> serve_trace;  // the last gm_serve's dispatches (gm_serve_trace)
+  std::vector<gm_dispatch_event> serve_trace;
+  std::deque<InFlight> inflight;     // gm_dispatch -> gm_poll_completions
+  std::vector<cudaEvent_t> ev_pool;  // recycled timing events  // the last gm_serve's dispatches (gm_serve_trace)
   int device = -1;
   int sms = 0;
   int driver_version = 0;
@@ -192,6 +203,20 @@ struct Runtime {
     cudaFree(d_desc);
     cudaFree(ident);
     cudaFreeHost(host_one);
+    for (InFlight& f : inflight)
+      for (cudaEvent_t e : {f.exec0, f.exec1, f.done}) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+  }
+
+  cudaEvent_t take_event() {
+    if (!ev_pool.empty()) {
+      cudaEvent_t e = ev_pool.back();
+      ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
   }
 
   void init(int dev_index, const Device& spec) {
@@ -561,6 +586,11 @@ struct Runtime {
       op.y = static_cast<const char*>(L.y);
       op.y_bytes = op.shape.m * op.shape.n * 2;
       op.x_pitch = L.ldx > 0 ? L.ldx : (L.kind == GM_LAYER_GEMM ? op.shape.k : op.conv.in_channels);
+      {
+        const bool gemm = L.kind == GM_LAYER_GEMM;
+        const int64_t rows = gemm ? op.shape.m : op.batch * op.conv.image_h * op.conv.image_w;
+        op.x_bytes = ((rows - 1) * op.x_pitch + (gemm ? op.shape.k : op.conv.in_channels)) * 2;
+      }
       if (L.res) {
         op.res = static_cast<const char*>(L.res);
         op.ldr = L.ldr > 0 ? L.ldr : op.shape.n;
@@ -1249,6 +1279,8 @@ int gm_create(const gm_device_spec* d, const gm_batch_policy* p, const gm_detect
     if (p) ctx->pol = to_policy(*p);
     if (det) ctx->det = to_detector(*det);
     ctx->cuda_device = cuda_device;
+    ctx->clock0_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                         std::chrono::steady_clock::now().time_since_epoch()).count();
     if (cuda_device >= 0) {
       ctx->rt = new Runtime();
       ctx->rt->init(cuda_device, ctx->dev);
@@ -1273,21 +1305,21 @@ int gm_ctx_queue(gm_ctx* ctx, gm_queue** q) {
   GM_API_BEGIN
   if (!ctx || !q) throw std::invalid_argument("null argument");
   *q = &ctx->queue;
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_ctx_cache(gm_ctx* ctx, gm_cache** c) {
   GM_API_BEGIN
   if (!ctx || !c) throw std::invalid_argument("null argument");
   *c = &ctx->cache;
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_ctx_device_spec(const gm_ctx* ctx, gm_device_spec* out) {
   GM_API_BEGIN
   if (!ctx || !out) throw std::invalid_argument("null argument");
   *out = from_device(ctx->dev);
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_ctx_set_option(gm_ctx* ctx, const char* name, int64_t value) {
@@ -1332,14 +1364,14 @@ int gm_ctx_set_option(gm_ctx* ctx, const char* name, int64_t value) {
   } else {
     throw std::invalid_argument("unknown option " + n);
   }
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_ctx_set_policy(gm_ctx* ctx, const gm_batch_policy* p) {
   GM_API_BEGIN
   if (!ctx || !p) throw std::invalid_argument("null argument");
   ctx->pol = to_policy(*p);
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_register_tenant(gm_ctx* ctx, const gm_tenant_desc* t, int32_t* tenant_index) {
@@ -1353,21 +1385,21 @@ int gm_register_tenant(gm_ctx* ctx, const gm_tenant_desc* t, int32_t* tenant_ind
   h.alpha = ctx->det.ewma_alpha;
   ctx->health.push_back(h);
   if (tenant_index) *tenant_index = idx;
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_layer_shape(gm_ctx* ctx, int32_t tenant, int32_t layer, gm_gemm_shape* out) {
   GM_API_BEGIN
   if (!out) throw std::invalid_argument("null argument: out");
   *out = from_shape(runtime_of(ctx).op_of(tenant, layer).shape);
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_tenant_count(const gm_ctx* ctx, int32_t* n) {
   GM_API_BEGIN
   if (!ctx || !n) throw std::invalid_argument("null argument");
   *n = ctx->rt ? static_cast<int32_t>(ctx->rt->tenant_ops.size()) : 0;
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_prepare(gm_ctx* ctx, const gm_plans* p, size_t i) {
@@ -1376,7 +1408,7 @@ int gm_prepare(gm_ctx* ctx, const gm_plans* p, size_t i) {
   Runtime& rt = runtime_of(ctx);
   cuda_check(cudaSetDevice(rt.device), "cudaSetDevice");
   rt.prepare(members_of(rt, p->plans[i]));
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_dispatch(gm_ctx* ctx, const gm_plans* p, size_t i, uint64_t stream, double* planned_s, int* cache_hit) {
@@ -1384,13 +1416,134 @@ int gm_dispatch(gm_ctx* ctx, const gm_plans* p, size_t i, uint64_t stream, doubl
   if (!p || i >= p->plans.size()) throw std::invalid_argument("plan index out of range");
   Runtime& rt = runtime_of(ctx);
   const Plan& plan = p->plans[i];
-  Prepared& prep = rt.prepare(members_of(rt, plan));
+  const std::vector<int> ops = members_of(rt, plan);
+  Prepared& prep = rt.prepare(ops);
   const int64_t misses = ctx->cache.c.misses;
   const double dur = charge(plan, ctx->cache.c, ctx->dev);
-  rt.launch(prep, reinterpret_cast<cudaStream_t>(stream));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaStreamCaptureStatus capturing = cudaStreamCaptureStatusNone;
+  cuda_check(cudaStreamIsCapturing(s, &capturing), "cudaStreamIsCapturing");
+  const bool track = capturing == cudaStreamCaptureStatusNone;
+  // request I/O (gm_enqueue): query inputs land right before the launch
+  auto io_of = [&](const Request& r) -> const gm_request_io* {
+    auto it = ctx->io.find(r.id);
+    return it == ctx->io.end() ? nullptr : &it->second;
+  };
+  for (size_t j = 0; j < plan.members.size(); ++j)
+    if (const gm_request_io* io = io_of(plan.members[j]); io && io->x && io->x_bytes)
+      cuda_check(cudaMemcpyAsync(const_cast<void*>(rt.flat[ops[j]].x), io->x, io->x_bytes, cudaMemcpyDefault, s),
+                 "request input copy");
+  InFlight f;
+  if (track) {
+    f.exec0 = rt.take_event();
+    f.exec1 = rt.take_event();
+    f.done = rt.take_event();
+    cuda_check(cudaEventRecord(f.exec0, s), "cudaEventRecord");
+  }
+  rt.launch(prep, s);
+  if (track) cuda_check(cudaEventRecord(f.exec1, s), "cudaEventRecord");
+  for (size_t j = 0; j < plan.members.size(); ++j)
+    if (const gm_request_io* io = io_of(plan.members[j]); io && io->y && io->y_bytes)
+      cuda_check(cudaMemcpyAsync(io->y, rt.flat[ops[j]].y, io->y_bytes, cudaMemcpyDefault, s), "request output copy");
+  if (track) {
+    cuda_check(cudaEventRecord(f.done, s), "cudaEventRecord");
+    f.members = plan.members;
+    f.dispatch_ns = gm_ctx_now_ns(ctx);
+    rt.inflight.push_back(std::move(f));
+  }
   if (planned_s) *planned_s = dur;
   if (cache_hit) *cache_hit = ctx->cache.c.misses == misses ? 1 : 0;
+  GM_CTX_API_END(ctx)
+}
+
+int gm_enqueue(gm_ctx* ctx, const gm_kernel_request* r, const gm_request_io* io) {
+  GM_API_BEGIN
+  if (!ctx || !r) throw std::invalid_argument("null argument");
+  const Request req = to_request(*r);
+  const bool has_io = io && ((io->x && io->x_bytes) || (io->y && io->y_bytes));
+  if (ctx->rt) {
+    const Operator& op = ctx->rt->op_of(req.tenant, req.layer);
+    if (req.shape.valid() && !(op.shape == req.shape))
+      throw std::invalid_argument("enqueue: request shape " + key_of(req.shape) + " does not match tenant " +
+                                  std::to_string(req.tenant) + " layer " + std::to_string(req.layer) + " (" +
+                                  key_of(op.shape) + ")");
+    if (has_io && io->x && static_cast<int64_t>(io->x_bytes) > op.x_bytes)
+      throw std::invalid_argument("enqueue: input copy of " + std::to_string(io->x_bytes) +
+                                  " bytes exceeds the layer's input (" + std::to_string(op.x_bytes) + ")");
+    if (has_io && io->y && static_cast<int64_t>(io->y_bytes) > op.y_bytes)
+      throw std::invalid_argument("enqueue: output copy of " + std::to_string(io->y_bytes) +
+                                  " bytes exceeds the layer's output (" + std::to_string(op.y_bytes) + ")");
+  } else if (has_io) {
+    throw NoDevice("context has no CUDA device (created with cuda_device < 0): request I/O needs one");
+  }
+  ctx->queue.q.push(req);  // scheduler.cpp:8-16 (duplicate id / invalid shape texts)
+  if (has_io) ctx->io[req.id] = *io;
+  if (!ctx->rt && req.tenant >= 0)
+    while (static_cast<int>(ctx->health.size()) <= req.tenant) {
+      Health h;
+      h.tenant = static_cast<int>(ctx->health.size());
+      h.alpha = ctx->det.ewma_alpha;
+      ctx->health.push_back(h);
+    }
+  GM_CTX_API_END(ctx)
+}
+
+int gm_poll_completions(gm_ctx* ctx, gm_completion* out, size_t cap, size_t* n) {
+  GM_API_BEGIN
+  if (!n) throw std::invalid_argument("null argument: n");
+  Runtime& rt = runtime_of(ctx);
+  *n = 0;
+  size_t written = 0;
+  for (auto it = rt.inflight.begin(); it != rt.inflight.end();) {
+    const cudaError_t q = cudaEventQuery(it->done);
+    if (q == cudaErrorNotReady) {
+      ++it;
+      continue;
+    }
+    cuda_check(q, "dispatch completion");
+    if (written + it->members.size() > cap) {
+      if (written == 0) throw RangeError("poll_completions: a finished dispatch has " +
+                                         std::to_string(it->members.size()) + " members, cap " + std::to_string(cap));
+      break;
+    }
+    float ms = 0;
+    cuda_check(cudaEventElapsedTime(&ms, it->exec0, it->exec1), "cudaEventElapsedTime");
+    const int64_t now = gm_ctx_now_ns(ctx);
+    for (const Request& r : it->members) {
+      gm_completion& c = out[written++];
+      c.request_id = r.id;
+      c.tenant_index = r.tenant;
+      c.layer_index = r.layer;
+      c.pass_index = r.pass;
+      c.batch = r.batch;
+      c.enqueue_time = r.enqueue;
+      c.slo_deadline = r.deadline;
+      c.dispatch_ns = it->dispatch_ns;
+      c.complete_ns = now;
+      c.exec_seconds = static_cast<double>(ms) * 1e-3;
+      c.plan_members = static_cast<int32_t>(it->members.size());
+      c.reserved0 = 0;
+      ctx->io.erase(r.id);
+    }
+    for (cudaEvent_t e : {it->exec0, it->exec1, it->done}) rt.ev_pool.push_back(e);
+    it = rt.inflight.erase(it);
+  }
+  *n = written;
+  GM_CTX_API_END(ctx)
+}
+
+int gm_ctx_in_flight(const gm_ctx* ctx, size_t* n) {
+  GM_API_BEGIN
+  if (!ctx || !n) throw std::invalid_argument("null argument");
+  *n = ctx->rt ? ctx->rt->inflight.size() : 0;
   GM_API_END
+}
+
+int gm_ctx_synchronize(gm_ctx* ctx) {
+  GM_API_BEGIN
+  Runtime& rt = runtime_of(ctx);
+  for (const InFlight& f : rt.inflight) cuda_check(cudaEventSynchronize(f.done), "cudaEventSynchronize");
+  GM_CTX_API_END(ctx)
 }
 
 int gm_launch_members(gm_ctx* ctx, const int32_t* tenants, const int32_t* layers, size_t n, uint64_t stream,
@@ -1402,7 +1555,7 @@ int gm_launch_members(gm_ctx* ctx, const int32_t* tenants, const int32_t* layers
   for (size_t j = 0; j < n; ++j) members.push_back(rt.flat_index(tenants[j], layers[j]));
   const int l = rt.launch(rt.prepare(members), reinterpret_cast<cudaStream_t>(stream));
   if (launches) *launches = l;
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_members_launch_count(gm_ctx* ctx, const int32_t* tenants, const int32_t* layers, size_t n, int32_t* launches) {
@@ -1413,7 +1566,7 @@ int gm_members_launch_count(gm_ctx* ctx, const int32_t* tenants, const int32_t* 
   for (size_t j = 0; j < n; ++j)
     if (rt.op_of(tenants[j], layers[j]).prepass) ops.push_back(rt.flat_index(tenants[j], layers[j]));
   *launches = 1 + rt.prepass_launches(ops);
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_plan_round(gm_ctx* ctx, const int32_t* tenants, size_t n, int64_t now, gm_plans** out) {
@@ -1439,7 +1592,7 @@ int gm_plan_round(gm_ctx* ctx, const int32_t* tenants, size_t n, int64_t now, gm
     plans->times.emplace_back(d.start, d.end);
   }
   *out = plans;
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_plans_times(const gm_plans* p, size_t i, int64_t* start, int64_t* end) {
@@ -1456,7 +1609,7 @@ int gm_prepare_plans(gm_ctx* ctx, const gm_plans* p) {
   Runtime& rt = runtime_of(ctx);
   cuda_check(cudaSetDevice(rt.device), "cudaSetDevice");
   for (const Plan& plan : p->plans) rt.prepare(members_of(rt, plan));
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_dispatch_plans(gm_ctx* ctx, const gm_plans* p, uint64_t stream, int32_t* launches) {
@@ -1466,7 +1619,7 @@ int gm_dispatch_plans(gm_ctx* ctx, const gm_plans* p, uint64_t stream, int32_t* 
   int l = 0;
   for (const Plan& plan : p->plans) l += rt.launch(rt.prepare(members_of(rt, plan)), reinterpret_cast<cudaStream_t>(stream));
   if (launches) *launches = l;
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_graph_capture_plans(gm_ctx* ctx, const gm_plans* p, int timed, gm_graph** out) {
@@ -1483,7 +1636,7 @@ int gm_graph_capture_plans(gm_ctx* ctx, const gm_plans* p, int timed, gm_graph**
       g.tiles += pr->n_tiles;
     }
   });
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_graph_capture_serial(gm_ctx* ctx, const int32_t* tenants, size_t n, int mode, int timed, gm_graph** out) {
@@ -1533,7 +1686,7 @@ int gm_graph_capture_serial(gm_ctx* ctx, const int32_t* tenants, size_t n, int m
     }
     for (cudaEvent_t e : done) cuda_check(cudaStreamWaitEvent(cs, e, 0), "cudaStreamWaitEvent");
   });
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_dispatch_round(gm_ctx* ctx, const gm_plans* p, uint64_t stream, int32_t* launches) {
@@ -1544,7 +1697,7 @@ int gm_dispatch_round(gm_ctx* ctx, const gm_plans* p, uint64_t stream, int32_t* 
   for (const Plan& plan : p->plans) plans.push_back(members_of(rt, plan));
   const int l = rt.launch(rt.prepare_round(plans), reinterpret_cast<cudaStream_t>(stream));
   if (launches) *launches = l;
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_trace_round(gm_ctx* ctx, const gm_plans* p, uint64_t stream, uint64_t* out, size_t cap, size_t* n_tiles) {
@@ -1570,7 +1723,7 @@ int gm_trace_round(gm_ctx* ctx, const gm_plans* p, uint64_t stream, uint64_t* ou
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   cudaFree(d_trace);
   cuda_check(e, "trace copy");
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_round_tiles(gm_ctx* ctx, const gm_plans* p, gm_tile* out, size_t cap, size_t* n) {
@@ -1589,7 +1742,7 @@ int gm_round_tiles(gm_ctx* ctx, const gm_plans* p, gm_tile* out, size_t cap, siz
   if (n) *n = v.size();
   if (!out || cap < v.size()) throw RangeError("output buffer too small");
   std::copy(v.begin(), v.end(), out);
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_round_tile_info(gm_ctx* ctx, const gm_plans* p, gm_round_tile* out, size_t cap, size_t* n) {
@@ -1628,7 +1781,7 @@ int gm_round_tile_info(gm_ctx* ctx, const gm_plans* p, gm_round_tile* out, size_
     o.plan = pr.tile_plan[i];
     o.cuda_core = dev::cuda_core_mode(md.a_mode) ? 1 : 0;
   }
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_graph_capture_round(gm_ctx* ctx, const gm_plans* p, int timed, gm_graph** out) {
@@ -1644,7 +1797,7 @@ int gm_graph_capture_round(gm_ctx* ctx, const gm_plans* p, int timed, gm_graph**
     g.superkernels += 1;
     g.tiles += pr->n_tiles;
   });
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_graph_capture_round_e2e(gm_ctx* ctx, const gm_plans* p, size_t n, const int32_t* tenants,
@@ -1748,7 +1901,7 @@ int gm_graph_capture_round_e2e(gm_ctx* ctx, const gm_plans* p, size_t n, const i
     for (size_t i = 0; i < n; ++i)
       cuda_check(cudaMemcpyAsync(h_out[i], d_out[i], out_bytes[i], cudaMemcpyDeviceToHost, cs), "D2H result");
   });
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_serve_trace(gm_ctx* ctx, gm_dispatch_event* out, size_t cap, size_t* n) {
@@ -1758,7 +1911,7 @@ int gm_serve_trace(gm_ctx* ctx, gm_dispatch_event* out, size_t cap, size_t* n) {
   if (!out) return GM_OK;
   if (cap < rt.serve_trace.size()) throw RangeError("output buffer too small");
   std::copy(rt.serve_trace.begin(), rt.serve_trace.end(), out);
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 int gm_graph_launch(gm_graph* g, uint64_t stream) {
@@ -1802,7 +1955,7 @@ int gm_ctx_launch_stats(const gm_ctx* ctx, int64_t* superkernels, int64_t* prepa
   if (superkernels) *superkernels = rt ? rt->n_superkernels : 0;
   if (prepasses) *prepasses = rt ? rt->n_prepasses : 0;
   if (tiles) *tiles = rt ? rt->n_tiles : 0;
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }
 
 }  // extern "C"
@@ -2144,5 +2297,5 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
   out->evicted_mask = evicted_mask;
   if (n_lat) *n_lat = lat_ms.size();
   if (latencies_ms && cap) std::copy(lat_ms.begin(), lat_ms.begin() + std::min(cap, lat_ms.size()), latencies_ms);
-  GM_API_END
+  GM_CTX_API_END(ctx)
 }

@@ -28,7 +28,7 @@ def test_ctypes_signatures_cover_the_header():
 
 def test_abi_version_and_host_only_context():
     lib = _native.lib()
-    assert lib.gm_abi_version() == 2
+    assert lib.gm_abi_version() == 3
     h = ctypes.c_void_p()
     assert lib.gm_create(None, None, None, -1, ctypes.byref(h)) == 0  # host-only: planner without a GPU
     q = ctypes.c_void_p()
@@ -38,7 +38,8 @@ def test_abi_version_and_host_only_context():
     assert lib.gm_register_tenant(h, None, ctypes.byref(n)) == _native.GM_EINVAL
     assert lib.gm_launch_members(h, (ctypes.c_int32 * 1)(0), (ctypes.c_int32 * 1)(0), 1, 0, None) == \
         _native.GM_ENODEV
-    assert b"no CUDA device" in lib.gm_last_error() or b"context has no CUDA device" in lib.gm_last_error()
+    assert b"context has no CUDA device" in lib.gm_last_error(None)
+    assert b"context has no CUDA device" in lib.gm_last_error(h)  # per-ctx error channel
     # the serving loop needs the device runtime too
     t = _native.gm_serve_tenant(1, (ctypes.c_int32 * 1)(0), (ctypes.c_int32 * 1)(1), 0.0, 1, 0, 0.04, 1)
     cfg = _native.gm_serve_config(1.0, 0.1, -1.0, 42, 1, 0, 0)
