@@ -99,7 +99,14 @@ struct Operator {
   int64_t x_pitch = 0;           // elements per input row (GEMM) or pixel (windowed ops)
   const char* res = nullptr;     // residual base and row stride (elements)
   int64_t ldr = 0;
+  int64_t cc_rows = 0;  // staged CUDA-core tile: output pixels per tile (0 = register-path tile)
 };
+
+// Rows (output pixels) per tile of an operator's descriptor variant.
+int64_t tile_rows_of(const Operator& op, bool tall) {
+  if (cuda_core_kind(op.kind)) return op.cc_rows > 0 ? op.cc_rows : cuda_core_rows(op.kind);
+  return int64_t{dev::kBM} << (tall ? 1 : 0);
+}
 
 struct Prepared {
   dev::TileEntry* tiles = nullptr;
@@ -177,6 +184,7 @@ struct Runtime {
   int64_t narrow_min_tiles = 20;  // >0: in a plan that cannot fill the SMs, narrow a member's N tile
                                  // (256 -> 128 -> 64) until it has this many tiles
   bool row_fold = true;          // S*Cin <= 32 convs (RGB stems) use the row-folded im2col path
+  bool staged_cc = true;         // pools / depthwise convs as staged CUDA-core tiles (applies at registration)
   bool dynamic_schedule = false;  // round programs: per-tenant ready queues (else static round-robin)
   bool greedy_schedule = false;   // round programs: greedy in-order tile claiming (else static round-robin)
   bool tall_tiles = true;         // 256-row tiles for narrow members of throughput-bound plans
@@ -256,9 +264,62 @@ struct Runtime {
     }
   }
 
+  // Staged CUDA-core tile geometry (pools, depthwise convs): a tile is `ro`
+  // whole output rows of one image x `cc` channels, and its input window --
+  // box {cc, (Q-1)*stride+S, (ro-1)*stride+R, 1} of the NHWC input -- lands in
+  // one ring slot (<= kCcStageBytes) by a single TMA load.  cc: a power of two
+  // >= 8 dividing C (16-byte channel groups; at most 32 groups), preferring
+  // >= 32 channels (64-byte box rows); then the most output work per tile.
+  // Ops no box fits keep the register-path tile.
+  void stage_cuda_core(Operator& op, dev::MemberDesc& md, const void* x) {
+    op.cc_rows = 0;
+    md.cc_rows = 0;
+    if (!staged_cc) return;
+    const Conv& c = op.conv;
+    const int64_t C = c.in_channels, P = md.pq / md.q, Q = md.q;
+    const int64_t Wb = (Q - 1) * c.stride + c.kernel_w;
+    if (op.x_pitch % 8 != 0 || Wb > 256 || !aligned16(x)) return;
+    int64_t best_cc = 0, best_ro = 0, best_work = 0;
+    const int64_t want_cc = std::min<int64_t>(C, 32);
+    for (int pass = 0; pass < 2 && best_cc == 0; ++pass)
+      for (int64_t cc = 256; cc >= 8; cc /= 2) {
+        if (C % cc != 0 || (pass == 0 && cc < want_cc)) continue;
+        for (int64_t ro = 1; ro <= P; ++ro) {
+          if (P % ro != 0) continue;
+          const int64_t Hb = (ro - 1) * c.stride + c.kernel_h;
+          if (Hb > 256 || cc * Wb * Hb * 2 > dev::kCcStageBytes) break;
+          if (ro * Q * cc > best_work) {
+            best_work = ro * Q * cc;
+            best_cc = cc;
+            best_ro = ro;
+          }
+        }
+      }
+    if (best_cc == 0) return;
+    const int64_t Hb = (best_ro - 1) * c.stride + c.kernel_h;
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(c.image_w),
+                                static_cast<cuuint64_t>(c.image_h), static_cast<cuuint64_t>(op.batch)};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(op.x_pitch * 2),
+                                   static_cast<cuuint64_t>(op.x_pitch * 2 * c.image_w),
+                                   static_cast<cuuint64_t>(op.x_pitch * 2 * c.image_w * c.image_h)};
+    const cuuint32_t box[4] = {static_cast<cuuint32_t>(best_cc), static_cast<cuuint32_t>(Wb),
+                               static_cast<cuuint32_t>(Hb), 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = encode_tiled(&md.a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, box,
+                                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (staged CUDA-core input) failed (" +
+                                           std::to_string(int(r)) + ")");
+    op.n_tile = static_cast<int>(best_cc);
+    op.cc_rows = best_ro * Q;
+    md.cc_rows = static_cast<int32_t>(best_ro);
+    md.tx_bytes = static_cast<uint32_t>(best_cc * Wb * Hb * 2);
+  }
+
   // A member's k-block stage (A region + B box) fits a 32 KB narrow-layout slot.
   int ring_narrow_of(const dev::MemberDesc& md, int b_rows) const {
     if (ring_layouts == 0) return 0;
+    if (md.cc_rows > 0) return 1;  // a staged CUDA-core box is <= kCcStageBytes
     const bool cols = md.a_mode == dev::kAIm2colNarrow || md.a_mode == dev::kAIm2colFold;
     const int a_bytes = cols ? dev::kABytes : a_box_rows(md.m) * dev::kBK * 2;
     return a_bytes + b_rows * dev::kBK * 2 <= 32768 ? 1 : 0;
@@ -555,7 +616,7 @@ struct Runtime {
         throw std::invalid_argument("register_tenant: unknown layer kind");
       }
       if (op.shape.n % 8 != 0) throw std::invalid_argument("register_tenant: output channels must be a multiple of 8");
-      if (op.shape.m > int64_t(0xFFFF) * (cuda_core_kind(op.kind) ? cuda_core_rows(op.kind) : dev::kBM) ||
+      if (op.shape.m > int64_t(0xFFFF) * (cuda_core_kind(op.kind) ? dev::kDwTileM : dev::kBM) ||
           op.shape.m > INT32_MAX)
         throw std::invalid_argument("register_tenant: M too large for the tile table");
       store_map(&md.c, L.y, op.shape.m, op.shape.n);
@@ -595,6 +656,7 @@ struct Runtime {
         op.res = static_cast<const char*>(L.res);
         op.ldr = L.ldr > 0 ? L.ldr : op.shape.n;
       }
+      if (cuda_core_kind(op.kind)) stage_cuda_core(op, md, L.x);
       md.n_tile = op.n_tile;
       md.ring_narrow = ring_narrow_of(md, b_box_rows(op.shape.n, op.n_tile));
       op.slot = static_cast<int>(host_desc.size() + descs.size());
@@ -732,7 +794,7 @@ struct Runtime {
     for (int f : members) {
       const Operator& op = flat[f];
       const auto [slot, w] = variant(f, plan_tiles, plan_tiles);
-      const int64_t tm = cuda_core_kind(op.kind) ? cuda_core_rows(op.kind) : dev::kBM << (is_tall(slot) ? 1 : 0);
+      const int64_t tm = tile_rows_of(op, is_tall(slot));
       const int64_t mt = (op.shape.m + tm - 1) / tm;
       const int64_t nt = (op.shape.n + w - 1) / w;
       for (int64_t a = 0; a < mt; ++a)
@@ -864,7 +926,7 @@ struct Runtime {
             res_op = &flat[it2->first];
           }
         }
-        const int64_t tm = cuda_core_kind(op.kind) ? cuda_core_rows(op.kind) : dev::kBM << (tall ? 1 : 0);
+        const int64_t tm = tile_rows_of(op, tall);
         const int64_t mt = (op.shape.m + tm - 1) / tm;
         const int64_t nt = (op.shape.n + w - 1) / w;
         // this instance's counters come after any gate counter pushed above
@@ -899,9 +961,10 @@ struct Runtime {
           splits = (kb + chunk - 1) / chunk;
         }
         // one counter per row block: 4 epilogue warps arrive per output tile
-        // (8 for a CUDA-core tile: all of them compute it), nt tiles per block
-        for (int64_t a = 0; a < mt; ++a)
-          targets.push_back(static_cast<uint32_t>(nt * (cuda_core_kind(op.kind) ? 8 : 4)));
+        // (8 for a register-path CUDA-core tile: all of them compute it; 1 for
+        // a staged one: its warpgroup publishes once), nt tiles per block
+        const int per_tile = !cuda_core_kind(op.kind) ? 4 : op.cc_rows > 0 ? 1 : 8;
+        for (int64_t a = 0; a < mt; ++a) targets.push_back(static_cast<uint32_t>(nt * per_tile));
         for (int64_t a = 0; a < mt; ++a) {
           const auto [dep, dep_n] = deps_of(a, false);
           const auto [rdep, rdep_n] = deps_of(a, true);
@@ -1359,6 +1422,9 @@ int gm_ctx_set_option(gm_ctx* ctx, const char* name, int64_t value) {
     rt.greedy_schedule = value != 0;  // applies to round programs prepared afterwards
   } else if (n == "narrow_min_tiles") {
     rt.narrow_min_tiles = value;  // applies to plans prepared afterwards (0 = always full width)
+  } else if (n == "staged_cc") {
+    rt.staged_cc = value != 0;  // applies to tenants registered afterwards
+
   } else if (n == "row_fold") {
     rt.row_fold = value != 0;  // applies to tenants registered afterwards
   } else {
@@ -1766,10 +1832,8 @@ int gm_round_tile_info(gm_ctx* ctx, const gm_plans* p, gm_round_tile* out, size_
     o.layer = op.layer;
     o.m_tile = te.m_tile;
     o.n_tile = te.n_tile;
-    o.rows = md.a_mode == dev::kDepthwise ? dev::kDwTileM
-             : dev::cuda_core_mode(md.a_mode) ? dev::kPoolTileM
-                                              : (md.tall ? 2 * dev::kBM : dev::kBM);
-    o.cols = dev::cuda_core_mode(md.a_mode) ? dev::kDwTileC : md.n_tile;
+    o.rows = static_cast<int32_t>(tile_rows_of(op, md.tall != 0));
+    o.cols = md.n_tile;
     o.splits = te.splits > 1 ? te.splits : 1;
     o.kb_begin = te.kb_begin;
     o.kb_end = te.kb_end;

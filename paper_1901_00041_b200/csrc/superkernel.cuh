@@ -49,7 +49,7 @@ struct Cfg {
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;
-  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 512 /*barriers, tile ring*/;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 1024 /*barriers, tile ring*/;
   // Two ring layouts over the same bytes: wide (kStages slots of kStageBytes)
   // and narrow (32 KB slots) for members whose stage fits in 32 KB (N tile
   // <= 128), which then keep more k-blocks in flight -- their k-block rate
@@ -142,6 +142,13 @@ struct alignas(128) MemberDesc {
   // producer gates on; it enters the accumulator through maps r / id.
   const __nv_bfloat16* res;
   int32_t ldr;
+  // Staged CUDA-core tiles (pools, depthwise; 0 = register path): output rows
+  // per tile.  The producer lands a tile's whole input window -- box
+  // {n_tile channels, (q-1)*stride+S columns, (cc_rows-1)*stride+R rows, 1
+  // image} of the NHWC input through map `a` -- in one operand-ring stage
+  // (tx_bytes <= kCcStageBytes), so the loads of later tiles stream while
+  // one epilogue warpgroup computes this one from shared memory.
+  int32_t cc_rows;
 };
 
 // Device tile-table entry; `member` is the registered slot index.
@@ -199,7 +206,10 @@ struct RoundArgs {
 
 constexpr int kTileQ = 8;   // claimed-tile ring between producer and consumers
 constexpr int kDwTag = 1 << 30;  // tile-ring tag: a depthwise tile (no TMA / MMA work)
+constexpr int kStagedTag = 1 << 29;  // with kDwTag: a staged CUDA-core tile (one ring stage, no MMA)
+constexpr int kCcStageBytes = 32768;  // a staged CUDA-core tile's input box fits either ring layout's slot
 constexpr int kSchedQ = 2;  // scheduler look-ahead: tiles claimed before the producer needs them
+constexpr int kPubQ = 4;    // per epilogue warpgroup: staged-tile publishes queued for the publisher warp
 
 __device__ __forceinline__ bool elect_one() {
   uint32_t p = 0;
@@ -266,6 +276,18 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   uint32_t done = 0;
@@ -297,6 +319,26 @@ __device__ __forceinline__ void tma_load_im2col(void* dst, const CUtensorMap* ma
       "[%2], {%7, %8};" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(off_w), "h"(off_h)
       : "memory");
+}
+
+// 4-D tiled box {c, w, h, n} (signed start; out-of-bounds elements zero-fill).
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c, int32_t w,
+                                            int32_t h, int32_t n) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n)
+      : "memory");
+}
+
+// Release-add on a round counter (orders the prior writes this thread observed,
+// including those of threads it synchronised with through a barrier).
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void named_barrier(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c0, int32_t c1) {
@@ -571,6 +613,142 @@ __device__ __forceinline__ void pool_tile(const MemberDesc* __restrict__ md, con
   }
 }
 
+// Staged CUDA-core tiles.  The tile is output rows [p0, p0 + cc_rows) x all
+// q columns of one image, channels [c0, c0 + n_tile); its input window sits in
+// shared memory as [Hb][Wb][n_tile] bf16 (the TMA box, zero outside the
+// image).  128 threads (one epilogue warpgroup): each owns one 8-channel group
+// (16 B) of a pixel; n_tile / 8 is a power of two <= 32, so a thread keeps its
+// channel group across pixels.  Max pooling skips taps outside the image (torch
+// MaxPool2d); average pooling and depthwise convs sum the zero fill (the
+// reference divides by R*S).  fp32 accumulation, fused activation, bf16 out.
+struct StagedGeom {
+  int cc, lg, Q, st, S, R, Wb, m0, h0, w0, c;
+};
+
+__device__ __forceinline__ StagedGeom staged_geom(const MemberDesc* __restrict__ md, const TileEntry& te, int gt) {
+  StagedGeom g;
+  g.cc = md->n_tile;
+  g.lg = __ffs(g.cc >> 3) - 1;  // log2(channel groups)
+  g.Q = md->q;
+  g.st = md->stride;
+  g.S = md->s_taps;
+  g.R = md->r_taps / g.S;
+  g.Wb = (g.Q - 1) * g.st + g.S;
+  g.m0 = te.m_tile * md->cc_rows * g.Q;
+  const int img = g.m0 / md->pq;
+  g.h0 = (g.m0 - img * md->pq) / g.Q * g.st - md->pad;
+  g.w0 = -md->pad;
+  g.c = te.n_tile * g.cc + (gt & ((1 << g.lg) - 1)) * 8;
+  return g;
+}
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4 v, float (&f)[8]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    f[2 * e] = __uint_as_float(w[e] << 16);
+    f[2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+  }
+}
+
+__device__ __forceinline__ void store_bf16x8(__nv_bfloat16* dst, const float (&a)[8], float scale, Clamp ck) {
+  uint4 o;
+  o.x = pack_bf16(__float_as_uint(a[0] * scale), __float_as_uint(a[1] * scale), ck);
+  o.y = pack_bf16(__float_as_uint(a[2] * scale), __float_as_uint(a[3] * scale), ck);
+  o.z = pack_bf16(__float_as_uint(a[4] * scale), __float_as_uint(a[5] * scale), ck);
+  o.w = pack_bf16(__float_as_uint(a[6] * scale), __float_as_uint(a[7] * scale), ck);
+  *reinterpret_cast<uint4*>(dst) = o;
+}
+
+__device__ __forceinline__ void staged_pool_tile(const MemberDesc* __restrict__ md, const TileEntry& te,
+                                                 const uint8_t* src, int gt) {
+  const StagedGeom g = staged_geom(md, te, gt);
+  const int H = md->h_in, W = md->w_in, C = md->ch;
+  const int npix = md->cc_rows * g.Q;
+  const bool mx = md->a_mode == kMaxPool;
+  const float scale = mx ? 1.f : 1.f / static_cast<float>(md->r_taps);
+  const Clamp ck = clamp_of(md->act);
+  const int row_bytes = g.Wb * g.cc * 2;
+  const uint8_t* base0 = src + (gt & ((1 << g.lg) - 1)) * 16;
+  for (int px = gt >> g.lg; px < npix; px += 128 >> g.lg) {
+    const int pr = px / g.Q, qc = px - pr * g.Q;
+    const int ih0 = g.h0 + pr * g.st, iw0 = g.w0 + qc * g.st;
+    const uint8_t* base = base0 + pr * g.st * row_bytes + qc * g.st * g.cc * 2;
+    float acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = mx ? -INFINITY : 0.f;
+    for (int r = 0; r < g.R; ++r) {
+      const bool rok = ih0 + r >= 0 && ih0 + r < H;
+      if (mx && !rok) continue;
+      const uint8_t* rowp = base + r * row_bytes;
+#pragma unroll 4
+      for (int s = 0; s < g.S; ++s) {
+        if (mx && (iw0 + s < 0 || iw0 + s >= W)) continue;
+        float f[8];
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(rowp + s * g.cc * 2), f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = mx ? fmaxf(acc[e], f[e]) : acc[e] + f[e];
+      }
+    }
+    store_bf16x8(md->dy + static_cast<int64_t>(g.m0 + px) * C + g.c, acc, scale, ck);
+  }
+}
+
+__device__ __forceinline__ void staged_dw_tile(const MemberDesc* __restrict__ md, const TileEntry& te,
+                                               const uint8_t* src, int gt) {
+  const StagedGeom g = staged_geom(md, te, gt);
+  const int C = md->ch;
+  const int npix = md->cc_rows * g.Q;
+  const Clamp ck = clamp_of(md->act);
+  const int row_bytes = g.Wb * g.cc * 2;
+  const uint8_t* base0 = src + (gt & ((1 << g.lg) - 1)) * 16;
+  const __nv_bfloat16* wp = md->dw + static_cast<int64_t>(g.c) * md->ldw;
+  if (g.R == 3 && g.S == 3) {
+    // 3x3 (every depthwise layer of MobileNet-v2): this thread's 8 channels x
+    // 9 taps in registers, taps unrolled
+    float wv[9][8];
+#pragma unroll
+    for (int k = 0; k < 9; ++k)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) wv[k][j] = __bfloat162float(wp[j * md->ldw + k]);
+    for (int px = gt >> g.lg; px < npix; px += 128 >> g.lg) {
+      const int pr = px / g.Q, qc = px - pr * g.Q;
+      const uint8_t* base = base0 + pr * g.st * row_bytes + qc * g.st * g.cc * 2;
+      float acc[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int s = 0; s < 3; ++s) {
+          float f[8];
+          bf16x8_to_f32(*reinterpret_cast<const uint4*>(base + r * row_bytes + s * g.cc * 2), f);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] = fmaf(f[e], wv[r * 3 + s][e], acc[e]);
+        }
+      store_bf16x8(md->dy + static_cast<int64_t>(g.m0 + px) * C + g.c, acc, 1.f, ck);
+    }
+    return;
+  }
+  // other filter shapes: weights re-read per tap (L1)
+  for (int px = gt >> g.lg; px < npix; px += 128 >> g.lg) {
+    const int pr = px / g.Q, qc = px - pr * g.Q;
+    const uint8_t* base = base0 + pr * g.st * row_bytes + qc * g.st * g.cc * 2;
+    float acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+    for (int r = 0; r < g.R; ++r)
+      for (int s = 0; s < g.S; ++s) {
+        float f[8];
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(base + r * row_bytes + s * g.cc * 2), f);
+        const int k = r * g.S + s;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = fmaf(f[e], __bfloat162float(wp[e * md->ldw + k]), acc[e]);
+      }
+    store_bf16x8(md->dy + static_cast<int64_t>(g.m0 + px) * C + g.c, acc, 1.f, ck);
+  }
+}
+
 // ---------------------------------------------------------------- kernel
 
 template <int BN>
@@ -594,9 +772,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tq_empty = tq_full + kTileQ;
   uint64_t* sq_full = tq_empty + kTileQ;  // scheduler -> producer (claim look-ahead)
   uint64_t* sq_empty = sq_full + kSchedQ;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sq_empty + kSchedQ);
+  uint64_t* pub_full = sq_empty + kSchedQ;  // [2][kPubQ]: epilogue warpgroup -> publisher warp
+  uint64_t* pub_empty = pub_full + 2 * kPubQ;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pub_empty + 2 * kPubQ);
   volatile int32_t* tq = reinterpret_cast<volatile int32_t*>(tmem_slot + 1);
   volatile int32_t* sq = tq + kTileQ;
+  volatile uint32_t* tq_aux = reinterpret_cast<volatile uint32_t*>(sq + kSchedQ);  // staged tiles: ring slot
+  volatile int32_t* pub_q = reinterpret_cast<volatile int32_t*>(tq_aux + kTileQ);    // [2][kPubQ] counter indices
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -636,6 +818,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sq_full[q], 1);
       mbar_init(&sq_empty[q], 1);
     }
+    for (int q = 0; q < 2 * kPubQ; ++q) {
+      mbar_init(&pub_full[q], 1);
+      mbar_init(&pub_empty[q], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -659,15 +845,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ring: current layout, next slot, per-slot use parity, last issued
       uint32_t stage = 0, ubits = 0, nslots = kStages, sbytes = C::kStageBytes;
       int layout = 0;
-      int last_slot = -1;
-      uint32_t last_par = 0;
       auto advance = [&]() {
-        last_slot = static_cast<int>(stage);
-        last_par = (ubits >> stage) & 1u;
         ubits ^= 1u << stage;
         stage = stage + 1 == nslots ? 0 : stage + 1;
       };
       auto wait_free = [&]() { mbar_wait(&empty[stage], ((ubits >> stage) & 1u) ^ 1u); };
+      auto set_layout = [&](int lay) {
+        if (lay == layout) return;
+        // drain every slot (staged CUDA-core slots are freed by the
+        // epilogue, possibly before earlier MMA slots)
+        for (uint32_t s = 0; s < nslots; ++s) mbar_wait(&empty[s], ((ubits >> s) & 1u) ^ 1u);
+        layout = lay;
+        nslots = layout ? C::kNarrowSlots : kStages;
+        sbytes = layout ? C::kNarrowBytes : C::kStageBytes;
+        stage = 0;
+      };
       bool first = true;
       uint32_t qslot = 0, qphase = 0, sslot = 0, sphase = 0;
       // Greedy schedule: the producer claims its own tiles in table order
@@ -701,8 +893,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           md = slots + te.member;
           dw = cuda_core_mode(md->a_mode);
         }
+        const bool staged = dw && md->cc_rows > 0;
+        if (staged) set_layout(md->ring_narrow);  // before the slot is named to the consumers
         mbar_wait(&tq_empty[qslot], qphase ^ 1);
-        tq[qslot] = dw ? (t | kDwTag) : t;  // consumers skip / route a depthwise tile without loading it
+        // consumers skip / route a CUDA-core tile without loading it; a staged
+        // one takes the next ring slot: slot | use parity << 4 | byte offset / 1 KB << 8
+        tq[qslot] = dw ? (t | kDwTag | (staged ? kStagedTag : 0)) : t;
+        if (staged) tq_aux[qslot] = stage | (((ubits >> stage) & 1u) << 4) | ((stage * sbytes) >> 10 << 8);
         mbar_arrive(&tq_full[qslot]);
         const uint32_t wslot = qslot, wphase = qphase;
         if (++qslot == kTileQ) {
@@ -711,6 +908,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (t < 0) break;
         if (dw) {  // computed by the epilogue warps
+          if (staged) {
+            // gate like an activation load, then the whole input window as
+            // one box into the next slot of the current ring layout
+            const int m0 = te.m_tile * md->cc_rows * md->q;
+            const int img = m0 / md->pq;
+            const int h0 = (m0 - img * md->pq) / md->q * md->stride - md->pad;
+            prefetch_tmap(&md->a);
+            wait_free();
+            if (trace) trace[6 * t + 0] = globaltimer();
+            if (first) {
+              asm volatile("griddepcontrol.wait;" ::: "memory");
+              first = false;
+            }
+            if (te.dep >= 0 || te.rdep >= 0) {
+              if (te.dep >= 0) wait_range(counters, targets, te.dep, te.dep_n, 32);
+              if (te.rdep >= 0) wait_range(counters, targets, te.rdep, te.rdep_n, 32);
+              asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
+            if (trace) trace[6 * t + 1] = globaltimer();
+            mbar_expect_tx(&full[stage], md->tx_bytes);
+            tma_load_4d(ring + stage * sbytes, &md->a, &full[stage], te.n_tile * md->n_tile, -md->pad, h0, img);
+            advance();
+          }
           if (greedy) {
             // claim the next tile only once every epilogue warp has taken this
             // one, so a CTA never hoards depthwise tiles other SMs could run
@@ -721,14 +941,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         prefetch_tmap(&md->a);
         prefetch_tmap(&md->b);
-        if (md->ring_narrow != layout) {
-          // drain: the last issued stage consumed means all are (in order)
-          if (last_slot >= 0) mbar_wait(&empty[last_slot], last_par);
-          layout = md->ring_narrow;
-          nslots = layout ? C::kNarrowSlots : kStages;
-          sbytes = layout ? C::kNarrowBytes : C::kStageBytes;
-          stage = 0;
-        }
+        set_layout(md->ring_narrow);
         const int kb_lo = te.kb_end ? te.kb_begin : 0;
         const int k_blocks = te.kb_end ? te.kb_end : md->k_blocks;
         const uint32_t tx = md->tx_bytes;
@@ -975,7 +1188,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         qphase ^= 1;
       }
       if (t < 0) break;
-      if (t & kDwTag) continue;  // depthwise: no accumulator, the epilogue warps compute it
+      if (t & kDwTag) {  // CUDA-core tile: no accumulator, the epilogue warps compute it
+        if (t & kStagedTag) {  // its input took one ring slot, which the epilogue frees
+          const int lay = __shfl_sync(0xffffffffu, slots[tiles[t & ~(kDwTag | kStagedTag)].member].ring_narrow, 0);
+          if (lay != layout) {  // the producer drained the ring before switching
+            layout = lay;
+            nslots = lay ? C::kNarrowSlots : kStages;
+            sbytes = lay ? C::kNarrowBytes : C::kStageBytes;
+            stage = 0;
+          }
+          // Wait for the box to land even though no MMA reads it: a parity
+          // wait only tells phases apart one use ahead, so skipping the slot
+          // unwaited would let this warp lap the ring and take a still-pending
+          // staged phase for its next GEMM use of the slot.
+          mbar_wait(&full[stage], (fbits >> stage) & 1u);
+          fbits ^= 1u << stage;
+          stage = stage + 1 == nslots ? 0 : stage + 1;
+        }
+        continue;
+      }
       const TileEntry te = tiles[t];
       const MemberDesc* md = slots + te.member;
       const int kb_lo = __shfl_sync(0xffffffffu, te.kb_end ? te.kb_begin : 0, 0);
@@ -1058,6 +1289,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+  } else if (warp == 2) {
+    if (lane == 0) {
+      // ------------------------------------------------ publisher
+      // Releases the round counters of staged CUDA-core tiles, so the
+      // computing warpgroup does not stall on the release fence (which waits
+      // for its stores).  Serves both groups' queues in arrival order per group.
+      uint32_t ps[2] = {0, 0}, ph[2] = {0, 0};
+      bool live[2] = {true, true};
+      while (live[0] || live[1]) {
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          if (!live[g] || !mbar_test(&pub_full[g * kPubQ + ps[g]], ph[g])) continue;
+          const int d = pub_q[g * kPubQ + ps[g]];
+          if (d < 0)
+            live[g] = false;
+          else
+            red_release_add(counters + d, 1u);
+          mbar_arrive(&pub_empty[g * kPubQ + ps[g]]);
+          if (++ps[g] == kPubQ) {
+            ps[g] = 0;
+            ph[g] ^= 1;
+          }
+        }
+      }
+    }
   } else if (warp == 3) {
     if (lane == 0 && !ra.next_tile) {  // greedy: the producer claims its own tiles
       // ------------------------------------------------ tile scheduler
@@ -1133,19 +1389,69 @@ __global__ void __launch_bounds__(kThreads, 1)
     int issued = 0;
     uint32_t qslot = 0, qphase = 0;
     bool dw_gated = false;  // PDL wait done before this warp's first depthwise tile
+    int cc_local = 0;       // staged CUDA-core tiles seen: warpgroup (cc_local & 1) computes each
+    uint32_t pslot = 0, pphase = 0;  // this group's publish queue (its first lane pushes)
     for (;;) {
       int t = 0;
+      uint32_t aux = 0;
       if (lane == 0) {
         mbar_wait(&tq_full[qslot], qphase);
         t = tq[qslot];
+        aux = tq_aux[qslot];
         mbar_arrive(&tq_empty[qslot]);
       }
       t = __shfl_sync(0xffffffffu, t, 0);
+      aux = __shfl_sync(0xffffffffu, aux, 0);
       if (++qslot == kTileQ) {
         qslot = 0;
         qphase ^= 1;
       }
-      if (t < 0) break;
+      if (t < 0) {
+        if ((warp & 3) == 0 && lane == 0) {  // end of this group's publish stream
+          mbar_wait(&pub_empty[acc * kPubQ + pslot], pphase ^ 1);
+          pub_q[acc * kPubQ + pslot] = -1;
+          mbar_arrive(&pub_full[acc * kPubQ + pslot]);
+        }
+        break;
+      }
+      if ((t & (kDwTag | kStagedTag)) == (kDwTag | kStagedTag)) {
+        // staged CUDA-core tile: one warpgroup computes it from its ring slot
+        // (the two groups alternate, so one group's store / publish latency
+        // overlaps the other's compute), frees the slot, publishes once
+        if ((cc_local++ & 1) != static_cast<int>(acc)) continue;
+        t &= ~(kDwTag | kStagedTag);
+        const TileEntry te = tiles[t];
+        const MemberDesc* md = slots + te.member;
+        const uint32_t slot = aux & 15u;
+        mbar_wait(&full[slot], (aux >> 4) & 1u);
+        const int gt = (warp & 3) * 32 + lane;
+        if (trace && gt == 0) {
+          const uint64_t now = globaltimer();
+          trace[6 * t + 2] = trace[6 * t + 3] = trace[6 * t + 4] = now;
+        }
+        const uint8_t* src = ring + ((aux >> 8) << 10);
+        if (md->a_mode == kDepthwise)
+          staged_dw_tile(md, te, src, gt);
+        else
+          staged_pool_tile(md, te, src, gt);
+        named_barrier(1 + static_cast<int>(acc), 128);  // the group's smem reads and global stores are issued
+        if (gt == 0) {
+          mbar_arrive(&empty[slot]);
+          // the publisher warp releases the counter (its gpu-scope release
+          // covers this group's stores: bar.sync, then mbarrier arrive/wait)
+          if (te.done >= 0) {
+            mbar_wait(&pub_empty[acc * kPubQ + pslot], pphase ^ 1);
+            pub_q[acc * kPubQ + pslot] = te.done;
+            mbar_arrive(&pub_full[acc * kPubQ + pslot]);
+            if (++pslot == kPubQ) {
+              pslot = 0;
+              pphase ^= 1;
+            }
+          }
+          if (trace) trace[6 * t + 5] = globaltimer();
+        }
+        continue;
+      }
       if (t & kDwTag) {
         t &= ~kDwTag;
         const TileEntry te = tiles[t];

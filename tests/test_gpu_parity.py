@@ -35,6 +35,9 @@ def fp(a):
 
 def expect(oracle, L, relu=False):
     """fp32 oracle output of one LayerBuffers (reads the device tensors' bf16 values)."""
+    if L.kind in ("maxpool", "avgpool"):
+        import oracle_check
+        return oracle_check.expect(L)
     x = np.ascontiguousarray(L.x.float().cpu().numpy())
     w = np.ascontiguousarray(L.w.float().cpu().numpy())
     if L.kind == "dwconv":
@@ -96,6 +99,18 @@ def dw_layer(b, hw, c, stride, relu=False, seed=0):
     return LayerBuffers("dwconv", x, w, y, conv=ConvSpec(hw, hw, 3, 3, c, c, stride, 1), batch=b, relu=relu)
 
 
+def pool_layer(kind, b, hw, c, r, stride, pad, seed=0):
+    """Max / average pool: a CUDA-core tile type (staged through the operand
+    ring when its input window fits one TMA box, else the register path)."""
+    from paper_1901_00041_b200.runtime import LayerBuffers
+    from paper_1901_00041_b200.scheduler import ConvSpec
+    g = torch.Generator().manual_seed(seed)
+    x = (torch.rand(b, hw, hw, c, generator=g) * 2 - 1).to(torch.bfloat16).cuda()
+    P = (hw + 2 * pad - r) // stride + 1
+    y = torch.full((b * P * P, c), float("nan"), dtype=torch.bfloat16, device="cuda")
+    return LayerBuffers(kind, x, None, y, conv=ConvSpec(hw, hw, r, r, c, c, stride, pad), batch=b)
+
+
 def gemm_layer(m, n, k, relu=False, seed=0):
     from paper_1901_00041_b200.runtime import LayerBuffers
     from paper_1901_00041_b200.scheduler import GemmShape
@@ -137,6 +152,13 @@ CASES = {
     "dwconv 3x3 s2 15x15x144 (odd, stride 2)": lambda: dw_layer(1, 15, 144, 2),
     "dwconv 3x3 s1 56x56x32 b3 (many tiles)": lambda: dw_layer(3, 56, 32, 1),
     "dwconv 3x3 s1 7x7x200 relu (partial channel tile)": lambda: dw_layer(1, 7, 200, 1, relu=True),
+    "dwconv 3x3 s2 300x300x16 (register path: window wider than a box)": lambda: dw_layer(1, 300, 16, 2),
+    "dwconv 3x3 s2 112x112x96 b1 (staged, 48 KB ring slots)": lambda: dw_layer(1, 112, 96, 2),
+    "maxpool 3x3 s2 p1 30x30x64 b2 (stem pool, staged)": lambda: pool_layer("maxpool", 2, 30, 64, 3, 2, 1),
+    "maxpool 3x3 s2 p1 13x13x24 b2 (8-channel tiles)": lambda: pool_layer("maxpool", 2, 13, 24, 3, 2, 1),
+    "maxpool 2x2 s2 16x16x128 (VGG pool)": lambda: pool_layer("maxpool", 1, 16, 128, 2, 2, 0),
+    "maxpool 2x2 s2 300x300x8 (register path: window wider than a box)": lambda: pool_layer("maxpool", 1, 300, 8, 2, 2, 0),
+    "avgpool 7x7 global 7x7x2048 b3": lambda: pool_layer("avgpool", 3, 7, 2048, 7, 1, 0),
 }
 
 

@@ -30,6 +30,7 @@ def run_and_check(eng, rnd, full_tenants=(0,), extra=16):
                 q = m.query_input
                 q.copy_((torch.rand(q.shape, device="cuda", generator=gen) * 2 - 1).to(q.dtype))
             prev = [m.query_output.clone() for m in eng.models]
+        s.wait_stream(torch.cuda.current_stream())  # the poison / query writes above
         g.launch(s.cuda_stream)
         torch.cuda.synchronize()
         for i, m in enumerate(eng.models):

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--out", default="")
     ap.add_argument("--opt", action="append", default=[], help="runtime option name=value")
     ap.add_argument("--tile-n", type=int, default=256)
+    ap.add_argument("--raw", default="", help="also save raw per-tile stamps (npz: stamps, plan, cta)")
     a = ap.parse_args()
     peaks = json.load(open("MEASURED_PEAKS.json"))
     P, BW = peaks["bf16_tflops"] * 1e12, peaks["hbm_gbs"] * 1e9
@@ -84,6 +85,11 @@ def main():
                 sorted(x[j + 1] - x[0] for x in cta))) for j, nm in enumerate(names)))
     total = (max(x[5] for x in t) - t0) / 1e3
     print(f"kernel span {total:.1f}us, roofline {tot_roof:.1f}us, tiles {n.value}")
+    if a.raw:
+        import numpy as np
+        np.savez_compressed(a.raw, stamps=np.array(t, dtype=np.uint64) - np.uint64(t0),
+                            plan=np.array([tile.flags for tile in tiles], dtype=np.int32),
+                            cta=np.arange(n.value, dtype=np.int32) % grid)
     if a.out:
         json.dump({"rows": rows, "span_us": total, "roof_us": tot_roof}, open(a.out, "w"), indent=1)
 
