@@ -267,9 +267,11 @@ struct Runtime {
   // Staged CUDA-core tile geometry (pools, depthwise convs): a tile is `ro`
   // whole output rows of one image x `cc` channels, and its input window --
   // box {cc, (Q-1)*stride+S, (ro-1)*stride+R, 1} of the NHWC input -- lands in
-  // one ring slot (<= kCcStageBytes) by a single TMA load.  cc: a power of two
-  // >= 8 dividing C (16-byte channel groups; at most 32 groups), preferring
-  // >= 32 channels (64-byte box rows); then the most output work per tile.
+  // one ring slot by a single TMA load.  TMA moves a box one innermost row
+  // (cc channels) at a time, so the longest rows win first: cc a multiple of
+  // 8 dividing C, up to 128 channels (256-byte rows; at most 32 8-channel
+  // groups); then the most output work per tile.  A box that fits a 32 KB
+  // slot runs in the narrow ring layout, else in a wide (BN = 256: 48 KB) one.
   // Ops no box fits keep the register-path tile.
   void stage_cuda_core(Operator& op, dev::MemberDesc& md, const void* x) {
     op.cc_rows = 0;
@@ -279,22 +281,23 @@ struct Runtime {
     const int64_t C = c.in_channels, P = md.pq / md.q, Q = md.q;
     const int64_t Wb = (Q - 1) * c.stride + c.kernel_w;
     if (op.x_pitch % 8 != 0 || Wb > 256 || !aligned16(x)) return;
-    int64_t best_cc = 0, best_ro = 0, best_work = 0;
-    const int64_t want_cc = std::min<int64_t>(C, 32);
-    for (int pass = 0; pass < 2 && best_cc == 0; ++pass)
-      for (int64_t cc = 256; cc >= 8; cc /= 2) {
-        if (C % cc != 0 || (pass == 0 && cc < want_cc)) continue;
-        for (int64_t ro = 1; ro <= P; ++ro) {
-          if (P % ro != 0) continue;
-          const int64_t Hb = (ro - 1) * c.stride + c.kernel_h;
-          if (Hb > 256 || cc * Wb * Hb * 2 > dev::kCcStageBytes) break;
-          if (ro * Q * cc > best_work) {
-            best_work = ro * Q * cc;
-            best_cc = cc;
-            best_ro = ro;
-          }
+    const int64_t cap = bn == 256 ? dev::Cfg<256>::kStageBytes : dev::Cfg<128>::kStageBytes;
+    int64_t best_cc = 0, best_ro = 0, best_work = 0, best_row = 0;
+    for (int64_t cc = 8; cc <= std::min<int64_t>(C, 256); cc += 8) {
+      if (C % cc != 0) continue;
+      const int64_t row = std::min<int64_t>(cc, 128);
+      for (int64_t ro = 1; ro <= P; ++ro) {
+        if (P % ro != 0) continue;
+        const int64_t Hb = (ro - 1) * c.stride + c.kernel_h;
+        if (Hb > 256 || cc * Wb * Hb * 2 > cap) break;
+        if (row > best_row || (row == best_row && ro * Q * cc > best_work)) {
+          best_row = row;
+          best_work = ro * Q * cc;
+          best_cc = cc;
+          best_ro = ro;
         }
       }
+    }
     if (best_cc == 0) return;
     const int64_t Hb = (best_ro - 1) * c.stride + c.kernel_h;
     const cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(c.image_w),
@@ -319,7 +322,7 @@ struct Runtime {
   // A member's k-block stage (A region + B box) fits a 32 KB narrow-layout slot.
   int ring_narrow_of(const dev::MemberDesc& md, int b_rows) const {
     if (ring_layouts == 0) return 0;
-    if (md.cc_rows > 0) return 1;  // a staged CUDA-core box is <= kCcStageBytes
+    if (md.cc_rows > 0) return md.tx_bytes <= 32768 ? 1 : 0;  // a staged CUDA-core tile's box
     const bool cols = md.a_mode == dev::kAIm2colNarrow || md.a_mode == dev::kAIm2colFold;
     const int a_bytes = cols ? dev::kABytes : a_box_rows(md.m) * dev::kBK * 2;
     return a_bytes + b_rows * dev::kBK * 2 <= 32768 ? 1 : 0;

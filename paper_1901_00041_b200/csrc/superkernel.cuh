@@ -146,8 +146,8 @@ struct alignas(128) MemberDesc {
   // per tile.  The producer lands a tile's whole input window -- box
   // {n_tile channels, (q-1)*stride+S columns, (cc_rows-1)*stride+R rows, 1
   // image} of the NHWC input through map `a` -- in one operand-ring stage
-  // (tx_bytes <= kCcStageBytes), so the loads of later tiles stream while
-  // one epilogue warpgroup computes this one from shared memory.
+  // (tx_bytes; ring_narrow when it fits a 32 KB slot), so the loads of later
+  // tiles stream while one epilogue warpgroup computes this one from smem.
   int32_t cc_rows;
 };
 
@@ -207,7 +207,6 @@ struct RoundArgs {
 constexpr int kTileQ = 8;   // claimed-tile ring between producer and consumers
 constexpr int kDwTag = 1 << 30;  // tile-ring tag: a depthwise tile (no TMA / MMA work)
 constexpr int kStagedTag = 1 << 29;  // with kDwTag: a staged CUDA-core tile (one ring stage, no MMA)
-constexpr int kCcStageBytes = 32768;  // a staged CUDA-core tile's input box fits either ring layout's slot
 constexpr int kSchedQ = 2;  // scheduler look-ahead: tiles claimed before the producer needs them
 constexpr int kPubQ = 4;    // per epilogue warpgroup: staged-tile publishes queued for the publisher warp
 
@@ -617,18 +616,22 @@ __device__ __forceinline__ void pool_tile(const MemberDesc* __restrict__ md, con
 // q columns of one image, channels [c0, c0 + n_tile); its input window sits in
 // shared memory as [Hb][Wb][n_tile] bf16 (the TMA box, zero outside the
 // image).  128 threads (one epilogue warpgroup): each owns one 8-channel group
-// (16 B) of a pixel; n_tile / 8 is a power of two <= 32, so a thread keeps its
-// channel group across pixels.  Max pooling skips taps outside the image (torch
+// (16 B) of a pixel and keeps it across pixels (n_tile / 8 <= 32 groups per
+// pixel; 128 mod groups threads idle).  Max pooling skips taps outside the image (torch
 // MaxPool2d); average pooling and depthwise convs sum the zero fill (the
 // reference divides by R*S).  fp32 accumulation, fused activation, bf16 out.
 struct StagedGeom {
-  int cc, lg, Q, st, S, R, Wb, m0, h0, w0, c;
+  int cc, Q, st, S, R, Wb, m0, h0, w0, c;
+  int cg, px0, pstep;  // this thread's channel group, first pixel, pixel step (px0 >= pstep: idle)
 };
 
 __device__ __forceinline__ StagedGeom staged_geom(const MemberDesc* __restrict__ md, const TileEntry& te, int gt) {
   StagedGeom g;
   g.cc = md->n_tile;
-  g.lg = __ffs(g.cc >> 3) - 1;  // log2(channel groups)
+  const int L = g.cc >> 3;  // 8-channel groups per pixel (<= 32)
+  g.cg = gt % L;
+  g.px0 = gt / L;
+  g.pstep = 128 / L;
   g.Q = md->q;
   g.st = md->stride;
   g.S = md->s_taps;
@@ -638,7 +641,7 @@ __device__ __forceinline__ StagedGeom staged_geom(const MemberDesc* __restrict__
   const int img = g.m0 / md->pq;
   g.h0 = (g.m0 - img * md->pq) / g.Q * g.st - md->pad;
   g.w0 = -md->pad;
-  g.c = te.n_tile * g.cc + (gt & ((1 << g.lg) - 1)) * 8;
+  g.c = te.n_tile * g.cc + g.cg * 8;
   return g;
 }
 
@@ -669,8 +672,8 @@ __device__ __forceinline__ void staged_pool_tile(const MemberDesc* __restrict__ 
   const float scale = mx ? 1.f : 1.f / static_cast<float>(md->r_taps);
   const Clamp ck = clamp_of(md->act);
   const int row_bytes = g.Wb * g.cc * 2;
-  const uint8_t* base0 = src + (gt & ((1 << g.lg) - 1)) * 16;
-  for (int px = gt >> g.lg; px < npix; px += 128 >> g.lg) {
+  const uint8_t* base0 = src + g.cg * 16;
+  for (int px = g.px0 < g.pstep ? g.px0 : npix; px < npix; px += g.pstep) {
     const int pr = px / g.Q, qc = px - pr * g.Q;
     const int ih0 = g.h0 + pr * g.st, iw0 = g.w0 + qc * g.st;
     const uint8_t* base = base0 + pr * g.st * row_bytes + qc * g.st * g.cc * 2;
@@ -701,7 +704,7 @@ __device__ __forceinline__ void staged_dw_tile(const MemberDesc* __restrict__ md
   const int npix = md->cc_rows * g.Q;
   const Clamp ck = clamp_of(md->act);
   const int row_bytes = g.Wb * g.cc * 2;
-  const uint8_t* base0 = src + (gt & ((1 << g.lg) - 1)) * 16;
+  const uint8_t* base0 = src + g.cg * 16;
   const __nv_bfloat16* wp = md->dw + static_cast<int64_t>(g.c) * md->ldw;
   if (g.R == 3 && g.S == 3) {
     // 3x3 (every depthwise layer of MobileNet-v2): this thread's 8 channels x
@@ -711,7 +714,7 @@ __device__ __forceinline__ void staged_dw_tile(const MemberDesc* __restrict__ md
     for (int k = 0; k < 9; ++k)
 #pragma unroll
       for (int j = 0; j < 8; ++j) wv[k][j] = __bfloat162float(wp[j * md->ldw + k]);
-    for (int px = gt >> g.lg; px < npix; px += 128 >> g.lg) {
+    for (int px = g.px0 < g.pstep ? g.px0 : npix; px < npix; px += g.pstep) {
       const int pr = px / g.Q, qc = px - pr * g.Q;
       const uint8_t* base = base0 + pr * g.st * row_bytes + qc * g.st * g.cc * 2;
       float acc[8];
@@ -731,7 +734,7 @@ __device__ __forceinline__ void staged_dw_tile(const MemberDesc* __restrict__ md
     return;
   }
   // other filter shapes: weights re-read per tap (L1)
-  for (int px = gt >> g.lg; px < npix; px += 128 >> g.lg) {
+  for (int px = g.px0 < g.pstep ? g.px0 : npix; px < npix; px += g.pstep) {
     const int pr = px / g.Q, qc = px - pr * g.Q;
     const uint8_t* base = base0 + pr * g.st * row_bytes + qc * g.st * g.cc * 2;
     float acc[8];
@@ -894,7 +897,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           dw = cuda_core_mode(md->a_mode);
         }
         const bool staged = dw && md->cc_rows > 0;
-        if (staged) set_layout(md->ring_narrow);  // before the slot is named to the consumers
+        if (staged) {
+          // Name the slot to the consumers only once its previous use is
+          // released: the epilogue's parity wait on it is then unambiguous
+          // (one phase ahead at most), however far ahead of the ring it runs.
+          set_layout(md->ring_narrow);
+          wait_free();
+        }
         mbar_wait(&tq_empty[qslot], qphase ^ 1);
         // consumers skip / route a CUDA-core tile without loading it; a staged
         // one takes the next ring slot: slot | use parity << 4 | byte offset / 1 KB << 8
@@ -915,7 +924,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int img = m0 / md->pq;
             const int h0 = (m0 - img * md->pq) / md->q * md->stride - md->pad;
             prefetch_tmap(&md->a);
-            wait_free();
             if (trace) trace[6 * t + 0] = globaltimer();
             if (first) {
               asm volatile("griddepcontrol.wait;" ::: "memory");

@@ -38,8 +38,12 @@ def bench(kind, hw, c, r, st, pad, b=8, tenants=4, reps=20):
     print(f"{kind:8s} {hw}x{hw}x{c} r{r} s{st} b{b} x{tenants}: {us:7.1f} us/launch, {byt / us / 1e3:7.1f} GB/s compulsory")
 
 
-bench("maxpool", 112, 64, 3, 2, 1)
-bench("maxpool", 224, 64, 2, 2, 0)
-bench("avgpool", 7, 2048, 7, 1, 0)
-bench("dwconv", 112, 96, 3, 2, 1)
-bench("dwconv", 56, 144, 3, 1, 1)
+CASES = {
+    "maxpool112": ("maxpool", 112, 64, 3, 2, 1),
+    "maxpool224": ("maxpool", 224, 64, 2, 2, 0),
+    "avgpool7": ("avgpool", 7, 2048, 7, 1, 0),
+    "dw112s2": ("dwconv", 112, 96, 3, 2, 1),
+    "dw56": ("dwconv", 56, 144, 3, 1, 1),
+}
+for name in (sys.argv[1:] or CASES):
+    bench(*CASES[name], reps=int(__import__("os").environ.get("REPS", "20")))
