@@ -313,6 +313,15 @@ struct Runtime {
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (staged CUDA-core input) failed (" +
                                            std::to_string(int(r)) + ")");
+    if (op.kind == GM_LAYER_DWCONV) {
+      const int taps = static_cast<int>(c.kernel_h * c.kernel_w);
+      cuda_check(cudaMalloc(&op.wpad, static_cast<size_t>(taps * C * 2)), "cudaMalloc(depthwise filters)");
+      dev::dw_tap_major<<<static_cast<int>(std::min<int64_t>((taps * C + 255) / 256, 4096)), 256>>>(
+          md.dw, md.ldw, static_cast<__nv_bfloat16*>(op.wpad), static_cast<int>(C), taps);
+      cuda_check(cudaGetLastError(), "launch dw_tap_major");
+      cuda_check(cudaDeviceSynchronize(), "dw_tap_major");
+      md.dwt = static_cast<const __nv_bfloat16*>(op.wpad);
+    }
     op.n_tile = static_cast<int>(best_cc);
     op.cc_rows = best_ro * Q;
     md.cc_rows = static_cast<int32_t>(best_ro);

@@ -149,6 +149,7 @@ struct alignas(128) MemberDesc {
   // (tx_bytes; ring_narrow when it fits a 32 KB slot), so the loads of later
   // tiles stream while one epilogue warpgroup computes this one from smem.
   int32_t cc_rows;
+  const __nv_bfloat16* dwt;  // staged depthwise: the filters tap-major [R*S][ch] (16-byte channel groups)
 };
 
 // Device tile-table entry; `member` is the registered slot index.
@@ -668,29 +669,58 @@ __device__ __forceinline__ void staged_pool_tile(const MemberDesc* __restrict__ 
   const StagedGeom g = staged_geom(md, te, gt);
   const int H = md->h_in, W = md->w_in, C = md->ch;
   const int npix = md->cc_rows * g.Q;
-  const bool mx = md->a_mode == kMaxPool;
-  const float scale = mx ? 1.f : 1.f / static_cast<float>(md->r_taps);
   const Clamp ck = clamp_of(md->act);
-  const int row_bytes = g.Wb * g.cc * 2;
+  const int row_bytes = g.Wb * g.cc * 2, px_bytes = g.cc * 2;
   const uint8_t* base0 = src + g.cg * 16;
-  for (int px = g.px0 < g.pstep ? g.px0 : npix; px < npix; px += g.pstep) {
+  const int px_first = g.px0 < g.pstep ? g.px0 : npix;
+  if (md->a_mode == kMaxPool) {
+    // max is exact in bf16: packed bf16x2 max over the taps inside the image
+    // (taps in the padding are skipped, as torch MaxPool2d does)
+    const __nv_bfloat162 ninf = __float2bfloat162_rn(-INFINITY);
+    for (int px = px_first; px < npix; px += g.pstep) {
+      const int pr = px / g.Q, qc = px - pr * g.Q;
+      const int ih0 = g.h0 + pr * g.st, iw0 = g.w0 + qc * g.st;
+      const uint8_t* base = base0 + pr * g.st * row_bytes + qc * g.st * px_bytes;
+      __nv_bfloat162 m[4] = {ninf, ninf, ninf, ninf};
+      for (int r = 0; r < g.R; ++r) {
+        if (ih0 + r < 0 || ih0 + r >= H) continue;
+        const uint8_t* rowp = base + r * row_bytes;
+#pragma unroll 3
+        for (int s = 0; s < g.S; ++s) {
+          const uint4 v = *reinterpret_cast<const uint4*>(rowp + s * px_bytes);
+          const bool ok = iw0 + s >= 0 && iw0 + s < W;
+          const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            m[e] = ok ? __hmax2(m[e], *reinterpret_cast<const __nv_bfloat162*>(&w4[e])) : m[e];
+        }
+      }
+      float acc[8];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        acc[2 * e] = __low2float(m[e]);
+        acc[2 * e + 1] = __high2float(m[e]);
+      }
+      store_bf16x8(md->dy + static_cast<int64_t>(g.m0 + px) * C + g.c, acc, 1.f, ck);
+    }
+    return;
+  }
+  // average: fp32 sum of every tap (the zero fill counts), / R*S
+  const float scale = 1.f / static_cast<float>(md->r_taps);
+  for (int px = px_first; px < npix; px += g.pstep) {
     const int pr = px / g.Q, qc = px - pr * g.Q;
-    const int ih0 = g.h0 + pr * g.st, iw0 = g.w0 + qc * g.st;
-    const uint8_t* base = base0 + pr * g.st * row_bytes + qc * g.st * g.cc * 2;
+    const uint8_t* base = base0 + pr * g.st * row_bytes + qc * g.st * px_bytes;
     float acc[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = mx ? -INFINITY : 0.f;
+    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
     for (int r = 0; r < g.R; ++r) {
-      const bool rok = ih0 + r >= 0 && ih0 + r < H;
-      if (mx && !rok) continue;
       const uint8_t* rowp = base + r * row_bytes;
 #pragma unroll 4
       for (int s = 0; s < g.S; ++s) {
-        if (mx && (iw0 + s < 0 || iw0 + s >= W)) continue;
         float f[8];
-        bf16x8_to_f32(*reinterpret_cast<const uint4*>(rowp + s * g.cc * 2), f);
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(rowp + s * px_bytes), f);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] = mx ? fmaxf(acc[e], f[e]) : acc[e] + f[e];
+        for (int e = 0; e < 8; ++e) acc[e] += f[e];
       }
     }
     store_bf16x8(md->dy + static_cast<int64_t>(g.m0 + px) * C + g.c, acc, scale, ck);
@@ -708,12 +738,11 @@ __device__ __forceinline__ void staged_dw_tile(const MemberDesc* __restrict__ md
   const __nv_bfloat16* wp = md->dw + static_cast<int64_t>(g.c) * md->ldw;
   if (g.R == 3 && g.S == 3) {
     // 3x3 (every depthwise layer of MobileNet-v2): this thread's 8 channels x
-    // 9 taps in registers, taps unrolled
+    // 9 taps in registers (one 16-byte load per tap), taps unrolled
     float wv[9][8];
 #pragma unroll
     for (int k = 0; k < 9; ++k)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) wv[k][j] = __bfloat162float(wp[j * md->ldw + k]);
+      bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(md->dwt + static_cast<int64_t>(k) * C + g.c)), wv[k]);
     for (int px = g.px0 < g.pstep ? g.px0 : npix; px < npix; px += g.pstep) {
       const int pr = px / g.Q, qc = px - pr * g.Q;
       const uint8_t* base = base0 + pr * g.st * row_bytes + qc * g.st * g.cc * 2;
@@ -1306,9 +1335,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t ps[2] = {0, 0}, ph[2] = {0, 0};
       bool live[2] = {true, true};
       while (live[0] || live[1]) {
+        bool any = false;
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
           if (!live[g] || !mbar_test(&pub_full[g * kPubQ + ps[g]], ph[g])) continue;
+          any = true;
           const int d = pub_q[g * kPubQ + ps[g]];
           if (d < 0)
             live[g] = false;
@@ -1320,6 +1351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ph[g] ^= 1;
           }
         }
+        if (!any) __nanosleep(100);  // idle: leave the issue slots to the SM sub-partition's other warps
       }
     }
   } else if (warp == 3) {
@@ -1666,6 +1698,15 @@ __global__ void pad_narrow_weights(const __nv_bfloat16* __restrict__ src, int64_
     const int tap = rem / kNarrowC;
     const int c = rem - tap * kNarrowC;
     dst[i] = c < cin ? src[static_cast<int64_t>(o) * ldw + tap * cin + c] : __float2bfloat16(0.f);
+  }
+}
+
+// Depthwise filters [C, ldw] (R*S taps per row) -> tap-major [R*S, C].
+__global__ void dw_tap_major(const __nv_bfloat16* __restrict__ src, int64_t ldw, __nv_bfloat16* __restrict__ dst, int ch,
+                             int taps) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ch * taps; i += gridDim.x * blockDim.x) {
+    const int k = i / ch, c = i - k * ch;
+    dst[i] = src[static_cast<int64_t>(c) * ldw + k];
   }
 }
 
