@@ -578,6 +578,16 @@ typedef struct gm_serve_tenant {
   int32_t reserved0;
   double slo_latency;             /* seconds; a query meets its SLO if latency <= slo */
   int64_t flops_per_query;        /* algorithmic FLOPs of one query (credited at completion) */
+  /* Per-query data (optional; all null/0 = timestamps only).  Pinned host
+   * slots of io_slots queries: query k of the tenant (arrival order) reads its
+   * input from host_input slot k % io_slots (one query's rows of layer 0's x)
+   * and gets its result in host_output slot k % io_slots (its rows of the last
+   * layer's y).  Each dispatch copies its queries' inputs in before the round
+   * and their results out after it, so a query's latency includes both. */
+  const void* host_input;
+  void* host_output;
+  int32_t io_slots;
+  int32_t reserved1;
 } gm_serve_tenant;
 
 typedef struct gm_serve_config {
@@ -597,6 +607,14 @@ typedef struct gm_serve_config {
   int32_t reserved1;
   double degrade_slowdown;
   double degrade_start;
+  /* Member-set plan cache: > 0 bounds it (least recently used sets not in
+   * flight are dropped; single-tenant sets stay).  async_plan: a set seen for
+   * the first time is planned and uploaded on a worker thread while its
+   * dispatch runs as back-to-back single-tenant rounds (no dispatch waits on
+   * planning).  With more formable sets than `prewarm`, the pre-warm covers
+   * the single-tenant sets and the full set only. */
+  int32_t plan_cache_cap;
+  int32_t async_plan;
 } gm_serve_config;
 
 typedef struct gm_serve_stats {
@@ -610,6 +628,10 @@ typedef struct gm_serve_stats {
   int64_t plan_hits, plan_misses;          /* member-set plan / device-table cache */
   int32_t evicted, reserved0;
   uint64_t evicted_mask;                   /* bit i: logical tenant i was evicted (i < 64) */
+  int64_t plan_evictions;                  /* member sets dropped from the bounded cache */
+  int64_t plan_fallbacks;                  /* dispatches run as single-tenant rounds (set being prepared) */
+  int64_t plans_cached;                    /* member sets cached at the end */
+  int64_t h2d_bytes, d2h_bytes;            /* per-query I/O moved inside the serving loop */
 } gm_serve_stats;
 
 int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, const gm_serve_config* cfg,

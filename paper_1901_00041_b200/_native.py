@@ -122,14 +122,16 @@ P = C.POINTER
 class gm_serve_tenant(C.Structure):
     _fields_ = [("n_variants", C.c_int32), ("variant_tenant", C.POINTER(C.c_int32)),
                 ("variant_batch", C.POINTER(C.c_int32)), ("rate_qps", C.c_double), ("concurrency", C.c_int32),
-                ("reserved0", C.c_int32), ("slo_latency", C.c_double), ("flops_per_query", C.c_int64)]
+                ("reserved0", C.c_int32), ("slo_latency", C.c_double), ("flops_per_query", C.c_int64),
+                ("host_input", C.c_void_p), ("host_output", C.c_void_p), ("io_slots", C.c_int32),
+                ("reserved1", C.c_int32)]
 
 
 class gm_serve_config(C.Structure):
     _fields_ = [("duration", C.c_double), ("warmup", C.c_double), ("max_wait", C.c_double), ("seed", C.c_uint64),
                 ("depth", C.c_int32), ("prewarm", C.c_int32), ("stream", C.c_uint64),
                 ("degrade_tenant", C.c_int32), ("reserved1", C.c_int32), ("degrade_slowdown", C.c_double),
-                ("degrade_start", C.c_double)]
+                ("degrade_start", C.c_double), ("plan_cache_cap", C.c_int32), ("async_plan", C.c_int32)]
 
 
 class gm_serve_stats(C.Structure):
@@ -138,7 +140,9 @@ class gm_serve_stats(C.Structure):
                 ("p99_ms", C.c_double), ("max_ms", C.c_double), ("mean_ms", C.c_double),
                 ("slo_violation_frac", C.c_double), ("mean_queries_per_round", C.c_double),
                 ("mean_round_ms", C.c_double), ("plan_hits", C.c_int64), ("plan_misses", C.c_int64),
-                ("evicted", C.c_int32), ("reserved0", C.c_int32), ("evicted_mask", C.c_uint64)]
+                ("evicted", C.c_int32), ("reserved0", C.c_int32), ("evicted_mask", C.c_uint64),
+                ("plan_evictions", C.c_int64), ("plan_fallbacks", C.c_int64), ("plans_cached", C.c_int64),
+                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
 
 
 class gm_request_io(C.Structure):

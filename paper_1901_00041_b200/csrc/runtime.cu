@@ -9,7 +9,9 @@
 #include <cmath>
 #include <cstring>
 #include <deque>
+#include <condition_variable>
 #include <map>
+#include <mutex>
 #include <random>
 #include <string>
 #include <thread>
@@ -171,6 +173,19 @@ struct Runtime {
   size_t d_cap = 0;
   std::unordered_map<std::string, Prepared> prepared;
   std::unordered_map<std::string, Prepared> rounds;
+  std::recursive_mutex rounds_mu;
+  // Drop a round program from the cache; its device tables are freed once the
+  // caller guarantees no launch of it is pending (returns false if unknown).
+  bool forget_round(const Prepared* p, std::vector<Prepared>& graveyard) {
+    std::lock_guard<std::recursive_mutex> lock(rounds_mu);
+    for (auto it = rounds.begin(); it != rounds.end(); ++it)
+      if (&it->second == p) {
+        graveyard.push_back(std::move(it->second));
+        rounds.erase(it);
+        return true;
+      }
+    return false;
+  }
   int64_t n_superkernels = 0, n_prepasses = 0, n_tiles = 0;
   bool pdl = true;      // programmatic dependent launch between consecutive super-kernels
   bool split_k = false;      // round programs split few-tile long-K members (opt-in)
@@ -860,6 +875,7 @@ struct Runtime {
   // launch.  Member instances get completion counters; a member depends on the
   // same tenant's previous layer when that layer ran earlier in the round.
   Prepared& prepare_round(const std::vector<std::vector<int>>& plans, bool gated = false) {
+    std::lock_guard<std::recursive_mutex> lock(rounds_mu);  // gm_serve prepares member sets on a worker thread
     std::string key = gated ? "G" : "R";
     for (const auto& pl : plans) {
       for (int f : pl) {
@@ -2057,12 +2073,19 @@ int gm_ctx_launch_stats(const gm_ctx* ctx, int64_t* superkernels, int64_t* prepa
 namespace gmb {
 namespace {
 
+struct ServeQuery {
+  int64_t arrival_ns;
+  int64_t seq;  // per logical tenant: arrival order (its host I/O slot is seq % io_slots)
+};
+
 struct ServeRound {
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  std::vector<std::pair<int, std::vector<int64_t>>> members;  // (logical tenant, arrival ns of its queries)
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;  // launch begin / end, copy-out end
+  std::vector<std::pair<int, std::vector<ServeQuery>>> members;  // (logical tenant, its queries)
+  std::vector<std::vector<int>> keys;  // cached member sets launched (one, or singles while the set is prepared)
   int64_t dispatch_ns = 0;
   double flops = 0;  // the members' queries' FLOPs (served work)
   int32_t tiles = 0;
+  int32_t launches = 0;
 };
 
 int64_t since(std::chrono::steady_clock::time_point t0) {
@@ -2079,6 +2102,7 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
   Runtime& rt = runtime_of(ctx);
   cuda_check(cudaSetDevice(rt.device), "cudaSetDevice");
   if (cfg->prewarm < 0) throw std::invalid_argument("serve: prewarm cap must be >= 0");
+  if (cfg->plan_cache_cap < 0) throw std::invalid_argument("serve: plan cache cap must be >= 0");
   // degradation is off when degrade_slowdown == 0 (a zero-initialised config)
   const int deg_t = cfg->degrade_slowdown != 0.0 ? cfg->degrade_tenant : -1;
   if (deg_t >= static_cast<int>(n)) throw std::invalid_argument("serve: degradation names unknown tenant");
@@ -2096,11 +2120,20 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
     double rate = 0, slo = 0.1;
     int conc = 0;
     int64_t flops = 0;
-    std::deque<int64_t> pending;
+    std::deque<ServeQuery> pending;
     std::vector<int64_t> delayed;  // closed-loop re-arrivals after a degraded (delayed) completion
-    int64_t next_arrival = 0;
+    int64_t next_arrival = 0, next_seq = 0;
     std::mt19937_64 rng;
     bool live = true;
+    // per-query I/O (host_input != null): pinned host slots, the device query
+    // input (layer 0's x) and output (last layer's y), bytes per query
+    const char* hin = nullptr;
+    char* hout = nullptr;
+    int slots = 0;
+    char* dx = nullptr;
+    const char* dy = nullptr;
+    int64_t in_q = 0, out_q = 0;
+    void push(int64_t arrival) { pending.push_back(ServeQuery{arrival, next_seq++}); }
   };
   std::vector<T> ts(n);
   std::vector<Health> health(n);
@@ -2120,6 +2153,21 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
     ts[i].conc = st.concurrency;
     ts[i].slo = st.slo_latency > 0 ? st.slo_latency : 0.1;
     ts[i].flops = st.flops_per_query;
+    if (st.host_input || st.host_output) {
+      if (!st.host_input || !st.host_output || st.io_slots < 1)
+        throw std::invalid_argument("serve: per-query I/O needs host_input, host_output and io_slots >= 1");
+      const auto [bmax, tid] = ts[i].variants.back();
+      const Operator& first = rt.op_of(tid, 0);
+      const Operator& last = rt.flat[rt.tenant_ops[tid].back()];
+      const int64_t cols = first.kind == GM_LAYER_GEMM ? first.shape.k : first.conv.in_channels;
+      ts[i].hin = static_cast<const char*>(st.host_input);
+      ts[i].hout = static_cast<char*>(st.host_output);
+      ts[i].slots = st.io_slots;
+      ts[i].dx = const_cast<char*>(static_cast<const char*>(first.x));
+      ts[i].dy = last.y;
+      ts[i].in_q = (first.x_bytes + (first.x_pitch - cols) * 2) / bmax;  // rows of one query x pitch
+      ts[i].out_q = last.y_bytes / bmax;
+    }
     // per-tenant stream: splitmix-chained seed (hash, never XOR)
     uint64_t h = cfg->seed + 0x9E3779B97F4A7C15ull * (i + 1);
     h = (h ^ (h >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -2136,16 +2184,25 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
     if (t.rate > 0)
       t.next_arrival = draw(t);
     else
-      for (int c = 0; c < t.conc; ++c) t.pending.push_back(0);
+      for (int c = 0; c < t.conc; ++c) t.push(0);
   }
 
-  // plan + device-table cache per member set
+  // Plan + device-table cache per member set (the SuperKernelCache on B200),
+  // bounded (plan_cache_cap > 0: least recently used sets not in flight are
+  // dropped).  Single-tenant sets (every variant) are pinned: with async_plan a
+  // set seen for the first time is planned and uploaded on a worker thread
+  // while its dispatch runs as back-to-back single-tenant rounds.
   struct Cached {
     Prepared* prep;
     double planned_s;
+    uint64_t last_use;
+    int inflight;
+    bool pinned;
   };
   std::map<std::vector<int>, Cached> cache;
-  int64_t plan_hits = 0, plan_misses = 0;
+  std::vector<Prepared> graveyard;  // evicted device tables, freed after the loop
+  int64_t plan_hits = 0, plan_misses = 0, evictions = 0, fallbacks = 0;
+  uint64_t use_clock = 0;
   auto plan_members = [&](const std::vector<int>& key) {
     std::vector<RoundTenant> round;
     for (int id : key) {
@@ -2162,28 +2219,104 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
       plans.push_back(members_of(rt, d.plan));
       end = std::max(end, d.end);
     }
-    return cache.emplace(key, Cached{&rt.prepare_round(plans), to_seconds(end)}).first;
+    return std::make_pair(&rt.prepare_round(plans), to_seconds(end));
   };
-  // Pre-warm: plan and upload every member set the batcher can form (one
-  // variant or none per tenant), so no dispatch pays the miss path on the
-  // clock -- the steady state the reference's cache converges to
-  // ("cache super-kernels as workloads stabilize").
+  auto insert = [&](const std::vector<int>& key, std::pair<Prepared*, double> pp, bool pinned) {
+    auto it = cache.emplace(key, Cached{pp.first, pp.second, ++use_clock, 0, pinned}).first;
+    if (cfg->plan_cache_cap > 0) {
+      while (static_cast<int64_t>(cache.size()) > cfg->plan_cache_cap) {
+        auto victim = cache.end();
+        for (auto c = cache.begin(); c != cache.end(); ++c)
+          if (!c->second.pinned && c->second.inflight == 0 && c != it &&
+              (victim == cache.end() || c->second.last_use < victim->second.last_use))
+            victim = c;
+        if (victim == cache.end()) break;
+        rt.forget_round(victim->second.prep, graveyard);
+        cache.erase(victim);
+        ++evictions;
+      }
+    }
+    return it;
+  };
+  // Worker thread (async_plan): plans and uploads member sets off the
+  // dispatch path; the loop picks them up between dispatches.
+  std::mutex wmu;
+  std::condition_variable wcv;
+  std::deque<std::vector<int>> wtodo;
+  std::vector<std::pair<std::vector<int>, std::pair<Prepared*, double>>> wdone;
+  std::map<std::vector<int>, bool> wqueued;
+  std::string werr;
+  bool wstop = false;
+  std::thread worker;
+  if (cfg->async_plan) {
+    worker = std::thread([&]() {
+      try {
+        cuda_check(cudaSetDevice(rt.device), "cudaSetDevice");
+        for (;;) {
+          std::vector<int> key;
+          {
+            std::unique_lock<std::mutex> lk(wmu);
+            wcv.wait(lk, [&] { return wstop || !wtodo.empty(); });
+            if (wstop) return;
+            key = std::move(wtodo.front());
+            wtodo.pop_front();
+          }
+          auto pp = plan_members(key);
+          std::lock_guard<std::mutex> lk(wmu);
+          wdone.emplace_back(std::move(key), pp);
+        }
+      } catch (const std::exception& e) {
+        std::lock_guard<std::mutex> lk(wmu);
+        werr = e.what();
+      }
+    });
+  }
+  struct StopWorker {
+    std::thread& w;
+    std::mutex& mu;
+    std::condition_variable& cv;
+    bool& stop;
+    ~StopWorker() {
+      if (!w.joinable()) return;
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        stop = true;
+      }
+      cv.notify_all();
+      w.join();
+    }
+  } stop_worker{worker, wmu, wcv, wstop};
+  // Pre-warm: every formable member set (one variant or none per tenant) when
+  // there are at most cfg->prewarm of them -- the steady state the
+  // reference's cache converges to ("cache super-kernels as
+  // workloads stabilize") -- else the single-tenant sets and the full set.
   if (cfg->prewarm) {
     size_t combos = 1;
-    for (const T& t : ts) combos = std::min<size_t>(combos * (t.variants.size() + 1), 1u << 20);
-    if (combos - 1 > static_cast<size_t>(cfg->prewarm))
-      throw std::invalid_argument("serve: " + std::to_string(combos - 1) + " member sets exceed the prewarm cap");
-    std::vector<size_t> pick(n, 0);
-    for (size_t c = 1; c < combos; ++c) {
-      size_t x = c;
-      std::vector<int> key;
-      for (size_t i = 0; i < n; ++i) {
-        const size_t k = x % (ts[i].variants.size() + 1);
-        x /= ts[i].variants.size() + 1;
-        if (k) key.push_back(ts[i].variants[k - 1].second);
+    for (const T& t : ts) combos = std::min<size_t>(combos * (t.variants.size() + 1), size_t{1} << 40);
+    if (combos - 1 <= static_cast<size_t>(cfg->prewarm)) {
+      for (size_t c = 1; c < combos; ++c) {
+        size_t x = c;
+        std::vector<int> key;
+        for (size_t i = 0; i < n; ++i) {
+          const size_t k = x % (ts[i].variants.size() + 1);
+          x /= ts[i].variants.size() + 1;
+          if (k) key.push_back(ts[i].variants[k - 1].second);
+        }
+        if (!cache.count(key)) insert(key, plan_members(key), true);
       }
-      if (!cache.count(key)) plan_members(key);
+    } else {
+      std::vector<int> full;
+      for (const T& t : ts) {
+        for (const auto& [b, id] : t.variants)
+          if (!cache.count({id})) insert({id}, plan_members({id}), true);
+        full.push_back(t.variants.back().second);
+      }
+      if (!cache.count(full)) insert(full, plan_members(full), false);
     }
+  } else if (cfg->async_plan) {
+    for (const T& t : ts)
+      for (const auto& [b, id] : t.variants)
+        if (!cache.count({id})) insert({id}, plan_members({id}), true);
   }
   std::vector<cudaEvent_t> pool;
   auto get_event = [&]() {
@@ -2199,41 +2332,65 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
   std::deque<ServeRound> inflight;
   std::vector<gm_dispatch_event> trace;
   std::vector<double> lat_ms;
-  int64_t queries = 0, rounds = 0, dispatched_queries = 0, slo_miss = 0, flops_done = 0;
+  int64_t queries = 0, rounds = 0, dispatched_queries = 0, slo_miss = 0, flops_done = 0, h2d = 0, d2h = 0;
   double round_ms_sum = 0;
   double predicted_s = 0;  // EWMA of measured round device time (SLO trigger)
   int evicted = 0;
   uint64_t evicted_mask = 0;
+  // contiguous runs of a tenant's query slots: copy(dev offset, host offset, bytes)
+  auto for_runs = [](const T& t, const std::vector<ServeQuery>& qs, int64_t qbytes, auto&& copy) {
+    size_t j = 0;
+    while (j < qs.size()) {
+      const int64_t slot0 = qs[j].seq % t.slots;
+      size_t k = j + 1;
+      while (k < qs.size() && qs[k].seq % t.slots == slot0 + static_cast<int64_t>(k - j)) ++k;
+      copy(static_cast<int64_t>(j) * qbytes, slot0 * qbytes, static_cast<int64_t>(k - j) * qbytes);
+      j = k;
+    }
+  };
   const auto t0 = std::chrono::steady_clock::now();
 
   for (;;) {
     int64_t now = since(t0);
+    if (cfg->async_plan) {  // member sets the worker finished
+      std::lock_guard<std::mutex> lk(wmu);
+      if (!werr.empty()) throw std::runtime_error("serve: background planning failed: " + werr);
+      for (auto& [key, pp] : wdone) {
+        wqueued.erase(key);
+        if (!cache.count(key)) insert(key, pp, false);
+      }
+      wdone.clear();
+    }
     // arrivals (stop admitting at the end of the window)
     for (T& t : ts) {
       if (!t.delayed.empty() && t.live) {
         auto keep = t.delayed.begin();
         for (int64_t a : t.delayed)
           if (a <= now)
-            t.pending.push_back(a);
+            t.push(a);
           else
             *keep++ = a;
         t.delayed.erase(keep, t.delayed.end());
       }
       if (!t.live || t.rate <= 0) continue;
       while (t.next_arrival <= now && t.next_arrival < duration_ns) {
-        t.pending.push_back(t.next_arrival);
+        t.push(t.next_arrival);
         t.next_arrival += draw(t);
       }
     }
     // completions, in dispatch order
-    while (!inflight.empty() && cudaEventQuery(inflight.front().ev1) == cudaSuccess) {
+    while (!inflight.empty() && cudaEventQuery(inflight.front().ev2) == cudaSuccess) {
       ServeRound r = std::move(inflight.front());
       inflight.pop_front();
       const int64_t done = since(t0);
       float ms = 0;
       cuda_check(cudaEventElapsedTime(&ms, r.ev0, r.ev1), "cudaEventElapsedTime");
-      pool.push_back(r.ev0);
-      pool.push_back(r.ev1);
+      for (cudaEvent_t e : {r.ev0, r.ev1, r.ev2})
+        if (e) pool.push_back(e);
+      for (const auto& key : r.keys) {
+        auto it = cache.find(key);
+        if (it != cache.end()) --it->second.inflight;
+      }
       round_ms_sum += ms;
       {
         gm_dispatch_event ev{};
@@ -2243,21 +2400,21 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
         ev.flops = r.flops;
         for (auto& m : r.members) ev.queries += static_cast<int32_t>(m.second.size());
         ev.tenants = static_cast<int32_t>(r.members.size());
-        ev.launches = 1;
+        ev.launches = r.launches;
         ev.tiles = r.tiles;
         trace.push_back(ev);
       }
       predicted_s = rounds == 1 && predicted_s == 0 ? ms * 1e-3 : 0.8 * predicted_s + 0.2 * ms * 1e-3;
-      for (auto& [ti, arr] : r.members) {
+      for (auto& [ti, qs] : r.members) {
         T& t = ts[ti];
         // a degraded tenant's completion is observed exec x slowdown after its
         // dispatch (completion_with_degradation, sim.cpp:105-110)
         const bool deg = static_cast<int>(ti) == deg_t && r.dispatch_ns >= deg_start_ns && cfg->degrade_slowdown > 1.0;
         const double exec_s = ms * 1e-3 * (deg ? cfg->degrade_slowdown : 1.0);
         const int64_t seen = deg ? done + std::llround(ms * 1e6 * (cfg->degrade_slowdown - 1.0)) : done;
-        for (int64_t a : arr) {
-          const double l = (seen - a) * 1e-6;
-          if (a >= warmup_ns && seen <= duration_ns) {
+        for (const ServeQuery& q : qs) {
+          const double l = (seen - q.arrival_ns) * 1e-6;
+          if (q.arrival_ns >= warmup_ns && seen <= duration_ns) {
             lat_ms.push_back(l);
             ++queries;
             flops_done += t.flops;
@@ -2265,7 +2422,7 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
           }
           if (t.rate <= 0 && t.live && seen < duration_ns) {  // closed loop: the next query
             if (seen <= done)
-              t.pending.push_back(seen);
+              t.push(seen);
             else
               t.delayed.push_back(seen);
           }
@@ -2293,8 +2450,8 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
       ++live;
       pending += t.pending.size();
       if (!t.pending.empty()) {
-        oldest = std::min(oldest, t.pending.front());
-        if (t.pending.front() + to_ns(t.slo) - pred_ns <= now) slo_due = true;
+        oldest = std::min(oldest, t.pending.front().arrival_ns);
+        if (t.pending.front().arrival_ns + to_ns(t.slo) - pred_ns <= now) slo_due = true;
       }
     }
     if (now >= duration_ns && inflight.empty() && (pending == 0 || now >= duration_ns + to_ns(1.0))) break;
@@ -2316,27 +2473,72 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
               break;
             }
           key.push_back(rtid);
-          std::vector<int64_t> arr(t.pending.begin(), t.pending.begin() + q);
+          std::vector<ServeQuery> qs(t.pending.begin(), t.pending.begin() + q);
           t.pending.erase(t.pending.begin(), t.pending.begin() + q);
           dispatched_queries += q;
           r.flops += static_cast<double>(q) * static_cast<double>(t.flops);
-          r.members.emplace_back(static_cast<int>(i), std::move(arr));
+          r.members.emplace_back(static_cast<int>(i), std::move(qs));
         }
+        // the member set's round program, or (async planning, first sighting)
+        // its members' single-tenant rounds while the worker prepares it
+        std::vector<Cached*> progs;
         auto it = cache.find(key);
-        if (it == cache.end()) {
-          ++plan_misses;
-          it = plan_members(key);
-        } else {
+        if (it != cache.end()) {
           ++plan_hits;
+          progs.push_back(&it->second);
+          r.keys.push_back(key);
+        } else if (cfg->async_plan) {
+          ++plan_misses;
+          ++fallbacks;
+          {
+            std::lock_guard<std::mutex> lk(wmu);
+            if (!wqueued.count(key)) {
+              wqueued[key] = true;
+              wtodo.push_back(key);
+            }
+          }
+          wcv.notify_one();
+          for (int id : key) {
+            progs.push_back(&cache.at({id}));
+            r.keys.push_back({id});
+          }
+        } else {
+          ++plan_misses;
+          auto it2 = insert(key, plan_members(key), false);
+          progs.push_back(&it2->second);
+          r.keys.push_back(key);
         }
-        if (predicted_s == 0) predicted_s = it->second.planned_s;
+        if (predicted_s == 0) predicted_s = progs.front()->planned_s;
+        for (size_t m = 0; m < r.members.size(); ++m) {  // this dispatch's query inputs
+          const T& t = ts[r.members[m].first];
+          if (!t.hin) continue;
+          for_runs(t, r.members[m].second, t.in_q, [&](int64_t doff, int64_t hoff, int64_t bytes) {
+            cuda_check(cudaMemcpyAsync(t.dx + doff, t.hin + hoff, bytes, cudaMemcpyHostToDevice, stream), "H2D");
+            h2d += bytes;
+          });
+        }
         r.ev0 = get_event();
         r.ev1 = get_event();
+        r.ev2 = get_event();
         r.dispatch_ns = now;
-        r.tiles = it->second.prep->n_tiles;
         cuda_check(cudaEventRecord(r.ev0, stream), "cudaEventRecord");
-        rt.launch(*it->second.prep, stream);
+        for (Cached* c : progs) {
+          c->last_use = ++use_clock;
+          ++c->inflight;
+          r.tiles += c->prep->n_tiles;
+          rt.launch(*c->prep, stream);
+          ++r.launches;  // round programs (a layer-0 pre-pass rides with its program)
+        }
         cuda_check(cudaEventRecord(r.ev1, stream), "cudaEventRecord");
+        for (size_t m = 0; m < r.members.size(); ++m) {  // and results
+          const T& t = ts[r.members[m].first];
+          if (!t.hout) continue;
+          for_runs(t, r.members[m].second, t.out_q, [&](int64_t doff, int64_t hoff, int64_t bytes) {
+            cuda_check(cudaMemcpyAsync(t.hout + hoff, t.dy + doff, bytes, cudaMemcpyDeviceToHost, stream), "D2H");
+            d2h += bytes;
+          });
+        }
+        cuda_check(cudaEventRecord(r.ev2, stream), "cudaEventRecord");
         inflight.push_back(std::move(r));
         ++rounds;
         continue;
@@ -2347,6 +2549,7 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
   }
   cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
   for (cudaEvent_t e : pool) cudaEventDestroy(e);
+  for (Prepared& p : graveyard) p.release();
   rt.serve_trace = std::move(trace);
 
   std::memset(out, 0, sizeof(*out));
@@ -2371,6 +2574,11 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
   out->plan_misses = plan_misses;
   out->evicted = evicted;
   out->evicted_mask = evicted_mask;
+  out->plan_evictions = evictions;
+  out->plan_fallbacks = fallbacks;
+  out->plans_cached = static_cast<int64_t>(cache.size());
+  out->h2d_bytes = h2d;
+  out->d2h_bytes = d2h;
   if (n_lat) *n_lat = lat_ms.size();
   if (latencies_ms && cap) std::copy(lat_ms.begin(), lat_ms.begin() + std::min(cap, lat_ms.size()), latencies_ms);
   GM_CTX_API_END(ctx)

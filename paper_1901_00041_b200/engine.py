@@ -343,13 +343,18 @@ class ServeTenant:
     ``rate_qps`` > 0: Poisson arrivals; 0: closed loop with ``concurrency``
     queries outstanding.  The dynamic batcher serves up to ``max_batch``
     queries per dispatch with the smallest registered variant in ``batches``
-    that holds them (default: powers of two up to ``max_batch``)."""
+    that holds them (default: powers of two up to ``max_batch``).
+    ``io_slots`` > 0: queries carry data -- pinned host slots of that many
+    query inputs / results (``ServingEngine.host_inputs[i]`` /
+    ``host_outputs[i]``); query k uses slot k % io_slots, copied in before
+    its dispatch's round and out after it."""
     layers: Sequence[Layer]
     max_batch: int = 8
     rate_qps: float = 0.0
     concurrency: int = 1
     slo_latency: float = 0.040
     batches: Optional[Sequence[int]] = None
+    io_slots: int = 0
 
 
 @dataclass
@@ -407,13 +412,34 @@ class ServingEngine:
                 vs.append((b, self.ctx.register_tenant(bufs, slo_latency=spec.slo_latency,
                                                        tenant_id=f"t{tenant_offset + i}/b{b}")))
             self._variants.append(vs)
+        # per-query I/O slots (pinned): one query's rows of layer 0's input /
+        # of the last layer's output each
+        self.host_inputs: List[Optional[torch.Tensor]] = []
+        self.host_outputs: List[Optional[torch.Tensor]] = []
+        for spec, m in zip(self.specs, self.models):
+            if spec.io_slots <= 0:
+                self.host_inputs.append(None)
+                self.host_outputs.append(None)
+                continue
+            x, y = m.query_input, m.query_output
+            qx = x.reshape(spec.max_batch, -1)
+            qy = y.reshape(spec.max_batch, -1)
+            hin = torch.empty((spec.io_slots, qx.shape[1]), dtype=x.dtype).pin_memory()
+            g = torch.Generator().manual_seed(seed * 7919 + tenant_offset + len(self.host_inputs))
+            hin.copy_((torch.rand(hin.shape, generator=g) * 2 - 1).to(x.dtype))
+            b0 = m.buffers[0]
+            if b0.kind != "gemm" and x.shape[-1] > b0.conv.in_channels:  # narrow pitch: pad channels stay zero
+                hin.view(spec.io_slots, -1, x.shape[-1])[..., b0.conv.in_channels:] = 0
+            self.host_inputs.append(hin)
+            self.host_outputs.append(torch.zeros((spec.io_slots, qy.shape[1]), dtype=y.dtype).pin_memory())
 
     def flops_per_query(self, i: int) -> int:
         return sum(L.flops(1) for L in self.specs[i].layers)
 
     def serve(self, duration: float, warmup: float = 0.1, max_wait: float = -1.0, depth: int = 1,
               seed: int = 42, stream: Optional[torch.cuda.Stream] = None, prewarm: int = 4096,
-              degrade: Optional[Tuple[int, float, float]] = None) -> ServeResult:
+              degrade: Optional[Tuple[int, float, float]] = None, plan_cache_cap: int = 0,
+              async_plan: bool = False) -> ServeResult:
         """``degrade`` = (tenant, slowdown, start_s): inject_degradation
         (sim.cpp:60-68) on real hardware -- that tenant's observed completions
         stretch by ``slowdown`` from ``start_s`` on, feeding the straggler
@@ -425,12 +451,17 @@ class ServingEngine:
             tid = (C.c_int32 * len(vs))(*[t for _, t in vs])
             bat = (C.c_int32 * len(vs))(*[b for b, _ in vs])
             keep += [tid, bat]
+            hin, hout = self.host_inputs[i], self.host_outputs[i]
             arr[i] = N.gm_serve_tenant(len(vs), tid, bat, float(spec.rate_qps), int(spec.concurrency), 0,
-                                       float(spec.slo_latency), self.flops_per_query(i))
+                                       float(spec.slo_latency), self.flops_per_query(i),
+                                       hin.data_ptr() if hin is not None else None,
+                                       hout.data_ptr() if hout is not None else None,
+                                       int(spec.io_slots) if hin is not None else 0, 0)
         s = stream or torch.cuda.Stream(self.device)
         dt, dslow, dstart = degrade if degrade is not None else (-1, 1.0, 0.0)
         cfg = N.gm_serve_config(float(duration), float(warmup), float(max_wait), int(seed), int(depth),
-                                int(prewarm), int(s.cuda_stream), int(dt), 0, float(dslow), float(dstart))
+                                int(prewarm), int(s.cuda_stream), int(dt), 0, float(dslow), float(dstart),
+                                int(plan_cache_cap), int(bool(async_plan)))
         out = N.gm_serve_stats()
         cap = 1 << 20
         lat = (C.c_double * cap)()

@@ -87,3 +87,72 @@ def test_degraded_tenant_is_detected_and_evicted():
     assert s["queries"] > 50  # tenants 0 and 2 kept serving
     clean = eng.serve(duration=0.4, warmup=0.05)
     assert clean.stats["evicted"] == 0
+
+
+def _expected_slot_outputs(eng, i):
+    """Every I/O slot's result as a directly launched max-batch round of tenant
+    i computes it (slot inputs copied in bmax at a time)."""
+    spec, m = eng.specs[i], eng.models[i]
+    bmax = spec.max_batch
+    assert spec.io_slots % bmax == 0
+    rnd = eng.ctx.plan_round([eng._variants[i][-1][1]], 0)
+    s = torch.cuda.Stream()
+    out = []
+    for j0 in range(0, spec.io_slots, bmax):
+        m.query_input.view(bmax, -1).copy_(eng.host_inputs[i][j0:j0 + bmax])
+        torch.cuda.synchronize()
+        rnd.launch_round(s.cuda_stream)
+        torch.cuda.synchronize()
+        out.append(m.query_output.reshape(bmax, -1).cpu().clone())
+    return torch.cat(out)
+
+
+def test_data_bearing_queries_get_their_own_results():
+    """Per-query I/O inside gm_serve: each query's input is copied in from its
+    host slot before its dispatch and its result copied out after, so every
+    slot ends up holding the model applied to that slot's input, whatever
+    batch / dispatch the query rode in."""
+    from paper_1901_00041_b200.engine import ServeTenant, ServingEngine
+    specs = [ServeTenant(_layers(), max_batch=4, concurrency=3, io_slots=8) for _ in range(3)]
+    eng = ServingEngine(specs, device_index=0)
+    r = eng.serve(duration=0.5, warmup=0.05)
+    s = r.stats
+    assert s["queries"] > 30
+    qin = eng.host_inputs[0][0].numel() * 2
+    qout = eng.host_outputs[0][0].numel() * 2
+    assert s["h2d_bytes"] == s["dispatched_queries"] * qin
+    assert s["d2h_bytes"] == s["dispatched_queries"] * qout
+    for i in range(3):
+        got = eng.host_outputs[i].clone()
+        exp = _expected_slot_outputs(eng, i)
+        assert torch.equal(got, exp), f"tenant {i}"
+
+
+def test_bounded_plan_cache_with_background_planning():
+    """Many tenants x batch variants: the formable member sets (3^6 - 1) are
+    not pre-warmed; each new set is planned on the worker thread while its
+    dispatch runs as single-tenant rounds, and the cache stays bounded (least
+    recently used sets dropped).  Results stay correct throughout."""
+    from paper_1901_00041_b200.engine import ServeTenant, ServingEngine
+    specs = [ServeTenant(_layers(), max_batch=2, batches=[1, 2], rate_qps=900.0, slo_latency=0.2, io_slots=4)
+             for _ in range(6)]
+    eng = ServingEngine(specs, device_index=0)
+    r = eng.serve(duration=1.0, warmup=0.05, max_wait=0.0005, prewarm=0, plan_cache_cap=16, async_plan=True)
+    s = r.stats
+    assert s["queries"] > 500
+    assert s["plan_fallbacks"] > 0 and s["plan_misses"] >= s["plan_fallbacks"]
+    assert s["plan_evictions"] > 0 and s["plans_cached"] <= 16
+    launches = [e["launches"] for e in r.dispatches]
+    assert max(launches) > 1 and min(launches) == 1  # fallbacks ran as singles, cached sets as one round
+    for i in range(6):
+        assert torch.equal(eng.host_outputs[i].clone(), _expected_slot_outputs(eng, i)), f"tenant {i}"
+
+
+def test_prewarm_scales_past_exhaustive_sets():
+    """16 tenants x 2 variants (3^16 sets): pre-warm falls back to the
+    single-tenant sets plus the full set instead of refusing."""
+    from paper_1901_00041_b200.engine import ServeTenant, ServingEngine
+    specs = [ServeTenant(_layers()[:3], max_batch=2, batches=[1, 2], concurrency=2) for _ in range(16)]
+    eng = ServingEngine(specs, device_index=0)
+    r = eng.serve(duration=0.3, warmup=0.05, prewarm=4096, async_plan=True)
+    assert r.stats["queries"] > 50 and r.stats["plans_cached"] >= 33
