@@ -43,6 +43,9 @@ def parse_args():
     ap.add_argument("--csv", default="", help="also write the reference's CSV v1 rows (report.py) to this path")
     ap.add_argument("--extra", default="mix,bert",
                     help="extra BASELINE configs at N=1: mix (configs[2]) and bert (configs[3]); '' to skip")
+    ap.add_argument("--total-tenants", type=int, default=0,
+                    help="BASELINE configs[4]: this many ResNet-50 tenants placed across the job's GPUs "
+                         "(strong scaling), served per GPU; 0 = skip")
     ap.add_argument("--serve-seconds", type=float, default=1.5,
                     help="real-clock serving run per load point (0 = skip the serving section)")
     ap.add_argument("--slo", type=float, default=0.040, help="query SLO (s) of the serving run")
@@ -396,9 +399,10 @@ def run_ours(args):
         serving = run_serving(args, layers, local, rank, world, dist if world > 1 else None)
 
     extra = {}
-    if args.extra and rank == 0 and world == 1:
+    if (args.extra and rank == 0 and world == 1) or args.total_tenants > 0:
         del eng
         torch.cuda.empty_cache()
+    if args.extra and rank == 0 and world == 1:
         for name in args.extra.split(","):
             extra[name] = {"mix": run_mix, "bert": run_bert}[name](torch, args, dev, stream)
 
@@ -408,6 +412,9 @@ def run_ours(args):
         rs = [int(r) for r in args.table1.split(",")]
         table1 = run_table1(torch, rs, dev, stream)
         table1["other_presets"] = {p: run_table1(torch, rs, dev, stream, p) for p in ("rnn-matvec", "square-256")}
+
+    # BASELINE configs[4]: the fixed tenant total placed across the job's GPUs
+    c5 = run_c5(torch, args, dev, rank, world, dist if world > 1 else None) if args.total_tenants > 0 else None
 
     if rank != 0:
         if world > 1:
@@ -518,6 +525,8 @@ def run_ours(args):
         line["serving"] = serving
     for name, sec in extra.items():
         line["config_" + name] = sec
+    if c5 is not None:
+        line["config_c5"] = c5
     print(json.dumps(line), flush=True)
     if args.csv:
         from paper_1901_00041_b200 import report
@@ -527,54 +536,107 @@ def run_ours(args):
     return 0
 
 
+SERVE_KEEP = ("tflops", "qps", "p50_ms", "p99_ms", "max_ms", "slo_violation_frac", "queries", "rounds",
+              "mean_queries_per_round", "mean_round_ms", "plan_hits", "plan_misses", "plan_fallbacks",
+              "plan_evictions", "plan_padded", "plans_cached", "evicted", "h2d_bytes", "d2h_bytes")
+
+
+def serve_session(eng, seconds, rank, world, dist, **kw):
+    """One timed gm_serve run (after a short warm-up run that fills the plan
+    cache and pages in the path); stats summed / latencies merged over ranks
+    (one all-gather after the run, off the hot path; nearest-rank p99)."""
+    eng.serve(duration=0.3, warmup=0.1, seed=1, **kw)
+    if dist is not None:
+        dist.barrier()
+    r = eng.serve(duration=seconds, warmup=min(0.2, seconds / 4), seed=42 + rank, **kw)
+    st = {k: r.stats[k] for k in SERVE_KEEP}
+    lat = r.latencies_ms
+    if dist is not None:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (lat, st))
+        lat = [x for g, _ in gathered for x in g]
+        per = [s2 for _, s2 in gathered]
+        q = sum(s2["queries"] for s2 in per)
+        st = dict(per[0], tflops=sum(s2["tflops"] for s2 in per), qps=sum(s2["qps"] for s2 in per), queries=q,
+                  slo_violation_frac=sum(s2["slo_violation_frac"] * s2["queries"] for s2 in per) / q if q else None,
+                  h2d_bytes=sum(s2["h2d_bytes"] for s2 in per), d2h_bytes=sum(s2["d2h_bytes"] for s2 in per))
+        if lat:
+            st.update(p50_ms=nearest_rank(lat, 50.0), p99_ms=nearest_rank(lat, 99.0), max_ms=max(lat))
+    return st
+
+
+def serve_points(factory, seconds, rank=0, world=1, dist=None, slo_mult=2.0, **kw):
+    """Closed-loop saturation, Poisson at 50% / 80% of the saturated query
+    rate under the tenants' own SLOs, and an SLO-bound point: Poisson at 80%
+    with every SLO set to ``slo_mult`` x the saturated mean round time, so the
+    batcher's SLO trigger and the violation count are exercised.  Queries
+    carry data (per-query H2D / D2H inside the serving loop)."""
+    sat = serve_session(factory(None, None), seconds, rank, world, dist, **kw)
+    pts = {"closed_loop": sat}
+    for f in (0.5, 0.8):
+        pts[f"poisson_{int(f * 100)}pct"] = dict(serve_session(factory(f * sat["qps"], None), seconds, rank, world,
+                                                               dist, **kw), load=f)
+    slo = slo_mult * sat["mean_round_ms"] / 1e3
+    pts["slo_bound_80pct"] = dict(serve_session(factory(0.8 * sat["qps"], slo), seconds, rank, world, dist, **kw),
+                                  load=0.8, slo_ms=slo * 1e3)
+    return pts
+
+
 def run_serving(args, layers, local, rank, world, dist):
-    """Real-clock serving of the same tenants through gm_serve (the B200 form of
-    run_space_time): closed loop at saturation, then Poisson arrivals at 50% and
-    80% of the saturated query rate.  Query latency = completion - arrival
-    (queueing + batching wait + execution); p99 by nearest rank over every
-    rank's samples (one all-gather after the run, off the hot path)."""
+    """Real-clock serving of the headline tenants through gm_serve (the B200
+    form of run_space_time) on every rank: closed loop at saturation, Poisson
+    at 50% / 80% of that rate (SLO --slo), and an SLO-bound point (SLO = 2 x
+    the saturated round time).  Query latency = completion - arrival
+    (queueing + batching wait + input copy + execution + result copy)."""
     from paper_1901_00041_b200.engine import ServeTenant, ServingEngine
     T = args.tenants
 
-    def session(rate, conc):
-        specs = [ServeTenant(layers, max_batch=args.batch, rate_qps=rate, concurrency=conc, slo_latency=args.slo)
-                 for _ in range(T)]
-        eng = ServingEngine(specs, device_index=local, tenant_offset=rank * T)
-        eng.serve(duration=0.3, warmup=0.1, seed=1)  # prewarm plans + device tables, JIT of the path
-        if dist is not None:
-            dist.barrier()
-        r = eng.serve(duration=args.serve_seconds, warmup=min(0.2, args.serve_seconds / 4), seed=42 + rank)
-        lat = r.latencies_ms
-        if dist is not None:
-            gathered = [None] * world
-            dist.all_gather_object(gathered, lat)
-            lat = [x for g in gathered for x in g]
-            tot = [None] * world
-            dist.all_gather_object(tot, (r.stats["tflops"], r.stats["qps"], r.stats["slo_violation_frac"],
-                                         r.stats["queries"]))
-        else:
-            tot = [(r.stats["tflops"], r.stats["qps"], r.stats["slo_violation_frac"], r.stats["queries"])]
-        q = sum(t[3] for t in tot)
-        out = {"tflops": sum(t[0] for t in tot), "qps": sum(t[1] for t in tot),
-               "p50_ms": nearest_rank(lat, 50.0) if lat else None, "p99_ms": nearest_rank(lat, 99.0) if lat else None,
-               "max_ms": max(lat) if lat else None,
-               "slo_violation_frac": sum(t[2] * t[3] for t in tot) / q if q else None,
-               "queries": q, "rounds_per_gpu": r.stats["rounds"],
-               "mean_queries_per_round": r.stats["mean_queries_per_round"],
-               "mean_round_ms": r.stats["mean_round_ms"], "plan_misses_on_clock": r.stats["plan_misses"],
-               "evicted": r.stats["evicted"]}
-        del eng
-        return out
+    def factory(total_qps, slo):
+        rate = 0.0 if total_qps is None else total_qps / (T * world)
+        specs = [ServeTenant(layers, max_batch=args.batch, rate_qps=rate, concurrency=args.batch,
+                             slo_latency=slo or args.slo, io_slots=2 * args.batch) for _ in range(T)]
+        return ServingEngine(specs, device_index=local, tenant_offset=rank * T)
 
-    sat = session(0.0, args.batch)
-    per_tenant_qps = sat["qps"] / (T * world)
-    res = {"api": "ServingEngine.serve -> gm_serve (C++ real-clock loop, round-program dispatch)",
-           "slo_ms": args.slo * 1e3, "max_batch": args.batch, "seconds_per_point": args.serve_seconds,
-           "closed_loop": sat}
-    for frac in (0.5, 0.8):
-        res[f"poisson_{int(frac * 100)}pct"] = dict(session(frac * per_tenant_qps, 1),
-                                                   rate_qps_per_tenant=frac * per_tenant_qps)
-    return res
+    pts = serve_points(factory, args.serve_seconds, rank, world, dist)
+    return dict({"api": "ServingEngine.serve -> gm_serve (C++ real-clock loop: arrivals, dynamic batcher, "
+                        "per-query H2D / D2H, round-program dispatch, CUDA-event completions)",
+                 "slo_ms": args.slo * 1e3, "max_batch": args.batch, "seconds_per_point": args.serve_seconds},
+                **pts)
+
+
+def run_c5(torch, args, dev, rank, world, dist):
+    """BASELINE configs[4]: --total-tenants ResNet-50 tenants placed across the
+    job's GPUs (placement.place_tenants: LPT by FLOPs, tenant-sharded, no
+    collective; strong scaling: the total is fixed), each GPU serving its
+    shard through gm_serve with dynamic batching (variants 1/2/4/8, bounded
+    plan cache, background planning of new member sets), Poisson arrivals at
+    50% of the closed-loop saturated rate under an SLO of 2x the saturated
+    round time.  p99 is the nearest rank over every GPU's queries."""
+    from paper_1901_00041_b200 import workload as W
+    from paper_1901_00041_b200.engine import ServeTenant, ServingEngine
+    from paper_1901_00041_b200.placement import place_tenants, tenants_of
+    layers = W.resnet50(224)
+    total = args.total_tenants
+    demand = [(sum(L.flops(args.batch) for L in layers), sum(L.compulsory_bytes(args.batch) for L in layers))] * total
+    mine = tenants_of(rank, place_tenants(demand, world))
+
+    def factory(total_qps, slo):
+        rate = 0.0 if total_qps is None else total_qps / total
+        specs = [ServeTenant(layers, max_batch=args.batch, batches=[1, 2, 4, 8], rate_qps=rate,
+                             concurrency=args.batch, slo_latency=slo or args.slo, io_slots=2 * args.batch)
+                 for _ in mine]
+        return ServingEngine(specs, device_index=dev.index, tenant_offset=mine[0] if mine else 0)
+
+    kw = dict(prewarm=1, plan_cache_cap=256, async_plan=True)
+    sat = serve_session(factory(None, None), args.serve_seconds, rank, world, dist, **kw)
+    slo = 2.0 * sat["mean_round_ms"] / 1e3
+    half = serve_session(factory(0.5 * sat["qps"], slo), args.serve_seconds, rank, world, dist, **kw)
+    return {"workload": f"{total} tenants x resnet50@224 placed across {world} GPU(s) (BASELINE configs[4]): "
+                        f"tenant-sharded, {len(mine)} on GPU {rank}; dynamic batching up to {args.batch} "
+                        "(variants 1/2/4/8); data-bearing queries",
+            "scaling": "strong (total tenants fixed)", "tenants_per_gpu": len(mine),
+            "closed_loop": sat, "poisson_50pct_slo_bound": dict(half, slo_ms=slo * 1e3, load=0.5),
+            "p99_ms": half["p99_ms"]}
 
 
 def round_modes(torch, eng, stream, steps, warmup=3):
@@ -596,23 +658,6 @@ def round_modes(torch, eng, stream, steps, warmup=3):
     return out
 
 
-def serve_points(eng_factory, seconds, fracs=(0.5, 0.8)):
-    """Closed-loop saturation, then Poisson at fractions of the saturated rate."""
-    eng = eng_factory(None)
-    eng.serve(duration=0.3, warmup=0.1, seed=1)
-    sat = eng.serve(duration=seconds, warmup=min(0.2, seconds / 4), seed=42).stats
-    del eng
-    pts = {"closed_loop": sat}
-    for f in fracs:
-        eng = eng_factory(f * sat["qps"])
-        eng.serve(duration=0.3, warmup=0.1, seed=1)
-        pts[f"poisson_{int(f * 100)}pct"] = eng.serve(duration=seconds, warmup=min(0.2, seconds / 4), seed=42).stats
-        del eng
-    keep = ("tflops", "qps", "p50_ms", "p99_ms", "max_ms", "slo_violation_frac", "queries", "rounds",
-            "mean_queries_per_round", "mean_round_ms", "plan_misses", "evicted")
-    return {k: {f: v[f] for f in keep} for k, v in pts.items()}
-
-
 def run_mix(torch, args, dev, stream):
     """BASELINE configs[2]: ResNet-50 + VGG-16 + MobileNet-v2 tenants (two each)
     at 224, different layer lists in one round program (MobileNet's depthwise
@@ -627,18 +672,19 @@ def run_mix(torch, args, dev, stream):
     rm = round_modes(torch, eng, stream, max(5, args.steps // 2))
     del eng
 
-    def factory(total_qps):
+    def factory(total_qps, slo):
         specs = []
-        for _, layers, slo in models:
+        for _, layers, own_slo in models:
             rate = 0.0 if total_qps is None else total_qps / len(models)
-            specs.append(ServeTenant(layers, max_batch=8, rate_qps=rate, concurrency=8, slo_latency=slo,
-                                     batches=[2, 8]))
+            specs.append(ServeTenant(layers, max_batch=8, rate_qps=rate, concurrency=8, slo_latency=slo or own_slo,
+                                     batches=[2, 8], io_slots=16))
         return ServingEngine(specs, device_index=dev.index)
 
-    sv = serve_points(factory, max(0.5, args.serve_seconds))
+    sv = serve_points(factory, max(0.5, args.serve_seconds)) if args.serve_seconds > 0 else None
     return {"workload": "2x resnet50 + 2x vgg16 + 2x mobilenet_v2 @224 (BASELINE configs[2]); round modes at "
                         "batch 4; serving: max batch 8 (variants 2/8), SLO 40/60/20 ms, Poisson at 50%/80% of "
-                        "closed-loop saturation (equal per-tenant rates)",
+                        "closed-loop saturation (equal per-tenant rates), SLO-bound point (2x round time); "
+                        "data-bearing queries",
             "round_b4": rm, "serving": sv}
 
 
@@ -652,6 +698,20 @@ def run_bert(torch, args, dev, stream):
         eng = SpaceTimeEngine([W.bert_base_gemms(128, layers=12)] * 16, [b] * 16, device_index=dev.index)
         out[f"batch{b}"] = round_modes(torch, eng, stream, max(5, args.steps // 2))
         del eng
+    if args.serve_seconds > 0:
+        from paper_1901_00041_b200.engine import ServeTenant, ServingEngine
+        layers = W.bert_base_gemms(128, layers=12)
+
+        def factory(total_qps, slo):
+            rate = 0.0 if total_qps is None else total_qps / 16
+            specs = [ServeTenant(layers, max_batch=4, batches=[1, 2, 4], rate_qps=rate, concurrency=4,
+                                 slo_latency=slo or 0.020, io_slots=8) for _ in range(16)]
+            return ServingEngine(specs, device_index=dev.index)
+
+        out["serving"] = serve_points(factory, max(0.5, args.serve_seconds), prewarm=1, plan_cache_cap=256,
+                                      async_plan=True)
+        out["serving_note"] = ("16 tenants, dynamic batch 1-4 (variants 1/2/4; 4^16 member sets: bounded plan "
+                               "cache, new sets planned in the background), SLO 20 ms, data-bearing queries")
     return out
 
 

@@ -610,8 +610,8 @@ typedef struct gm_serve_config {
   /* Member-set plan cache: > 0 bounds it (least recently used sets not in
    * flight are dropped; single-tenant sets stay).  async_plan: a set seen for
    * the first time is planned and uploaded on a worker thread while its
-   * dispatch runs as back-to-back single-tenant rounds (no dispatch waits on
-   * planning).  With more formable sets than `prewarm`, the pre-warm covers
+   * dispatch runs as back-to-back round programs of cached sub-sets, largest
+   * first (single-tenant sets always exist; no dispatch waits on planning).  With more formable sets than `prewarm`, the pre-warm covers
    * the single-tenant sets and the full set only. */
   int32_t plan_cache_cap;
   int32_t async_plan;
@@ -632,6 +632,7 @@ typedef struct gm_serve_stats {
   int64_t plan_fallbacks;                  /* dispatches run as single-tenant rounds (set being prepared) */
   int64_t plans_cached;                    /* member sets cached at the end */
   int64_t h2d_bytes, d2h_bytes;            /* per-query I/O moved inside the serving loop */
+  int64_t plan_padded;                     /* fallbacks run as a cached superset (padded batches / tenants) */
 } gm_serve_stats;
 
 int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, const gm_serve_config* cfg,

@@ -142,7 +142,7 @@ class gm_serve_stats(C.Structure):
                 ("mean_round_ms", C.c_double), ("plan_hits", C.c_int64), ("plan_misses", C.c_int64),
                 ("evicted", C.c_int32), ("reserved0", C.c_int32), ("evicted_mask", C.c_uint64),
                 ("plan_evictions", C.c_int64), ("plan_fallbacks", C.c_int64), ("plans_cached", C.c_int64),
-                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
+                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("plan_padded", C.c_int64)]
 
 
 class gm_request_io(C.Structure):

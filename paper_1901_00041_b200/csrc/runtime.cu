@@ -129,6 +129,7 @@ struct Prepared {
   int32_t* qinfo = nullptr;  // [nq] begins then [nq] lengths
   int nq = 0;
   bool self_reset = true;  // round programs: counters in use, the last CTA resets them
+  double measured_s = 0;   // serving: EWMA of this program's device time when a dispatch ran it alone
   bool greedy = false;  // greedy in-order claiming (one claim counter after the counters and queue heads)
   // input-gated round programs (end-to-end serving): per tenant, a counter
   // (target 1) its first layer depends on, set by a 4-byte DMA after the
@@ -174,6 +175,10 @@ struct Runtime {
   std::unordered_map<std::string, Prepared> prepared;
   std::unordered_map<std::string, Prepared> rounds;
   std::recursive_mutex rounds_mu;
+  // serving: EWMA of measured / planned device time of single-tenant and of
+  // multi-tenant round programs (the planner's b200 profile is a roofline;
+  // few-tile rounds run latency-bound)
+  double serve_ratio[2] = {1.0, 1.0};
   // Drop a round program from the cache; its device tables are freed once the
   // caller guarantees no launch of it is pending (returns false if unknown).
   bool forget_round(const Prepared* p, std::vector<Prepared>& graveyard) {
@@ -2191,16 +2196,28 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
   // bounded (plan_cache_cap > 0: least recently used sets not in flight are
   // dropped).  Single-tenant sets (every variant) are pinned: with async_plan a
   // set seen for the first time is planned and uploaded on a worker thread
-  // while its dispatch runs as back-to-back single-tenant rounds.
+  // while its dispatch runs as back-to-back round programs of cached
+  // sub-sets (largest first, then single-tenant sets).
   struct Cached {
     Prepared* prep;
     double planned_s;
     uint64_t last_use;
     int inflight;
     bool pinned;
+    size_t members;
   };
   std::map<std::vector<int>, Cached> cache;
   std::vector<Prepared> graveyard;  // evicted device tables, freed after the loop
+  std::unordered_map<int, std::pair<int, int>> var_of;  // runtime tenant -> (logical tenant, batch)
+  for (size_t i = 0; i < n; ++i)
+    for (const auto& [b, id] : ts[i].variants) var_of[id] = {static_cast<int>(i), b};
+  int64_t padded = 0;
+  std::map<std::vector<int>, int> misses_of;  // async planning: sightings of not-yet-planned sets
+  // a cached program's expected device time: measured (alone, this ctx), else
+  // planned scaled by what measurements showed of the planner's estimates
+  auto expect_s = [&](const Cached& c) {
+    return c.prep->measured_s > 0 ? c.prep->measured_s : c.planned_s * rt.serve_ratio[c.members > 1 ? 1 : 0];
+  };
   int64_t plan_hits = 0, plan_misses = 0, evictions = 0, fallbacks = 0;
   uint64_t use_clock = 0;
   auto plan_members = [&](const std::vector<int>& key) {
@@ -2222,7 +2239,7 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
     return std::make_pair(&rt.prepare_round(plans), to_seconds(end));
   };
   auto insert = [&](const std::vector<int>& key, std::pair<Prepared*, double> pp, bool pinned) {
-    auto it = cache.emplace(key, Cached{pp.first, pp.second, ++use_clock, 0, pinned}).first;
+    auto it = cache.emplace(key, Cached{pp.first, pp.second, ++use_clock, 0, pinned, key.size()}).first;
     if (cfg->plan_cache_cap > 0) {
       while (static_cast<int64_t>(cache.size()) > cfg->plan_cache_cap) {
         auto victim = cache.end();
@@ -2387,9 +2404,24 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
       cuda_check(cudaEventElapsedTime(&ms, r.ev0, r.ev1), "cudaEventElapsedTime");
       for (cudaEvent_t e : {r.ev0, r.ev1, r.ev2})
         if (e) pool.push_back(e);
-      for (const auto& key : r.keys) {
-        auto it = cache.find(key);
-        if (it != cache.end()) --it->second.inflight;
+      {
+        double planned = 0;
+        bool singles = true;
+        for (const auto& key : r.keys) {
+          auto it = cache.find(key);
+          if (it == cache.end()) continue;
+          --it->second.inflight;
+          planned += it->second.planned_s;
+          singles = singles && key.size() == 1;
+          if (r.keys.size() == 1) {  // a program timed alone
+            Prepared& pr = *it->second.prep;
+            pr.measured_s = pr.measured_s > 0 ? 0.7 * pr.measured_s + 0.3 * ms * 1e-3 : ms * 1e-3;
+          }
+        }
+        if (planned > 0 && (r.keys.size() == 1 || singles)) {
+          double& ratio = rt.serve_ratio[singles ? 0 : 1];
+          ratio = 0.9 * ratio + 0.1 * (ms * 1e-3 / planned);
+        }
       }
       round_ms_sum += ms;
       {
@@ -2490,17 +2522,84 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
         } else if (cfg->async_plan) {
           ++plan_misses;
           ++fallbacks;
-          {
-            std::lock_guard<std::mutex> lk(wmu);
-            if (!wqueued.count(key)) {
-              wqueued[key] = true;
-              wtodo.push_back(key);
+          // admission on the second sighting (a set seen once rarely recurs
+          // among many tenants; padding serves it meanwhile)
+          if (++misses_of[key] >= 2) {
+            {
+              std::lock_guard<std::mutex> lk(wmu);
+              if (!wqueued.count(key)) {
+                wqueued[key] = true;
+                wtodo.push_back(key);
+              }
+            }
+            wcv.notify_one();
+            misses_of.erase(key);
+          }
+          if (misses_of.size() > 4096) misses_of.clear();
+          // Meanwhile: (a) the cached set expected shortest (measured device
+          // time, else its plan scaled by the measured/planned ratio) among
+          // those holding every member tenant at a batch variant >= its
+          // queries (padding: other tenants and larger batches ride along;
+          // only the members' rows are copied), or (b) a cover by cached
+          // sub-sets, largest first, then single-tenant sets, back to back --
+          // whichever is expected shorter.
+          const std::vector<int>* pad = nullptr;
+          double pad_s = 0;
+          for (auto& [k2, c2] : cache) {
+            if (pad && expect_s(c2) >= pad_s) continue;
+            bool covers = true;
+            for (int id : key) {
+              const auto [lt, b] = var_of.at(id);
+              bool held = false;
+              for (int id2 : k2) {
+                const auto [lt2, b2] = var_of.at(id2);
+                if (lt2 == lt && b2 >= b) {
+                  held = true;
+                  break;
+                }
+              }
+              if (!held) {
+                covers = false;
+                break;
+              }
+            }
+            if (covers) {
+              pad = &k2;
+              pad_s = expect_s(c2);
             }
           }
-          wcv.notify_one();
-          for (int id : key) {
-            progs.push_back(&cache.at({id}));
-            r.keys.push_back({id});
+          std::vector<const std::vector<int>*> cover;
+          double cover_s = 0;
+          std::vector<int> rest = key;
+          std::vector<std::pair<size_t, const std::vector<int>*>> cand;
+          for (auto& [k2, c2] : cache)
+            if (k2.size() > 1 && k2.size() < key.size()) cand.emplace_back(k2.size(), &k2);
+          std::sort(cand.begin(), cand.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+          for (const auto& [sz, k2] : cand) {
+            if (sz > rest.size()) continue;
+            bool sub = true;
+            for (int id : *k2)
+              if (std::find(rest.begin(), rest.end(), id) == rest.end()) {
+                sub = false;
+                break;
+              }
+            if (!sub) continue;
+            cover.push_back(k2);
+            rest.erase(std::remove_if(rest.begin(), rest.end(),
+                                      [&](int id) { return std::find(k2->begin(), k2->end(), id) != k2->end(); }),
+                       rest.end());
+          }
+          for (int id : rest) cover.push_back(&cache.find({id})->first);
+          for (const auto* k2 : cover) cover_s += expect_s(cache.at(*k2));
+          if (pad && pad_s <= cover_s) {
+            ++padded;
+            progs.push_back(&cache.at(*pad));
+            r.keys.push_back(*pad);
+          } else {
+            for (const auto* k2 : cover) {
+              progs.push_back(&cache.at(*k2));
+              r.keys.push_back(*k2);
+            }
           }
         } else {
           ++plan_misses;
@@ -2577,6 +2676,7 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
   out->plan_evictions = evictions;
   out->plan_fallbacks = fallbacks;
   out->plans_cached = static_cast<int64_t>(cache.size());
+  out->plan_padded = padded;
   out->h2d_bytes = h2d;
   out->d2h_bytes = d2h;
   if (n_lat) *n_lat = lat_ms.size();

@@ -143,7 +143,8 @@ def test_bounded_plan_cache_with_background_planning():
     assert s["plan_fallbacks"] > 0 and s["plan_misses"] >= s["plan_fallbacks"]
     assert s["plan_evictions"] > 0 and s["plans_cached"] <= 16
     launches = [e["launches"] for e in r.dispatches]
-    assert max(launches) > 1 and min(launches) == 1  # fallbacks ran as singles, cached sets as one round
+    # fallbacks ran as a padded cached superset (one round) or a cover of cached sub-sets
+    assert min(launches) == 1 and sum(n > 1 for n in launches) + s["plan_padded"] == s["plan_fallbacks"]
     for i in range(6):
         assert torch.equal(eng.host_outputs[i].clone(), _expected_slot_outputs(eng, i)), f"tenant {i}"
 
