@@ -392,6 +392,18 @@ int gm_ctx_set_option(gm_ctx* ctx, const char* name, int64_t value);
 int gm_register_tenant(gm_ctx* ctx, const gm_tenant_desc* t, int32_t* tenant_index);
 int gm_layer_shape(gm_ctx* ctx, int32_t tenant, int32_t layer, gm_gemm_shape* out);
 int gm_tenant_count(const gm_ctx* ctx, int32_t* n);
+/* Re-admit a tenant on another context (another GPU, or the same one): the
+ * destination allocates the tenant's buffers (owned by that ctx), copies its
+ * weights and external inputs with cudaMemcpyPeerAsync on `stream`, and
+ * registers the layers with the same dataflow; *out_tenant = the new index.
+ * Replaces the reference's terminal eviction (scheduler.cpp:225-244; SPEC.md:331
+ * names re-admission as the open extension).  Errors report on `src`. */
+int gm_migrate_tenant(gm_ctx* src, int32_t tenant, gm_ctx* dst, uint64_t stream, int32_t* out_tenant);
+/* Several tenants at once: a source buffer several of them reference (a
+ * logical tenant's batch variants are registrations over one set of buffers)
+ * is placed once on the destination and shared there too. */
+int gm_migrate_tenants(gm_ctx* src, const int32_t* tenants, size_t n, gm_ctx* dst, uint64_t stream,
+                       int32_t* out_tenants);
 
 /* Prepare (host→device upload on a miss, never inside graph capture) and
  * launch the super-kernel of plan i on `stream` (a cudaStream_t; 0 = legacy

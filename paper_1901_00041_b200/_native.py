@@ -228,6 +228,8 @@ _SIGS = {
     "gm_register_tenant": (C.c_int, [C.c_void_p, P(gm_tenant_desc), P(C.c_int32)]),
     "gm_layer_shape": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, P(gm_gemm_shape)]),
     "gm_tenant_count": (C.c_int, [C.c_void_p, P(C.c_int32)]),
+    "gm_migrate_tenant": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_uint64, P(C.c_int32)]),
+    "gm_migrate_tenants": (C.c_int, [C.c_void_p, P(C.c_int32), C.c_size_t, C.c_void_p, C.c_uint64, P(C.c_int32)]),
     "gm_prepare": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
     "gm_dispatch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint64, P(C.c_double), P(C.c_int)]),
     "gm_enqueue": (C.c_int, [C.c_void_p, P(gm_kernel_request), P(gm_request_io)]),

@@ -167,6 +167,9 @@ struct Runtime {
   EncodeIm2colFn encode_im2col = nullptr;
   std::vector<std::vector<int>> tenant_ops;  // tenant -> indices into flat
   std::vector<double> tenant_slo;            // seconds per pass
+  std::vector<std::vector<gm_layer_desc>> tenant_layers;  // registration descriptors (gm_migrate_tenant)
+  std::vector<int32_t> tenant_conc;
+  std::vector<void*> owned;                  // device buffers this runtime allocated (migrated tenants)
   std::vector<Operator> flat;
   std::vector<int> slot_op;  // descriptor slot -> index into flat
   std::vector<dev::MemberDesc> host_desc;
@@ -230,6 +233,7 @@ struct Runtime {
     }
     cudaFree(d_desc);
     cudaFree(ident);
+    for (void* p : owned) cudaFree(p);
     cudaFreeHost(host_one);
     for (InFlight& f : inflight)
       for (cudaEvent_t e : {f.exec0, f.exec1, f.done}) cudaEventDestroy(e);
@@ -766,6 +770,8 @@ struct Runtime {
     slot_op.insert(slot_op.end(), slot_of_new.begin(), slot_of_new.end());
     tenant_ops.push_back(std::move(ops));
     tenant_slo.push_back(t.slo_latency > 0 ? t.slo_latency : 0.1);
+    tenant_layers.emplace_back(t.layers, t.layers + t.n_layers);
+    tenant_conc.push_back(t.concurrency);
     return static_cast<int>(tenant_ops.size() - 1);
   }
 
@@ -1499,6 +1505,121 @@ int gm_tenant_count(const gm_ctx* ctx, int32_t* n) {
   if (!ctx || !n) throw std::invalid_argument("null argument");
   *n = ctx->rt ? static_cast<int32_t>(ctx->rt->tenant_ops.size()) : 0;
   GM_CTX_API_END(ctx)
+}
+
+// Re-placement of a tenant on another GPU's context (the
+// reference makes eviction terminal, scheduler.cpp:225-244, and names
+// re-admission as the open extension): the destination allocates
+// the tenant's buffers, its weights and external inputs move with
+// cudaMemcpyPeerAsync (NVLink P2P when the devices can reach each other;
+// the same device is a plain device copy), and the layers register there with
+// the same dataflow (views into producers' outputs keep their offsets).
+int gm_migrate_tenants(gm_ctx* src, const int32_t* tenants, size_t n, gm_ctx* dst, uint64_t stream,
+                       int32_t* out_tenants) {
+  GM_API_BEGIN
+  if (!tenants || !out_tenants || n == 0) throw std::invalid_argument("null argument");
+  Runtime& a = runtime_of(src);
+  Runtime& b = runtime_of(dst);
+  for (size_t t = 0; t < n; ++t) a.op_of(tenants[t], 0);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cuda_check(cudaSetDevice(b.device), "cudaSetDevice");
+  if (a.device != b.device) {
+    int can = 0;
+    cuda_check(cudaDeviceCanAccessPeer(&can, b.device, a.device), "cudaDeviceCanAccessPeer");
+    if (can) {
+      const cudaError_t e = cudaDeviceEnablePeerAccess(a.device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled)
+        cudaGetLastError();
+      else
+        cuda_check(e, "cudaDeviceEnablePeerAccess");
+    }
+  }
+  // Source byte ranges already placed on the destination: a buffer several of
+  // the tenants reference (a tenant's batch variants share one set) moves once.
+  struct Range {
+    const char* lo;
+    int64_t bytes;
+    char* dst;
+  };
+  std::vector<Range> placed;
+  auto find = [&](const void* p, int64_t bytes) -> char* {
+    const char* c = static_cast<const char*>(p);
+    for (const Range& r : placed)
+      if (c >= r.lo && c + bytes <= r.lo + r.bytes) return r.dst + (c - r.lo);
+    return nullptr;
+  };
+  auto place = [&](const void* p, int64_t bytes, bool copy) {
+    if (char* d = find(p, bytes)) return d;
+    void* q = nullptr;
+    cuda_check(cudaMalloc(&q, static_cast<size_t>(std::max<int64_t>(bytes, 16))), "cudaMalloc(migrated tenant)");
+    b.owned.push_back(q);
+    if (copy)
+      cuda_check(cudaMemcpyPeerAsync(q, b.device, p, a.device, static_cast<size_t>(bytes), st), "cudaMemcpyPeerAsync");
+    placed.push_back(Range{static_cast<const char*>(p), bytes, static_cast<char*>(q)});
+    return static_cast<char*>(q);
+  };
+  // largest first, so a variant's buffers (views of the largest's) translate
+  std::vector<size_t> order(n);
+  for (size_t t = 0; t < n; ++t) order[t] = t;
+  auto footprint = [&](int32_t tn) {
+    int64_t s = 0;
+    for (int f : a.tenant_ops[tn]) s += a.flat[f].y_bytes + a.flat[f].x_bytes;
+    return s;
+  };
+  std::stable_sort(order.begin(), order.end(),
+                   [&](size_t x, size_t y) { return footprint(tenants[x]) > footprint(tenants[y]); });
+  std::vector<std::vector<gm_layer_desc>> nds(n);
+  for (size_t oi : order) {
+    const int32_t tenant = tenants[oi];
+    const std::vector<gm_layer_desc>& descs = a.tenant_layers.at(static_cast<size_t>(tenant));
+    const std::vector<int>& ops = a.tenant_ops[tenant];
+    std::vector<gm_layer_desc>& nd = nds[oi];
+    nd = descs;
+    for (size_t i = 0; i < descs.size(); ++i) {  // outputs first: inputs may be views of them
+      const Operator& op = a.flat[ops[i]];
+      nd[i].y = place(descs[i].y, op.y_bytes, false);
+    }
+    for (size_t i = 0; i < descs.size(); ++i) {
+      const gm_layer_desc& L = descs[i];
+      const Operator& op = a.flat[ops[i]];
+      nd[i].x = place(L.x, op.x_bytes, L.src < 0);
+      if (L.w) {
+        int64_t rows = 0, k = 0;
+        if (L.kind == GM_LAYER_GEMM) {
+          rows = L.gemm.n;
+          k = L.gemm.k;
+        } else if (L.kind == GM_LAYER_DWCONV) {
+          rows = L.conv.in_channels;
+          k = L.conv.kernel_h * L.conv.kernel_w;
+        } else {
+          rows = L.conv.out_channels;
+          k = L.conv.kernel_h * L.conv.kernel_w * L.conv.in_channels;
+        }
+        const int64_t ldw = L.ldw > 0 ? L.ldw : k;
+        nd[i].w = place(L.w, ((rows - 1) * ldw + k) * 2, true);
+      }
+      if (L.res) {
+        const int64_t ldr = L.ldr > 0 ? L.ldr : op.shape.n;
+        nd[i].res = place(L.res, ((op.shape.m - 1) * ldr + op.shape.n) * 2, L.res_src < 0);
+      }
+    }
+  }
+  cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize(migration)");
+  for (size_t t = 0; t < n; ++t) {
+    const std::string id = "migrated/" + std::to_string(tenants[t]);
+    gm_tenant_desc td{id.c_str(), nds[t].data(), nds[t].size(), a.tenant_slo[tenants[t]], a.tenant_conc[tenants[t]], 0};
+    const int idx = b.register_tenant(td);
+    Health h;
+    h.tenant = idx;
+    h.alpha = dst->det.ewma_alpha;
+    dst->health.push_back(h);
+    out_tenants[t] = idx;
+  }
+  GM_CTX_API_END(src)
+}
+
+int gm_migrate_tenant(gm_ctx* src, int32_t tenant, gm_ctx* dst, uint64_t stream, int32_t* out_tenant) {
+  return gm_migrate_tenants(src, &tenant, 1, dst, stream, out_tenant);
 }
 
 int gm_prepare(gm_ctx* ctx, const gm_plans* p, size_t i) {

@@ -433,6 +433,29 @@ class ServingEngine:
             self.host_inputs.append(hin)
             self.host_outputs.append(torch.zeros((spec.io_slots, qy.shape[1]), dtype=y.dtype).pin_memory())
 
+    def readmit(self, tenants: Sequence[int], other: "ServingEngine") -> List[int]:
+        """Re-place evicted logical tenants on another engine (another GPU's
+        context, or the same GPU's): every batch variant migrates with
+        gm_migrate_tenant (weights and inputs by peer copy) and ``other``
+        serves the tenant from then on (placement.least_loaded picks
+        ``other`` among several).  Returns their logical indices in ``other``."""
+        out = []
+        for i in tenants:
+            moved = self.ctx.migrate_tenants([tid for _, tid in self._variants[i]], other.ctx)
+            vs = [(b, t) for (b, _), t in zip(self._variants[i], moved)]
+            spec = self.specs[i]
+            hin, hout = self.host_inputs[i], self.host_outputs[i]
+            other.specs.append(ServeTenant(spec.layers, max_batch=spec.max_batch, rate_qps=spec.rate_qps,
+                                           concurrency=spec.concurrency, slo_latency=spec.slo_latency,
+                                           batches=[b for b, _ in vs], io_slots=spec.io_slots if hin is not None else 0))
+            other.models.append(None)
+            other._variants.append(vs)
+            # the tenant's query slots travel with it (same inputs, fresh results)
+            other.host_inputs.append(hin.clone().pin_memory() if hin is not None else None)
+            other.host_outputs.append(torch.zeros_like(hout).pin_memory() if hout is not None else None)
+            out.append(len(other.specs) - 1)
+        return out
+
     def flops_per_query(self, i: int) -> int:
         return sum(L.flops(1) for L in self.specs[i].layers)
 

@@ -27,6 +27,16 @@ def place_tenants(demands: Sequence[Tuple[int, int]], n_gpus: int) -> List[int]:
     return out
 
 
+def least_loaded(loads: Sequence[Tuple[int, int]], exclude: Sequence[int] = ()) -> int:
+    """The GPU an evicted tenant is re-admitted on: least (FLOPs, weight
+    bytes) load, ties to the lowest index, never one in ``exclude`` (the GPU
+    it was evicted from)."""
+    cand = [g for g in range(len(loads)) if g not in set(exclude)]
+    if not cand:
+        raise ValueError("no GPU to re-admit on")
+    return min(cand, key=lambda g: (loads[g], g))
+
+
 def tenants_of(rank: int, placement: Sequence[int]) -> List[int]:
     return [t for t, g in enumerate(placement) if g == rank]
 

@@ -87,6 +87,23 @@ class Context:
         self.policy = policy
 
     # ------------------------------------------------------------ tenants
+    def migrate_tenant(self, tenant: int, dst: "Context", stream: int = 0) -> int:
+        """Re-admit ``tenant`` on ``dst`` (gm_migrate_tenant): its weights and
+        external inputs move to buffers the destination owns (peer copies over
+        NVLink between GPUs); returns its index in ``dst``."""
+        out = C.c_int32()
+        check(lib().gm_migrate_tenant(self.handle, int(tenant), dst.handle, int(stream), C.byref(out)))
+        return out.value
+
+    def migrate_tenants(self, tenants: Sequence[int], dst: "Context", stream: int = 0) -> List[int]:
+        """gm_migrate_tenants: buffers shared among ``tenants`` (batch
+        variants of one logical tenant) stay shared on ``dst``."""
+        n = len(tenants)
+        src = (C.c_int32 * n)(*tenants)
+        out = (C.c_int32 * n)()
+        check(lib().gm_migrate_tenants(self.handle, src, n, dst.handle, int(stream), out))
+        return list(out)
+
     def register_tenant(self, layers: Sequence[LayerBuffers], slo_latency: float = 0.1, concurrency: int = 1,
                         tenant_id: str = "") -> int:
         descs = (N.gm_layer_desc * len(layers))()

@@ -121,3 +121,13 @@ def test_two_rank_shard_plans_equal_reference():
     assert [r[1] for r in res] == [list(range(0, 16, 2)), list(range(1, 16, 2))]
     assert all(r[2] for r in res), "a shard's plan differs from the reference planner on that shard"
     assert res[0][3] == res[1][3] and res[0][3][0] > 0  # identical shards, identical plan lengths
+
+
+def test_least_loaded_readmission_target():
+    from paper_1901_00041_b200.placement import least_loaded
+    loads = [(40, 5), (10, 9), (10, 2), (30, 1)]
+    assert least_loaded(loads) == 2
+    assert least_loaded(loads, exclude=[2]) == 1
+    assert least_loaded([(5, 5), (5, 5)], exclude=[0]) == 1
+    with pytest.raises(ValueError):
+        least_loaded([(1, 1)], exclude=[0])

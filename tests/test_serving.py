@@ -157,3 +157,26 @@ def test_prewarm_scales_past_exhaustive_sets():
     eng = ServingEngine(specs, device_index=0)
     r = eng.serve(duration=0.3, warmup=0.05, prewarm=4096, async_plan=True)
     assert r.stats["queries"] > 50 and r.stats["plans_cached"] >= 33
+
+
+def test_evicted_tenant_is_readmitted_on_another_gpu():
+    """Re-placement instead of terminal eviction (SPEC.md:331's open extension):
+    the monitor evicts the degraded tenant on engine A; its variants migrate
+    (gm_migrate_tenant: buffers owned by the destination context, weights and
+    inputs by peer copy -- NVLink between two GPUs, a device copy on one) to
+    engine B on the least-loaded other GPU (GPU 1 when the box has it, else a
+    second context on GPU 0), which serves its data-bearing queries; every
+    query slot's result equals what the tenant computed on A."""
+    from paper_1901_00041_b200.engine import ServeTenant, ServingEngine
+    from paper_1901_00041_b200.placement import least_loaded
+    specs = [ServeTenant(_layers(), max_batch=4, concurrency=1, slo_latency=0.5, io_slots=4) for _ in range(3)]
+    a = ServingEngine(specs, device_index=0)
+    r = a.serve(duration=0.8, warmup=0.05, degrade=(1, 3.0, 0.1))
+    assert r.stats["evicted_mask"] == 0b10
+    n_gpu = torch.cuda.device_count()
+    target = least_loaded([(3, 0)] + [(0, 0)] * (n_gpu - 1), exclude=[0]) if n_gpu > 1 else 0
+    b = ServingEngine([ServeTenant(_layers(), max_batch=4, concurrency=2)], device_index=target)
+    (j,) = a.readmit([1], b)
+    rb = b.serve(duration=0.4, warmup=0.05)
+    assert rb.stats["queries"] > 20 and rb.stats["evicted"] == 0
+    assert torch.equal(b.host_outputs[j].clone(), _expected_slot_outputs(a, 1))
