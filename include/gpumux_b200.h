@@ -67,6 +67,12 @@ typedef struct gm_device_spec {
   int64_t tile_n;
   double space_sched_penalty;
   double launch_serialization;
+  /* b200 extension, 0 in the reference profiles: a super-kernel lasts at
+   * least waves x (tile_latency + kblock_latency x k-blocks (64 of K) of its
+   * longest-K member) -- the latency bound of few-tile plans on the
+   * persistent kernel, fitted by tools/calibrate_b200.py. */
+  double tile_latency;
+  double kblock_latency;
 } gm_device_spec;
 
 typedef struct gm_kernel_cost {     /* KernelCost, cost_model.hpp:14-20 */

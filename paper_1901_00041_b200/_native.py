@@ -33,7 +33,7 @@ class gm_device_spec(C.Structure):
         ("blocks_per_sm", C.c_int64), ("launch_overhead", C.c_double), ("context_switch_overhead", C.c_double),
         ("planning_overhead", C.c_double), ("mem_capacity", C.c_double), ("process_context_bytes", C.c_double),
         ("tile_m", C.c_int64), ("tile_n", C.c_int64), ("space_sched_penalty", C.c_double),
-        ("launch_serialization", C.c_double),
+        ("launch_serialization", C.c_double), ("tile_latency", C.c_double), ("kblock_latency", C.c_double),
     ]
 
 

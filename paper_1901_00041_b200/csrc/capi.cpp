@@ -56,6 +56,8 @@ Device to_device(const gm_device_spec& d) {
   o.tile_n = d.tile_n;
   o.space_sched_penalty = d.space_sched_penalty;
   o.launch_serialization = d.launch_serialization;
+  o.tile_latency = d.tile_latency;
+  o.kblock_latency = d.kblock_latency;
   return o;
 }
 
@@ -74,6 +76,8 @@ gm_device_spec from_device(const Device& d) {
   o.tile_n = d.tile_n;
   o.space_sched_penalty = d.space_sched_penalty;
   o.launch_serialization = d.launch_serialization;
+  o.tile_latency = d.tile_latency;
+  o.kblock_latency = d.kblock_latency;
   return o;
 }
 

@@ -47,6 +47,7 @@ void Device::check() const {
   if (mem_capacity <= 0) throw std::invalid_argument("device: mem_capacity must be > 0");
   if (process_context_bytes < 0)
     throw std::invalid_argument("device: process_context_bytes must be >= 0");
+  if (tile_latency < 0 || kblock_latency < 0) throw std::invalid_argument("device: latencies must be >= 0");
 }
 
 Device v100_device() {
@@ -96,7 +97,7 @@ std::int64_t tiles_of(const Shape& s, const Device& d) {
 }
 
 Cost roofline_totals(std::int64_t flops, std::int64_t bytes, std::int64_t blocks,
-                     const Device& d, std::int64_t slot_budget, std::int64_t launches) {
+                     const Device& d, std::int64_t slot_budget, std::int64_t launches, std::int64_t kb_max) {
   Cost c;
   c.flops = flops;
   c.bytes = bytes;
@@ -107,7 +108,11 @@ Cost roofline_totals(std::int64_t flops, std::int64_t bytes, std::int64_t blocks
   const double eff = static_cast<double>(blocks) / static_cast<double>(c.waves * slot_budget);
   const double t_compute = static_cast<double>(flops) / (d.peak_flops * eff);
   const double t_memory = static_cast<double>(bytes) / d.mem_bandwidth;
-  c.duration = static_cast<double>(launches) * d.launch_overhead + std::max(t_compute, t_memory);
+  double t = std::max(t_compute, t_memory);
+  if (d.tile_latency > 0 || d.kblock_latency > 0)  // b200 latency term (absent in the reference profiles)
+    t = std::max(t, static_cast<double>(c.waves) *
+                        (d.tile_latency + static_cast<double>(kb_max) * d.kblock_latency));
+  c.duration = static_cast<double>(launches) * d.launch_overhead + t;
   return c;
 }
 
@@ -117,14 +122,15 @@ Cost roofline(std::span<const Group> groups, const Device& d, std::int64_t slot_
   if (slot_budget < 1 || slot_budget > d.slots())
     throw std::invalid_argument("slot_budget out of range");
   if (launches < 1) throw std::invalid_argument("launches must be >= 1");
-  std::int64_t flops = 0, bytes = 0, blocks = 0;
+  std::int64_t flops = 0, bytes = 0, blocks = 0, kb_max = 0;
   for (const Group& g : groups) {
     if (g.count < 1 || !g.shape.valid()) throw std::invalid_argument("invalid kernel group");
     flops += g.count * flops_of(g.shape);
     bytes += g.count * bytes_of(g.shape);
     blocks += g.count * tiles_of(g.shape, d);
+    kb_max = std::max(kb_max, kblocks_of(g.shape));
   }
-  return roofline_totals(flops, bytes, blocks, d, slot_budget, launches);
+  return roofline_totals(flops, bytes, blocks, d, slot_budget, launches, kb_max);
 }
 
 // ---------------------------------------------------------------- queue
@@ -167,17 +173,18 @@ namespace {
 
 // Integer totals of a member set; a plan's cost is a pure function of them.
 struct Totals {
-  std::int64_t flops = 0, bytes = 0, blocks = 0;
+  std::int64_t flops = 0, bytes = 0, blocks = 0, kb_max = 0;
   void add(const Shape& s, const Device& d, std::int64_t times = 1) {
     flops += times * flops_of(s);
     bytes += times * bytes_of(s);
     blocks += times * tiles_of(s, d);
+    kb_max = std::max(kb_max, kblocks_of(s));
   }
 };
 
 Cost cost_from(const Totals& t, bool uniform, const Policy& p, const Device& d) {
   if (t.blocks == 0) throw std::invalid_argument("empty dispatch");
-  Cost c = roofline_totals(t.flops, t.bytes, t.blocks, d, d.slots(), 1);
+  Cost c = roofline_totals(t.flops, t.bytes, t.blocks, d, d.slots(), 1, t.kb_max);
   if (!uniform) c.duration *= p.variable_inefficiency;
   return c;
 }
@@ -322,6 +329,7 @@ std::vector<Plan> form_plans(Queue& q, TimeNs now, const Policy& p, const Device
         t.flops = probe * one.flops;
         t.bytes = probe * one.bytes;
         t.blocks = probe * one.blocks;
+        t.kb_max = one.kb_max;
         const double predicted = cost_from(t, true, p, d).duration;
         for (const Request& r : fifo) {
           if (headroom(r, now, predicted, p) <= 0) {

@@ -67,6 +67,12 @@ struct Device {
   std::int64_t tile_n = 64;
   double space_sched_penalty = 1.5;
   double launch_serialization = 0.5;
+  // b200 extension (0 = the reference's pure roofline): a super-kernel lasts
+  // at least its waves x (tile_latency + k-blocks of its longest-K member x
+  // kblock_latency) -- few-tile, long-K plans are latency-bound on the
+  // persistent kernel (a k-block = 64 of K; tools/calibrate_b200.py fits both)
+  double tile_latency = 0;
+  double kblock_latency = 0;
 
   std::int64_t slots() const { return sm_count * blocks_per_sm; }
   void check() const;  // device.cpp:19-39
@@ -90,8 +96,10 @@ std::int64_t tiles_of(const Shape& s, const Device& d);  // cost_model.cpp:14-16
 Cost roofline(std::span<const Group> groups, const Device& d, std::int64_t slot_budget,
               std::int64_t launches);
 // Same formula from pre-validated integer totals.
+// kb_max: k-blocks (64 of K) of the longest-K member (the latency term).
 Cost roofline_totals(std::int64_t flops, std::int64_t bytes, std::int64_t blocks,
-                     const Device& d, std::int64_t slot_budget, std::int64_t launches);
+                     const Device& d, std::int64_t slot_budget, std::int64_t launches, std::int64_t kb_max = 0);
+inline std::int64_t kblocks_of(const Shape& s) { return (s.k + 63) / 64; }
 
 // scheduler.hpp:17-25 (+ B200 extension field `batch`, never read here)
 struct Request {

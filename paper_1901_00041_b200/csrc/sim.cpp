@@ -225,7 +225,8 @@ SpaceTimeTrace simulate_space_time(const SpaceTimeConfig& cfg) {
             std::min<std::int64_t>(static_cast<std::int64_t>(grp.size()), std::max<std::int64_t>(pol.target_batch, 1));
         const std::int64_t tiles = tiles_of(shape, dev);
         const double predicted =
-            roofline_totals(probe * flops_of(shape), probe * bytes_of(shape), probe * tiles, dev, dev.slots(), 1)
+            roofline_totals(probe * flops_of(shape), probe * bytes_of(shape), probe * tiles, dev, dev.slots(), 1,
+                            kblocks_of(shape))
                 .duration;
         const TimeNs predicted_ns = to_ns(predicted * (1.0 + pol.slo_safety_margin));
         for (const Request& r : grp) wake = std::min(wake, r.deadline - predicted_ns);
@@ -318,7 +319,7 @@ RoundResult plan_round(const std::vector<RoundTenant>& tenants, TimeNs start, co
         const std::int64_t probe =
             std::min<std::int64_t>(static_cast<std::int64_t>(grp.size()), std::max<std::int64_t>(pol.target_batch, 1));
         const double predicted = roofline_totals(probe * flops_of(shape), probe * bytes_of(shape),
-                                                 probe * tiles_of(shape, dev), dev, dev.slots(), 1)
+                                                 probe * tiles_of(shape, dev), dev, dev.slots(), 1, kblocks_of(shape))
                                      .duration;
         const TimeNs predicted_ns = to_ns(predicted * (1.0 + pol.slo_safety_margin));
         for (const Request& r : grp) wake = std::min(wake, r.deadline - predicted_ns);

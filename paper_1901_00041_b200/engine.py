@@ -393,7 +393,12 @@ class ServingEngine:
                  device_spec: Optional[DeviceSpec] = None, tenant_offset: int = 0):
         self.device = torch.device("cuda", device_index)
         torch.cuda.set_device(self.device)
-        self.ctx = Context(device_index, device=device_spec, policy=policy or BatchPolicy(target_batch=0))
+        # serving prices member sets with the calibrated profile (measured
+        # peaks + latency floor, profiles/b200_calibrated.json): the SLO
+        # trigger's first prediction and the fallback choice use it
+        from .scheduler import b200_calibrated_profile
+        self.ctx = Context(device_index, device=device_spec or b200_calibrated_profile(),
+                           policy=policy or BatchPolicy(target_batch=0))
         for name, value in (options or {}).items():
             self.ctx.set_option(name, value)
         self.specs = list(tenants)

@@ -104,6 +104,9 @@ class DeviceSpec:
     tile_n: int = 64
     space_sched_penalty: float = 1.5
     launch_serialization: float = 0.5
+    # b200 extension (0 = the reference's roofline): latency floor per wave
+    tile_latency: float = 0.0
+    kblock_latency: float = 0.0
 
     def slot_total(self) -> int:
         return self.sm_count * self.blocks_per_sm
@@ -135,11 +138,12 @@ def b200_profile() -> DeviceSpec:
 
 
 def b200_calibrated_profile(path: Optional[str] = None) -> DeviceSpec:
-    """The b200 profile with peak_flops / mem_bandwidth / launch_overhead fitted
-    to measured super-kernel times (tools/calibrate_b200.py writes
+    """The b200 profile with measured physical peaks and the latency floor
+    (launch_overhead, tile_latency, kblock_latency) fitted to measured
+    super-kernel times (tools/calibrate_b200.py writes
     profiles/b200_calibrated.json).  Falls back to the
     nominal profile when no calibration exists.  Tile shape and slot count are
-    the kernel's, so plans stay those of b200_profile()."""
+    the kernel's, so the member sets of a plan stay those of b200_profile()."""
     import json
     import os
     path = path or os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",

@@ -111,3 +111,23 @@ def test_b200_profile_is_the_kernel_tile():
     d = b200_profile()
     assert (d.tile_m, d.tile_n, d.sm_count, d.blocks_per_sm) == (128, 256, 148, 1)
     d.validate()
+
+
+def test_latency_floor_extension():
+    """The b200 latency term: zero in every reference profile (parity), else a
+    plan lasts at least waves x (tile_latency + kblocks(K_max) x kblock_latency)."""
+    from paper_1901_00041_b200.scheduler import GemmShape, KernelGroup, b200_profile, dispatch_duration
+    d = b200_profile()
+    assert d.tile_latency == 0 and d.kblock_latency == 0
+    g = [KernelGroup(GemmShape(392, 512, 4608), 1), KernelGroup(GemmShape(392, 512, 512), 2)]
+    base = dispatch_duration(g, d, d.slot_total(), 1)
+    d.tile_latency, d.kblock_latency = 3e-6, 0.2e-6
+    lat = dispatch_duration(g, d, d.slot_total(), 1)
+    assert lat.waves == base.waves == 1
+    assert lat.duration == pytest.approx(d.launch_overhead + 3e-6 + 72 * 0.2e-6)
+    d.kblock_latency = 0.0
+    d.tile_latency = 1e-12  # below the roofline: unchanged
+    assert dispatch_duration(g, d, d.slot_total(), 1).duration == base.duration
+    d.tile_latency = -1.0
+    with pytest.raises(ValueError):
+        d.validate()
