@@ -40,12 +40,19 @@ constexpr int kThreads = 384;  // 4 control warps + 2 epilogue warpgroups
 constexpr int kABytes = kBM * kBK * 2;
 constexpr int kEpiChunk = 32;                         // columns per store box
 constexpr int kEpiBufBytes = 32 * kEpiChunk * 2;      // 32 rows x 32 cols bf16
-constexpr int kEpiBytes = 8 * 2 * kEpiBufBytes;       // 8 epilogue warps x double buffer
+#ifndef GMB_EPI_BUFS
+#define GMB_EPI_BUFS 2
+#endif
+#ifndef GMB_WIDE_STAGES
+#define GMB_WIDE_STAGES 4
+#endif
+constexpr int kEpiBufs = GMB_EPI_BUFS;                // store staging buffers per epilogue warp
+constexpr int kEpiBytes = 8 * kEpiBufs * kEpiBufBytes;  // 8 epilogue warps
 
 template <int BN>
 struct Cfg {
   static_assert(BN == 128 || BN == 256, "N tile must be 128 or 256");
-  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr int kStages = BN == 256 ? GMB_WIDE_STAGES : 6;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;
@@ -665,7 +672,7 @@ __device__ __forceinline__ void store_bf16x8(__nv_bfloat16* dst, const float (&a
 }
 
 __device__ __forceinline__ void staged_pool_tile(const MemberDesc* __restrict__ md, const TileEntry& te,
-                                                 const uint8_t* src, int gt) {
+                                                 const uint8_t* src, int gt, int bar_id) {
   const StagedGeom g = staged_geom(md, te, gt);
   const int H = md->h_in, W = md->w_in, C = md->ch;
   const int npix = md->cc_rows * g.Q;
@@ -707,6 +714,48 @@ __device__ __forceinline__ void staged_pool_tile(const MemberDesc* __restrict__ 
   }
   // average: fp32 sum of every tap (the zero fill counts), / R*S
   const float scale = 1.f / static_cast<float>(md->r_taps);
+  if (npix <= g.pstep / 2) {
+    // few pixels (global pools: one per image): the idle pixel slots of the
+    // group split each pixel's rows of taps, then one slot adds the partial
+    // sums through the (consumed) input slot
+    // partial-sum parts per pixel: the group's spare pixel slots, at most one
+    // per filter row, and the other parts' sums must fit the input slot
+    const int per_part = npix * (g.cc >> 3) * 32;  // bytes of one part's partial sums
+    const int reps = min(min(g.pstep / npix, g.R), 1 + static_cast<int>(md->tx_bytes) / per_part);
+    const int px = g.px0 % npix, part = g.px0 / npix;
+    const bool active = g.px0 < g.pstep && part < reps;
+    float acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+    if (active) {
+      const int pr = px / g.Q, qc = px - pr * g.Q;
+      const uint8_t* base = base0 + pr * g.st * row_bytes + qc * g.st * px_bytes;
+      for (int r = part; r < g.R; r += reps) {
+        const uint8_t* rowp = base + r * row_bytes;
+#pragma unroll 4
+        for (int s = 0; s < g.S; ++s) {
+          float f[8];
+          bf16x8_to_f32(*reinterpret_cast<const uint4*>(rowp + s * px_bytes), f);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] += f[e];
+        }
+      }
+    }
+    // every thread of the group has read its taps: reuse the slot's first bytes
+    named_barrier(bar_id, 128);
+    float* scratch = reinterpret_cast<float*>(const_cast<uint8_t*>(src));
+    if (active && part > 0)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) scratch[((part - 1) * npix * (g.cc >> 3) + px * (g.cc >> 3) + g.cg) * 8 + e] = acc[e];
+    named_barrier(bar_id, 128);
+    if (active && part == 0) {
+      for (int p2 = 1; p2 < reps; ++p2)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += scratch[((p2 - 1) * npix * (g.cc >> 3) + px * (g.cc >> 3) + g.cg) * 8 + e];
+      store_bf16x8(md->dy + static_cast<int64_t>(g.m0 + px) * C + g.c, acc, scale, ck);
+    }
+    return;
+  }
   for (int px = px_first; px < npix; px += g.pstep) {
     const int pr = px / g.Q, qc = px - pr * g.Q;
     const uint8_t* base = base0 + pr * g.st * row_bytes + qc * g.st * px_bytes;
@@ -1424,7 +1473,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;  // the TMEM lane quarter this warp may access
     const uint32_t acc = static_cast<uint32_t>((warp - 4) >> 2);
     int mma_local = 0;  // accumulator tiles seen (depthwise tiles have none)
-    uint8_t* stage_buf = epi + (warp - 4) * 2 * kEpiBufBytes;
+    uint8_t* stage_buf = epi + (warp - 4) * kEpiBufs * kEpiBufBytes;
     uint32_t acc_phase = 0, buf = 0;
     int issued = 0;
     uint32_t qslot = 0, qphase = 0;
@@ -1473,7 +1522,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (md->a_mode == kDepthwise)
           staged_dw_tile(md, te, src, gt);
         else
-          staged_pool_tile(md, te, src, gt);
+          staged_pool_tile(md, te, src, gt, 1 + static_cast<int>(acc));
         named_barrier(1 + static_cast<int>(acc), 128);  // the group's smem reads and global stores are issued
         if (gt == 0) {
           mbar_arrive(&empty[slot]);
@@ -1537,13 +1586,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       // Claim the next staging buffer once the store issued from it two
       // chunks ago has finished reading it.
       auto claim = [&]() -> uint8_t* {
-        if (lane == 0 && issued >= 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        if (lane == 0 && issued >= kEpiBufs)
+          asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kEpiBufs - 1) : "memory");
         __syncwarp();
         return stage_buf + buf * kEpiBufBytes;
       };
       auto issue = [&]() {
         ++issued;
-        buf ^= 1;
+        buf = buf + 1 == kEpiBufs ? 0 : buf + 1;
       };
       // 32 fp32 accumulators of this lane's row (residual already added by
       // the MMA) -> activation -> bf16 -> one 32x32 store box.
