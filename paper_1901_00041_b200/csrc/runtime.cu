@@ -174,6 +174,7 @@ struct Runtime {
   std::vector<int> slot_op;  // descriptor slot -> index into flat
   std::vector<dev::MemberDesc> host_desc;
   dev::MemberDesc* d_desc = nullptr;
+  std::vector<dev::MemberDesc*> retired_desc;  // outgrown descriptor arrays (captured graphs may point at them)
   size_t d_cap = 0;
   std::unordered_map<std::string, Prepared> prepared;
   std::unordered_map<std::string, Prepared> rounds;
@@ -232,6 +233,7 @@ struct Runtime {
       cudaFree(op.wpad);
     }
     cudaFree(d_desc);
+    for (dev::MemberDesc* p : retired_desc) cudaFree(p);
     cudaFree(ident);
     for (void* p : owned) cudaFree(p);
     cudaFreeHost(host_one);
@@ -747,10 +749,9 @@ struct Runtime {
       while (cap < need_n) cap *= 2;
       dev::MemberDesc* nd = nullptr;
       cuda_check(cudaMalloc(&nd, cap * sizeof(dev::MemberDesc)), "cudaMalloc(descriptors)");
-      if (d_desc) {
-        cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
-        cudaFree(d_desc);
-      }
+      // the old array stays alive (freed with the runtime): launch programs
+      // captured before this registration keep reading their descriptors
+      if (d_desc) retired_desc.push_back(d_desc);
       d_desc = nd;
       d_cap = cap;
       host_desc.insert(host_desc.end(), descs.begin(), descs.end());

@@ -76,7 +76,10 @@ class Context:
             self.handle = None
 
     def __del__(self):
-        self.close()
+        try:  # (at interpreter exit the module globals may already be gone)
+            self.close()
+        except Exception:
+            pass
 
     def set_option(self, name: str, value: int) -> None:
         """Runtime execution option (see gm_ctx_set_option in the header)."""

@@ -264,7 +264,10 @@ class _Plans:
 
     def __del__(self):
         if self.handle:
-            lib().gm_plans_destroy(self.handle)
+            try:  # (at interpreter exit the module globals may already be gone)
+                lib().gm_plans_destroy(self.handle)
+            except Exception:
+                pass
             self.handle = None
 
 
@@ -281,7 +284,10 @@ class RequestQueue:
 
     def __del__(self):
         if getattr(self, "_owned", False) and self.handle:
-            lib().gm_queue_destroy(self.handle)
+            try:  # (at interpreter exit the module globals may already be gone)
+                lib().gm_queue_destroy(self.handle)
+            except Exception:
+                pass
             self.handle = None
 
     def enqueue(self, request: KernelRequest) -> None:
@@ -361,7 +367,10 @@ class SuperKernelCache:
 
     def __del__(self):
         if getattr(self, "_owned", False) and self.handle:
-            lib().gm_cache_destroy(self.handle)
+            try:  # (at interpreter exit the module globals may already be gone)
+                lib().gm_cache_destroy(self.handle)
+            except Exception:
+                pass
             self.handle = None
 
     def _stats(self):
