@@ -131,3 +131,25 @@ def test_latency_floor_extension():
     d.tile_latency = -1.0
     with pytest.raises(ValueError):
         d.validate()
+
+
+def test_calibrated_b200_profile_keeps_physical_peaks():
+    """profiles/b200_calibrated.json (tools/calibrate_b200.py on a B200): the
+    peaks are the measured dense bf16 burst and HBM copy bandwidth, the latency
+    floor is fitted, and the held-out error is what DESIGN reports."""
+    import json
+    import os
+    from paper_1901_00041_b200.scheduler import GemmShape, KernelGroup, b200_calibrated_profile, b200_profile, \
+        dispatch_duration
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                        "b200_calibrated.json")
+    cal = json.load(open(path))
+    d = b200_calibrated_profile()
+    assert d.peak_flops == cal["fitted"]["peak_flops"] and 1.5e15 < d.peak_flops < 2.3e15
+    assert d.mem_bandwidth == cal["fitted"]["mem_bandwidth"] and 5e12 < d.mem_bandwidth < 8.5e12
+    assert d.tile_latency > 0 and d.kblock_latency > 0
+    assert cal["median_rel_err_held_out"]["calibrated"] < 0.15 < cal["median_rel_err_held_out"]["nominal"]
+    # a few-tile long-K plan (stage-4 3x3 conv at b8) is latency-bound on the device
+    g = [KernelGroup(GemmShape(392, 512, 4608), 4)]
+    assert dispatch_duration(g, d, d.slot_total(), 1).duration > 2 * dispatch_duration(
+        g, b200_profile(), d.slot_total(), 1).duration
