@@ -149,7 +149,9 @@ def test_calibrated_b200_profile_keeps_physical_peaks():
     assert d.mem_bandwidth == cal["fitted"]["mem_bandwidth"] and 5e12 < d.mem_bandwidth < 8.5e12
     assert d.tile_latency > 0 and d.kblock_latency > 0
     assert cal["median_rel_err_held_out"]["calibrated"] < 0.15 < cal["median_rel_err_held_out"]["nominal"]
-    # a few-tile long-K plan (stage-4 3x3 conv at b8) is latency-bound on the device
-    g = [KernelGroup(GemmShape(392, 512, 4608), 4)]
-    assert dispatch_duration(g, d, d.slot_total(), 1).duration > 2 * dispatch_duration(
-        g, b200_profile(), d.slot_total(), 1).duration
+    # a one-wave, narrow, long-K plan is latency-bound on the device: the
+    # calibrated floor (waves x (tile + 72 k-blocks)) exceeds its roofline
+    g = [KernelGroup(GemmShape(128 * 148, 64, 4608), 1)]
+    cal_d = dispatch_duration(g, d, d.slot_total(), 1)
+    assert cal_d.duration >= cal_d.waves * (d.tile_latency + 72 * d.kblock_latency)
+    assert cal_d.duration > dispatch_duration(g, b200_profile(), d.slot_total(), 1).duration
