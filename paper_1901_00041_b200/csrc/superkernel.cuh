@@ -458,6 +458,19 @@ __device__ __forceinline__ float gelu_f(float x) {
   return 0.5f * x * (1.f + copysignf(erf_u, x));
 }
 
+// Two fp32 -> bf16x2 (round to nearest even) in one instruction; the .relu
+// form clamps negatives to 0 in the same instruction.
+__device__ __forceinline__ uint32_t cvt_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ uint32_t cvt_bf16x2_relu(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(uint32_t lo_bits, uint32_t hi_bits, Clamp k) {
   const float lo = fminf(fmaxf(__uint_as_float(lo_bits), k.lo), k.hi);
   const float hi = fminf(fmaxf(__uint_as_float(hi_bits), k.lo), k.hi);
@@ -1616,14 +1629,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         uint8_t* sbuf = claim();
         uint8_t* row = sbuf + lane * 64;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        // bf16 packing: one cvt per pair (the .relu form for relu; relu6 adds
+        // its upper clamp first) -- the activation branch is warp-uniform
+        auto pack4 = [&](auto cvt, int j) {
           uint4 pk;
-          pk.x = pack_bf16(v[8 * j + 0], v[8 * j + 1], ck);
-          pk.y = pack_bf16(v[8 * j + 2], v[8 * j + 3], ck);
-          pk.z = pack_bf16(v[8 * j + 4], v[8 * j + 5], ck);
-          pk.w = pack_bf16(v[8 * j + 6], v[8 * j + 7], ck);
+          pk.x = cvt(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]));
+          pk.y = cvt(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
+          pk.z = cvt(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
+          pk.w = cvt(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
           *reinterpret_cast<uint4*>(row + ((j ^ sw) << 4)) = pk;
+        };
+        if (act == kActRelu || act == kActRelu6) {
+          if (act == kActRelu6) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(fminf(__uint_as_float(v[i]), 6.f));
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) pack4([](float a, float b) { return cvt_bf16x2_relu(a, b); }, j);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) pack4([](float a, float b) { return cvt_bf16x2(a, b); }, j);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
