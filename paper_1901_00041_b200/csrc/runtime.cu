@@ -209,6 +209,7 @@ struct Runtime {
                                  // (256 -> 128 -> 64) until it has this many tiles
   bool row_fold = true;          // S*Cin <= 32 convs (RGB stems) use the row-folded im2col path
   bool staged_cc = true;         // pools / depthwise convs as staged CUDA-core tiles (applies at registration)
+  bool dual_mma = true;          // narrow tiles' k-blocks split between two MMA-issuing warps (static schedule)
   bool dynamic_schedule = false;  // round programs: per-tenant ready queues (else static round-robin)
   bool greedy_schedule = false;   // round programs: greedy in-order tile claiming (else static round-robin)
   bool tall_tiles = true;         // 256-row tiles for narrow members of throughput-bound plans
@@ -1264,7 +1265,7 @@ struct Runtime {
                       p.heads, p.qinfo, p.qinfo ? p.qinfo + p.nq : nullptr, p.nq,
                       p.greedy ? p.counters + p.n_counters + p.nq : nullptr,
                       p.counters && p.self_reset ? p.counters + p.n_counters + p.nq + 1 : nullptr,
-                      p.n_counters + p.nq + 1};
+                      p.n_counters + p.nq + 1, dual_mma && bn == 256 && !p.heads ? 1 : 0};
     void* args[4] = {&slots, &tiles, &n, &ra};
     cuda_check(cudaLaunchKernelExC(&cfg, kernel, args), "launch superkernel");
     if (ev_end) cuda_check(cudaEventRecordWithFlags(ev_end, stream, cudaEventRecordExternal), "event record");
@@ -1462,6 +1463,8 @@ int gm_ctx_set_option(gm_ctx* ctx, const char* name, int64_t value) {
     rt.greedy_schedule = value != 0;  // applies to round programs prepared afterwards
   } else if (n == "narrow_min_tiles") {
     rt.narrow_min_tiles = value;  // applies to plans prepared afterwards (0 = always full width)
+  } else if (n == "dual_mma") {
+    rt.dual_mma = value != 0;
   } else if (n == "staged_cc") {
     rt.staged_cc = value != 0;  // applies to tenants registered afterwards
 

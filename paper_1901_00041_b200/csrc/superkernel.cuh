@@ -210,7 +210,23 @@ struct RoundArgs {
   uint32_t* next_tile;        // greedy schedule: one global in-order claim counter (null = static / queues)
   uint32_t* exit_ctr;         // CTAs finished; the last one zeroes counters[0, n_reset) for the next launch
   int32_t n_reset;
+  // Two MMA issuers (static schedule only; the producer then claims its own
+  // tiles and warp 3 issues): a narrow tile's k-blocks alternate between
+  // warp 1 and warp 3, each accumulating into its own half of the tile's
+  // TMEM buffer (columns [0, 128) and [128, 256)); the epilogue adds them.
+  // Single-thread tcgen05.mma issue latency, not the tensor pipe, sets a
+  // narrow tile's k-block rate; two threads' issue latencies overlap.
+  int32_t dual_mma;
 };
+
+// A tile whose k-blocks the two MMA issuers split (see RoundArgs::dual_mma).
+__device__ __forceinline__ bool dual_tile(const MemberDesc* md, const TileEntry& te, int dual_mma) {
+  if (!dual_mma || md->tall || md->n_tile > 128 || te.splits > 1) return false;
+  const int kb_lo = te.kb_end ? te.kb_begin : 0;
+  const int k_tail = te.kb_end ? te.kb_end : md->k_blocks;
+  const int k_res = md->res && k_tail == md->k_blocks ? (min(md->n_tile, md->n - te.n_tile * md->n_tile) + 63) / 64 : 0;
+  return k_tail + k_res - kb_lo >= 2;
+}
 
 constexpr int kTileQ = 8;   // claimed-tile ring between producer and consumers
 constexpr int kDwTag = 1 << 30;  // tile-ring tag: a depthwise tile (no TMA / MMA work)
@@ -431,6 +447,24 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Adds 32 columns of a second accumulator (a dual tile's issuer-B half) into
+// v, 16 columns per load to bound live registers.
+__device__ __forceinline__ void tmem_add32(uint32_t taddr, uint32_t (&v)[32]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t w[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]),
+          "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
+        : "r"(taddr + 16 * h));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[16 * h + i] = __float_as_uint(__uint_as_float(v[16 * h + i]) + __uint_as_float(w[i]));
+  }
 }
 
 // Activations: relu / relu6 are a clamp [lo, hi] applied while packing
@@ -913,12 +947,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
-      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_full[a], ra.dual_mma ? 2 : 1);  // one commit per MMA issuer
       mbar_init(&acc_empty[a], 128);
     }
     for (int q = 0; q < kTileQ; ++q) {
       mbar_init(&tq_full[q], 1);
-      mbar_init(&tq_empty[q], 1 + 8);  // the MMA thread + one lane per epilogue warp
+      mbar_init(&tq_empty[q], (ra.dual_mma ? 2 : 1) + 8);  // the MMA issuer(s) + one lane per epilogue warp
     }
     for (int q = 0; q < kSchedQ; ++q) {
       mbar_init(&sq_full[q], 1);
@@ -972,6 +1006,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // from one global counter, the next one as it starts a tile's loads (a
       // one-tile look-ahead instead of the static round-robin assignment).
       const bool greedy = ra.next_tile != nullptr;
+      const bool self_sched = ra.dual_mma != 0;  // warp 3 issues MMAs: static round-robin here
+      int static_next = blockIdx.x;
       int next = 0;
       if (greedy) {
         // the claim counter is reset by the previous launch's last CTA
@@ -982,6 +1018,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         int t;
         if (greedy) {
           t = next < n_tiles ? next : -1;
+        } else if (self_sched) {
+          t = static_next < n_tiles ? static_next : -1;
+          static_next += gridDim.x;
+          if (static_next < n_tiles) {  // pull the next tile's entry and descriptor toward the SM
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(tiles + static_next));
+          }
         } else {
           mbar_wait(&sq_full[sslot], sphase);  // next tile from the scheduler warp
           t = sq[sslot];
@@ -1280,8 +1322,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (first) asm volatile("griddepcontrol.wait;" ::: "memory");
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer
+  } else if (warp == 1 || (warp == 3 && ra.dual_mma)) {
+    // ------------------------------------------------ MMA issuer(s)
+    const int role = warp == 3 ? 1 : 0;  // dual_mma: issuer B takes a dual tile's odd k-blocks
     // The whole warp runs the loop on warp-uniform values (tile fields are
     // broadcast from lane 0 with shfl), so the descriptor arithmetic lives in
     // uniform registers; one elected lane issues tcgen05.mma / commit.
@@ -1360,25 +1403,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint64_t b_hi64 = static_cast<uint64_t>((1024u >> 4) | (1u << 14) | (2u << 29)) << 32;
       mbar_wait(&acc_empty[acc], acc_phase ^ 1);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
+      const bool dual = __shfl_sync(0xffffffffu, dual_tile(md, te, ra.dual_mma) ? 1 : 0, 0) != 0;
+      const uint32_t d_tmem = tmem_base + acc * BN + (dual && role ? 128u : 0u);
       // One k-block: wait for its stage, issue `halves` x 4 UMMA_K steps, free
       // the stage.  Two loop instances so the common path carries no test.
       auto kloop = [&](auto halves_c) {
         constexpr int kHalves = decltype(halves_c)::value;
         for (int kb = kb_lo; kb < k_blocks; ++kb) {
+          // every issuer waits on every stage (parity waits must stay one use
+          // ahead at most); only the k-block's owner issues and frees it
           mbar_wait(&full[stage], (fbits >> stage) & 1u);
+          const int owner = dual ? (kb - kb_lo) & 1 : 0;
+          if (owner != role) {
+            fbits ^= 1u << stage;
+            stage = stage + 1 == nslots ? 0 : stage + 1;
+            continue;
+          }
           tc_fence_after();
           if (trace && kb == kb_lo && lane == 0) trace[6 * t + 2] = globaltimer();
           const uint32_t a_addr = ring_base + stage * sbytes;
           const uint32_t a_lo = ((a_addr >> 4) & 0x3FFFu) | a_lbo;
           const uint32_t b_lo = (((a_addr + (kABytes * kHalves)) >> 4) & 0x3FFFu) | (1u << 16);
+          const uint32_t first = kb - kb_lo <= (dual ? 1 : 0) ? 1u : 0u;  // this issuer's first k-block
           if (elect_one()) {
 #pragma unroll
             for (int h = 0; h < kHalves; ++h) {
               // half h: A box at +16 KB * h, accumulator columns + n_tile * h
               const uint32_t ah = a_lo + h * (kABytes >> 4);
               const uint32_t dh = d_tmem + h * d_half;
-              umma_bf16(dh, a_hi64 | ah, b_hi64 | b_lo, idesc, kb != kb_lo ? 1u : 0u);
+              umma_bf16(dh, a_hi64 | ah, b_hi64 | b_lo, idesc, first ^ 1u);
               umma_bf16(dh, a_hi64 | (ah + k1), b_hi64 | (b_lo + 2), idesc, 1u);
               umma_bf16(dh, a_hi64 | (ah + k2), b_hi64 | (b_lo + 4), idesc, 1u);
               umma_bf16(dh, a_hi64 | (ah + k3), b_hi64 | (b_lo + 6), idesc, 1u);
@@ -1394,9 +1447,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         kloop(std::integral_constant<int, 2>{});
       else
         kloop(std::integral_constant<int, 1>{});
-      if (elect_one()) umma_commit(&acc_full[acc]);  // accumulator ready for the epilogue
+      if (elect_one()) umma_commit(&acc_full[acc]);  // (each issuer's) accumulator ready for the epilogue
       __syncwarp();
-      if (trace && lane == 0) trace[6 * t + 3] = globaltimer();
+      if (trace && lane == 0 && role == 0) trace[6 * t + 3] = globaltimer();
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -1429,7 +1482,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 3) {
-    if (lane == 0 && !ra.next_tile) {  // greedy: the producer claims its own tiles
+    if (lane == 0 && !ra.next_tile) {  // greedy (and dual_mma): the producer claims its own tiles
       // ------------------------------------------------ tile scheduler
       // Claims this CTA's next tile (static round-robin, or the head of a
       // ready per-tenant queue) up to kSchedQ tiles ahead of the producer, so
@@ -1663,6 +1716,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (trace && quarter == 0 && lane == 0) trace[6 * t + 4] = globaltimer();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
       bool publish = te.done >= 0;
+      const bool dual = dual_tile(md, te, ra.dual_mma);
       if (te.splits > 1) {
         // ---- split-K partial: coalesced fp32 red.add into the workspace tile.
         // Lane-major layout: the 32 lanes' float4 of (chunk c, j) are 512
@@ -1723,6 +1777,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c = 0; c < cols; c += kEpiChunk) {
             uint32_t v[32];
             tmem_ld32(tcol + c, v);
+            if (dual) tmem_add32(tcol + 128 + c, v);  // issuer B's partial sum of the K loop
             store_bf16(v, c, mrow);
           }
         }
