@@ -209,7 +209,7 @@ struct Runtime {
                                  // (256 -> 128 -> 64) until it has this many tiles
   bool row_fold = true;          // S*Cin <= 32 convs (RGB stems) use the row-folded im2col path
   bool staged_cc = true;         // pools / depthwise convs as staged CUDA-core tiles (applies at registration)
-  bool dual_mma = true;          // narrow tiles' k-blocks split between two MMA-issuing warps (static schedule)
+  bool dual_mma = false;         // narrow tiles' k-blocks split between two MMA-issuing warps (static schedule)
   bool dynamic_schedule = false;  // round programs: per-tenant ready queues (else static round-robin)
   bool greedy_schedule = false;   // round programs: greedy in-order tile claiming (else static round-robin)
   bool tall_tiles = true;         // 256-row tiles for narrow members of throughput-bound plans
