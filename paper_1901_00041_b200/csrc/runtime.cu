@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <condition_variable>
@@ -258,6 +259,7 @@ struct Runtime {
     if (spec.tile_m != dev::kBM || (spec.tile_n != 128 && spec.tile_n != 256))
       throw std::invalid_argument("b200 runtime needs tile_m 128 and tile_n 128 or 256 (the super-kernel tile)");
     bn = static_cast<int>(spec.tile_n);
+    if (const char* e = std::getenv("GM_DUAL_MMA")) dual_mma = std::atoi(e) != 0;  // A/B override of the default
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) throw NoDevice("no CUDA device visible");
     if (dev_index >= count) throw NoDevice("CUDA device index out of range");

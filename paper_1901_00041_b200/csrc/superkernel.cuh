@@ -914,7 +914,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* sq_empty = sq_full + kSchedQ;
   uint64_t* pub_full = sq_empty + kSchedQ;  // [2][kPubQ]: epilogue warpgroup -> publisher warp
   uint64_t* pub_empty = pub_full + 2 * kPubQ;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pub_empty + 2 * kPubQ);
+  // dual_mma: per ring slot, both MMA issuers have passed the slot's current
+  // phase (count 2).  The producer refills a slot only then, so an issuer
+  // that merely skips a slot can never fall a whole use behind it.
+  uint64_t* passed = pub_empty + 2 * kPubQ;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(passed + C::kMaxSlots);
   volatile int32_t* tq = reinterpret_cast<volatile int32_t*>(tmem_slot + 1);
   volatile int32_t* sq = tq + kTileQ;
   volatile uint32_t* tq_aux = reinterpret_cast<volatile uint32_t*>(sq + kSchedQ);  // staged tiles: ring slot
@@ -962,6 +966,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&pub_full[q], 1);
       mbar_init(&pub_empty[q], 1);
     }
+    for (int q = 0; q < C::kMaxSlots; ++q) mbar_init(&passed[q], 2);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -989,12 +994,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         ubits ^= 1u << stage;
         stage = stage + 1 == nslots ? 0 : stage + 1;
       };
-      auto wait_free = [&]() { mbar_wait(&empty[stage], ((ubits >> stage) & 1u) ^ 1u); };
+      const bool dual_mma = ra.dual_mma != 0;
+      auto slot_free = [&](uint32_t s) {
+        mbar_wait(&empty[s], ((ubits >> s) & 1u) ^ 1u);
+        if (dual_mma) mbar_wait(&passed[s], ((ubits >> s) & 1u) ^ 1u);
+      };
+      auto wait_free = [&]() { slot_free(stage); };
       auto set_layout = [&](int lay) {
         if (lay == layout) return;
         // drain every slot (staged CUDA-core slots are freed by the
         // epilogue, possibly before earlier MMA slots)
-        for (uint32_t s = 0; s < nslots; ++s) mbar_wait(&empty[s], ((ubits >> s) & 1u) ^ 1u);
+        for (uint32_t s = 0; s < nslots; ++s) slot_free(s);
         layout = lay;
         nslots = layout ? C::kNarrowSlots : kStages;
         sbytes = layout ? C::kNarrowBytes : C::kStageBytes;
@@ -1220,7 +1230,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int pre = min(k_blocks - kb_lo, static_cast<int>(nslots) - 1);
           uint32_t st = stage;
           for (int j = 0; j < pre; ++j) {
-            mbar_wait(&empty[st], ((ubits >> st) & 1u) ^ 1u);
+            slot_free(st);
             mbar_expect_tx(&full[st], tx);
             load_b(kb_lo + j, st);
             st = st + 1 == nslots ? 0 : st + 1;
@@ -1356,6 +1366,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // unwaited would let this warp lap the ring and take a still-pending
           // staged phase for its next GEMM use of the slot.
           mbar_wait(&full[stage], (fbits >> stage) & 1u);
+          if (ra.dual_mma && lane == 0) mbar_arrive(&passed[stage]);
           fbits ^= 1u << stage;
           stage = stage + 1 == nslots ? 0 : stage + 1;
         }
@@ -1413,6 +1424,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // every issuer waits on every stage (parity waits must stay one use
           // ahead at most); only the k-block's owner issues and frees it
           mbar_wait(&full[stage], (fbits >> stage) & 1u);
+          if (ra.dual_mma && lane == 0) mbar_arrive(&passed[stage]);
           const int owner = dual ? (kb - kb_lo) & 1 : 0;
           if (owner != role) {
             fbits ^= 1u << stage;
