@@ -7,7 +7,6 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
-#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <condition_variable>
@@ -210,7 +209,6 @@ struct Runtime {
                                  // (256 -> 128 -> 64) until it has this many tiles
   bool row_fold = true;          // S*Cin <= 32 convs (RGB stems) use the row-folded im2col path
   bool staged_cc = true;         // pools / depthwise convs as staged CUDA-core tiles (applies at registration)
-  bool dual_mma = false;         // narrow tiles' k-blocks split between two MMA-issuing warps (static schedule)
   bool dynamic_schedule = false;  // round programs: per-tenant ready queues (else static round-robin)
   bool greedy_schedule = false;   // round programs: greedy in-order tile claiming (else static round-robin)
   bool tall_tiles = true;         // 256-row tiles for narrow members of throughput-bound plans
@@ -259,7 +257,6 @@ struct Runtime {
     if (spec.tile_m != dev::kBM || (spec.tile_n != 128 && spec.tile_n != 256))
       throw std::invalid_argument("b200 runtime needs tile_m 128 and tile_n 128 or 256 (the super-kernel tile)");
     bn = static_cast<int>(spec.tile_n);
-    if (const char* e = std::getenv("GM_DUAL_MMA")) dual_mma = std::atoi(e) != 0;  // A/B override of the default
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) throw NoDevice("no CUDA device visible");
     if (dev_index >= count) throw NoDevice("CUDA device index out of range");
@@ -1267,7 +1264,7 @@ struct Runtime {
                       p.heads, p.qinfo, p.qinfo ? p.qinfo + p.nq : nullptr, p.nq,
                       p.greedy ? p.counters + p.n_counters + p.nq : nullptr,
                       p.counters && p.self_reset ? p.counters + p.n_counters + p.nq + 1 : nullptr,
-                      p.n_counters + p.nq + 1, dual_mma && bn == 256 && !p.heads ? 1 : 0};
+                      p.n_counters + p.nq + 1};
     void* args[4] = {&slots, &tiles, &n, &ra};
     cuda_check(cudaLaunchKernelExC(&cfg, kernel, args), "launch superkernel");
     if (ev_end) cuda_check(cudaEventRecordWithFlags(ev_end, stream, cudaEventRecordExternal), "event record");
@@ -1465,8 +1462,6 @@ int gm_ctx_set_option(gm_ctx* ctx, const char* name, int64_t value) {
     rt.greedy_schedule = value != 0;  // applies to round programs prepared afterwards
   } else if (n == "narrow_min_tiles") {
     rt.narrow_min_tiles = value;  // applies to plans prepared afterwards (0 = always full width)
-  } else if (n == "dual_mma") {
-    rt.dual_mma = value != 0;
   } else if (n == "staged_cc") {
     rt.staged_cc = value != 0;  // applies to tenants registered afterwards
 

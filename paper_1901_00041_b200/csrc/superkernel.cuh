@@ -210,23 +210,7 @@ struct RoundArgs {
   uint32_t* next_tile;        // greedy schedule: one global in-order claim counter (null = static / queues)
   uint32_t* exit_ctr;         // CTAs finished; the last one zeroes counters[0, n_reset) for the next launch
   int32_t n_reset;
-  // Two MMA issuers (static schedule only; the producer then claims its own
-  // tiles and warp 3 issues): a narrow tile's k-blocks alternate between
-  // warp 1 and warp 3, each accumulating into its own half of the tile's
-  // TMEM buffer (columns [0, 128) and [128, 256)); the epilogue adds them.
-  // Single-thread tcgen05.mma issue latency, not the tensor pipe, sets a
-  // narrow tile's k-block rate; two threads' issue latencies overlap.
-  int32_t dual_mma;
 };
-
-// A tile whose k-blocks the two MMA issuers split (see RoundArgs::dual_mma).
-__device__ __forceinline__ bool dual_tile(const MemberDesc* md, const TileEntry& te, int dual_mma) {
-  if (!dual_mma || md->tall || md->n_tile > 128 || te.splits > 1) return false;
-  const int kb_lo = te.kb_end ? te.kb_begin : 0;
-  const int k_tail = te.kb_end ? te.kb_end : md->k_blocks;
-  const int k_res = md->res && k_tail == md->k_blocks ? (min(md->n_tile, md->n - te.n_tile * md->n_tile) + 63) / 64 : 0;
-  return k_tail + k_res - kb_lo >= 2;
-}
 
 constexpr int kTileQ = 8;   // claimed-tile ring between producer and consumers
 constexpr int kDwTag = 1 << 30;  // tile-ring tag: a depthwise tile (no TMA / MMA work)
@@ -447,24 +431,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
-// Adds 32 columns of a second accumulator (a dual tile's issuer-B half) into
-// v, 16 columns per load to bound live registers.
-__device__ __forceinline__ void tmem_add32(uint32_t taddr, uint32_t (&v)[32]) {
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    uint32_t w[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
-        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]),
-          "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
-        : "r"(taddr + 16 * h));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[16 * h + i] = __float_as_uint(__uint_as_float(v[16 * h + i]) + __uint_as_float(w[i]));
-  }
 }
 
 // Activations: relu / relu6 are a clamp [lo, hi] applied while packing
@@ -914,11 +880,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* sq_empty = sq_full + kSchedQ;
   uint64_t* pub_full = sq_empty + kSchedQ;  // [2][kPubQ]: epilogue warpgroup -> publisher warp
   uint64_t* pub_empty = pub_full + 2 * kPubQ;
-  // dual_mma: per ring slot, both MMA issuers have passed the slot's current
-  // phase (count 2).  The producer refills a slot only then, so an issuer
-  // that merely skips a slot can never fall a whole use behind it.
-  uint64_t* passed = pub_empty + 2 * kPubQ;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(passed + C::kMaxSlots);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pub_empty + 2 * kPubQ);
   volatile int32_t* tq = reinterpret_cast<volatile int32_t*>(tmem_slot + 1);
   volatile int32_t* sq = tq + kTileQ;
   volatile uint32_t* tq_aux = reinterpret_cast<volatile uint32_t*>(sq + kSchedQ);  // staged tiles: ring slot
@@ -951,12 +913,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
-      mbar_init(&acc_full[a], ra.dual_mma ? 2 : 1);  // one commit per MMA issuer
+      mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], 128);
     }
     for (int q = 0; q < kTileQ; ++q) {
       mbar_init(&tq_full[q], 1);
-      mbar_init(&tq_empty[q], (ra.dual_mma ? 2 : 1) + 8);  // the MMA issuer(s) + one lane per epilogue warp
+      mbar_init(&tq_empty[q], 1 + 8);  // the MMA thread + one lane per epilogue warp
     }
     for (int q = 0; q < kSchedQ; ++q) {
       mbar_init(&sq_full[q], 1);
@@ -966,7 +928,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&pub_full[q], 1);
       mbar_init(&pub_empty[q], 1);
     }
-    for (int q = 0; q < C::kMaxSlots; ++q) mbar_init(&passed[q], 2);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -994,17 +955,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         ubits ^= 1u << stage;
         stage = stage + 1 == nslots ? 0 : stage + 1;
       };
-      const bool dual_mma = ra.dual_mma != 0;
-      auto slot_free = [&](uint32_t s) {
-        mbar_wait(&empty[s], ((ubits >> s) & 1u) ^ 1u);
-        if (dual_mma) mbar_wait(&passed[s], ((ubits >> s) & 1u) ^ 1u);
-      };
-      auto wait_free = [&]() { slot_free(stage); };
+      auto wait_free = [&]() { mbar_wait(&empty[stage], ((ubits >> stage) & 1u) ^ 1u); };
       auto set_layout = [&](int lay) {
         if (lay == layout) return;
         // drain every slot (staged CUDA-core slots are freed by the
         // epilogue, possibly before earlier MMA slots)
-        for (uint32_t s = 0; s < nslots; ++s) slot_free(s);
+        for (uint32_t s = 0; s < nslots; ++s) mbar_wait(&empty[s], ((ubits >> s) & 1u) ^ 1u);
         layout = lay;
         nslots = layout ? C::kNarrowSlots : kStages;
         sbytes = layout ? C::kNarrowBytes : C::kStageBytes;
@@ -1016,8 +972,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       // from one global counter, the next one as it starts a tile's loads (a
       // one-tile look-ahead instead of the static round-robin assignment).
       const bool greedy = ra.next_tile != nullptr;
-      const bool self_sched = ra.dual_mma != 0;  // warp 3 issues MMAs: static round-robin here
-      int static_next = blockIdx.x;
       int next = 0;
       if (greedy) {
         // the claim counter is reset by the previous launch's last CTA
@@ -1028,12 +982,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         int t;
         if (greedy) {
           t = next < n_tiles ? next : -1;
-        } else if (self_sched) {
-          t = static_next < n_tiles ? static_next : -1;
-          static_next += gridDim.x;
-          if (static_next < n_tiles) {  // pull the next tile's entry and descriptor toward the SM
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(tiles + static_next));
-          }
         } else {
           mbar_wait(&sq_full[sslot], sphase);  // next tile from the scheduler warp
           t = sq[sslot];
@@ -1230,7 +1178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int pre = min(k_blocks - kb_lo, static_cast<int>(nslots) - 1);
           uint32_t st = stage;
           for (int j = 0; j < pre; ++j) {
-            slot_free(st);
+            mbar_wait(&empty[st], ((ubits >> st) & 1u) ^ 1u);
             mbar_expect_tx(&full[st], tx);
             load_b(kb_lo + j, st);
             st = st + 1 == nslots ? 0 : st + 1;
@@ -1332,9 +1280,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (first) asm volatile("griddepcontrol.wait;" ::: "memory");
     }
-  } else if (warp == 1 || (warp == 3 && ra.dual_mma)) {
-    // ------------------------------------------------ MMA issuer(s)
-    const int role = warp == 3 ? 1 : 0;  // dual_mma: issuer B takes a dual tile's odd k-blocks
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
     // The whole warp runs the loop on warp-uniform values (tile fields are
     // broadcast from lane 0 with shfl), so the descriptor arithmetic lives in
     // uniform registers; one elected lane issues tcgen05.mma / commit.
@@ -1366,7 +1313,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           // unwaited would let this warp lap the ring and take a still-pending
           // staged phase for its next GEMM use of the slot.
           mbar_wait(&full[stage], (fbits >> stage) & 1u);
-          if (ra.dual_mma && lane == 0) mbar_arrive(&passed[stage]);
           fbits ^= 1u << stage;
           stage = stage + 1 == nslots ? 0 : stage + 1;
         }
@@ -1414,36 +1360,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint64_t b_hi64 = static_cast<uint64_t>((1024u >> 4) | (1u << 14) | (2u << 29)) << 32;
       mbar_wait(&acc_empty[acc], acc_phase ^ 1);
       tc_fence_after();
-      const bool dual = __shfl_sync(0xffffffffu, dual_tile(md, te, ra.dual_mma) ? 1 : 0, 0) != 0;
-      const uint32_t d_tmem = tmem_base + acc * BN + (dual && role ? 128u : 0u);
+      const uint32_t d_tmem = tmem_base + acc * BN;
       // One k-block: wait for its stage, issue `halves` x 4 UMMA_K steps, free
       // the stage.  Two loop instances so the common path carries no test.
       auto kloop = [&](auto halves_c) {
         constexpr int kHalves = decltype(halves_c)::value;
         for (int kb = kb_lo; kb < k_blocks; ++kb) {
-          // every issuer waits on every stage (parity waits must stay one use
-          // ahead at most); only the k-block's owner issues and frees it
           mbar_wait(&full[stage], (fbits >> stage) & 1u);
-          if (ra.dual_mma && lane == 0) mbar_arrive(&passed[stage]);
-          const int owner = dual ? (kb - kb_lo) & 1 : 0;
-          if (owner != role) {
-            fbits ^= 1u << stage;
-            stage = stage + 1 == nslots ? 0 : stage + 1;
-            continue;
-          }
           tc_fence_after();
           if (trace && kb == kb_lo && lane == 0) trace[6 * t + 2] = globaltimer();
           const uint32_t a_addr = ring_base + stage * sbytes;
           const uint32_t a_lo = ((a_addr >> 4) & 0x3FFFu) | a_lbo;
           const uint32_t b_lo = (((a_addr + (kABytes * kHalves)) >> 4) & 0x3FFFu) | (1u << 16);
-          const uint32_t first = kb - kb_lo <= (dual ? 1 : 0) ? 1u : 0u;  // this issuer's first k-block
           if (elect_one()) {
 #pragma unroll
             for (int h = 0; h < kHalves; ++h) {
               // half h: A box at +16 KB * h, accumulator columns + n_tile * h
               const uint32_t ah = a_lo + h * (kABytes >> 4);
               const uint32_t dh = d_tmem + h * d_half;
-              umma_bf16(dh, a_hi64 | ah, b_hi64 | b_lo, idesc, first ^ 1u);
+              umma_bf16(dh, a_hi64 | ah, b_hi64 | b_lo, idesc, kb != kb_lo ? 1u : 0u);
               umma_bf16(dh, a_hi64 | (ah + k1), b_hi64 | (b_lo + 2), idesc, 1u);
               umma_bf16(dh, a_hi64 | (ah + k2), b_hi64 | (b_lo + 4), idesc, 1u);
               umma_bf16(dh, a_hi64 | (ah + k3), b_hi64 | (b_lo + 6), idesc, 1u);
@@ -1459,9 +1394,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         kloop(std::integral_constant<int, 2>{});
       else
         kloop(std::integral_constant<int, 1>{});
-      if (elect_one()) umma_commit(&acc_full[acc]);  // (each issuer's) accumulator ready for the epilogue
+      if (elect_one()) umma_commit(&acc_full[acc]);  // accumulator ready for the epilogue
       __syncwarp();
-      if (trace && lane == 0 && role == 0) trace[6 * t + 3] = globaltimer();
+      if (trace && lane == 0) trace[6 * t + 3] = globaltimer();
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -1494,7 +1429,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 3) {
-    if (lane == 0 && !ra.next_tile) {  // greedy (and dual_mma): the producer claims its own tiles
+    if (lane == 0 && !ra.next_tile) {  // greedy: the producer claims its own tiles
       // ------------------------------------------------ tile scheduler
       // Claims this CTA's next tile (static round-robin, or the head of a
       // ready per-tenant queue) up to kSchedQ tiles ahead of the producer, so
@@ -1728,7 +1663,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (trace && quarter == 0 && lane == 0) trace[6 * t + 4] = globaltimer();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
       bool publish = te.done >= 0;
-      const bool dual = dual_tile(md, te, ra.dual_mma);
       if (te.splits > 1) {
         // ---- split-K partial: coalesced fp32 red.add into the workspace tile.
         // Lane-major layout: the 32 lanes' float4 of (chunk c, j) are 512
@@ -1789,7 +1723,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c = 0; c < cols; c += kEpiChunk) {
             uint32_t v[32];
             tmem_ld32(tcol + c, v);
-            if (dual) tmem_add32(tcol + 128 + c, v);  // issuer B's partial sum of the K loop
             store_bf16(v, c, mrow);
           }
         }

@@ -400,8 +400,7 @@ def test_round_dependency_graph():
 
 
 @pytest.mark.parametrize("options", [{}, {"greedy_schedule": 1}, {"dynamic_schedule": 1}, {"critical_order": 0},
-                                     {"split_k": 1, "narrow_min_tiles": 64}, {"dual_mma": 0},
-                                     {"dual_mma": 1, "narrow_min_tiles": 64, "tall_tiles": 0}, {"staged_cc": 0}])
+                                     {"split_k": 1, "narrow_min_tiles": 64}, {"staged_cc": 0}])
 def test_dataflow_chain_every_schedule(oracle, options):
     """A chained ResNet-18 + MobileNet-v2 round (layer l reads layer l-1's
     output, residual adds read earlier layers) under every tile schedule,
