@@ -512,9 +512,10 @@ def run_ours(args):
         "e2e": {"value": world * flops_round / e2e_s / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
                 "api": "SpaceTimeEngine.serve_rounds: K back-to-back rounds from pinned host batches (two sets "
-                       "alternating), double-buffered: step i+1's H2D overlaps round i, landing in the query "
-                       "input of a second registration of the tenants whose round program alternates with the "
-                       "first's; every step's H2D, round program and D2H inside the timed wall-clock region",
+                       "alternating), double-buffered: a second registration of the tenants with its own query "
+                       "inputs and results alternates with the first, so step i+1's H2D and step i-1's D2H (two "
+                       "copy streams) overlap round i; every step's H2D, round program and D2H inside the timed "
+                       "wall-clock region",
                 "single_round": {"value": world * flops_round / e2e_sync_s / 1e12, "ms_per_step": e2e_sync_s * 1e3,
                                  "median_ms": sorted(e2e_times)[len(e2e_times) // 2] * 1e3,
                                  "min_ms": min(e2e_times) * 1e3,

@@ -280,12 +280,13 @@ class SpaceTimeEngine:
         return rnd
 
     def _alternate_round(self):
-        """A second registration of every tenant whose query input is its own
-        buffer (every other buffer shared), and its round program: serve_rounds
-        alternates the two, so step i+1's batch lands in the input step i is
-        not reading and no device-to-device staging move sits between rounds."""
+        """A second registration of every tenant whose query input and result
+        are its own buffers (every other buffer shared), and its round program:
+        serve_rounds alternates the two, so step i+1's batch lands in the input
+        step i is not reading, step i's results are copied out while step i+1
+        runs, and no device-to-device staging move sits between rounds."""
         import dataclasses
-        alt_inputs, alt_tenants = [], []
+        alt_inputs, alt_outputs, alt_tenants = [], [], []
         for t, m in zip(self.tenants, self.models):
             q = m.query_input
             xin = torch.zeros_like(q)
@@ -298,10 +299,13 @@ class SpaceTimeEngine:
                 return torch.as_strided(xin, tensor.size(), tensor.stride(), xin.storage_offset() + off)
 
             bufs = [dataclasses.replace(b, x=remap(b.x), res=remap(b.res)) for b in m.buffers]
+            yout = torch.empty_like(m.query_output)  # the last layer's output: nothing reads it in the round
+            bufs[-1] = dataclasses.replace(bufs[-1], y=yout)
             alt_inputs.append(xin)
+            alt_outputs.append(yout)
             alt_tenants.append(self.ctx.register_tenant(bufs, slo_latency=self.ctx_slo, tenant_id=f"alt{t}"))
         rnd = self.ctx.plan_round(alt_tenants, self._now)
-        return alt_inputs, self.capture_round(rnd)
+        return alt_inputs, alt_outputs, self.capture_round(rnd)
 
     def serve_rounds(self, steps: Sequence[Tuple[Sequence[torch.Tensor], Sequence[torch.Tensor]]],
                      stream: torch.cuda.Stream) -> Round:
@@ -341,27 +345,37 @@ class SpaceTimeEngine:
         if getattr(self, "_alt", None) is None:
             self._alt = self._alternate_round()
             self._copy_stream = torch.cuda.Stream(self.device)
-        alt_inputs, g_alt = self._alt
+            self._out_stream = torch.cuda.Stream(self.device)
+        alt_inputs, alt_outputs, g_alt = self._alt
         inputs = [[m.query_input for m in self.models], alt_inputs]
+        outputs = [[m.query_output for m in self.models], alt_outputs]
         graphs = [g, g_alt]
-        cs = self._copy_stream
+        cs, ds = self._copy_stream, self._out_stream  # H2D and D2H run in both directions at once
         landed = [torch.cuda.Event(), torch.cuda.Event()]
-        released = [torch.cuda.Event(), torch.cuda.Event()]
+        done = [torch.cuda.Event(), torch.cuda.Event()]
+        drained = [torch.cuda.Event(), torch.cuda.Event()]
         cs.wait_stream(stream)
+        ds.wait_stream(stream)
         for i, (h_in, h_out) in enumerate(steps):
             b = i & 1
             with torch.cuda.stream(cs):
                 if i >= 2:
-                    cs.wait_event(released[b])  # input set b read by step i-2's round
+                    cs.wait_event(done[b])  # input set b read by step i-2's round
                 for d, h in zip(inputs[b], h_in):
                     d.view(-1).copy_(h.view(-1), non_blocking=True)
                 landed[b].record(cs)
             with torch.cuda.stream(stream):
                 stream.wait_event(landed[b])
+                if i >= 2:
+                    stream.wait_event(drained[b])  # output set b copied out after step i-2
                 graphs[b].launch(stream.cuda_stream)
-                released[b].record(stream)
-                for m, h in zip(self.models, h_out):
-                    h.view(-1).copy_(m.query_output.view(-1), non_blocking=True)
+                done[b].record(stream)
+            with torch.cuda.stream(ds):
+                ds.wait_event(done[b])
+                for y, h in zip(outputs[b], h_out):
+                    h.view(-1).copy_(y.view(-1), non_blocking=True)
+                drained[b].record(ds)
+        ds.synchronize()
         stream.synchronize()
         return rnd
 
