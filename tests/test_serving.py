@@ -137,11 +137,13 @@ def test_bounded_plan_cache_with_background_planning():
     specs = [ServeTenant(_layers(), max_batch=2, batches=[1, 2], rate_qps=900.0, slo_latency=0.2, io_slots=4)
              for _ in range(6)]
     eng = ServingEngine(specs, device_index=0)
-    r = eng.serve(duration=1.0, warmup=0.05, max_wait=0.0005, prewarm=0, plan_cache_cap=16, async_plan=True)
+    # cap 13: the 12 pinned single-tenant sets plus one, so a second admitted
+    # set already evicts (sets are admitted on their second sighting)
+    r = eng.serve(duration=1.0, warmup=0.05, max_wait=0.0005, prewarm=0, plan_cache_cap=13, async_plan=True)
     s = r.stats
     assert s["queries"] > 500
     assert s["plan_fallbacks"] > 0 and s["plan_misses"] >= s["plan_fallbacks"]
-    assert s["plan_evictions"] > 0 and s["plans_cached"] <= 16
+    assert s["plan_evictions"] > 0 and s["plans_cached"] <= 14  # (+1: a victim may still be in flight)
     launches = [e["launches"] for e in r.dispatches]
     # fallbacks ran as a padded cached superset (one round) or a cover of cached sub-sets
     assert min(launches) == 1 and sum(n > 1 for n in launches) + s["plan_padded"] == s["plan_fallbacks"]
