@@ -13,6 +13,7 @@
 #include <map>
 #include <mutex>
 #include <random>
+#include <set>
 #include <string>
 #include <thread>
 #include <unordered_map>
@@ -2360,7 +2361,15 @@ extern "C" int gm_serve(gm_ctx* ctx, const gm_serve_tenant* tenants, size_t n, c
     }
     return std::make_pair(&rt.prepare_round(plans), to_seconds(end));
   };
+  // round programs that existed before this call (other launch programs may
+  // hold them) are never evicted
+  std::set<const Prepared*> preexisting;
+  {
+    std::lock_guard<std::recursive_mutex> lock(rt.rounds_mu);
+    for (const auto& [k, pr] : rt.rounds) preexisting.insert(&pr);
+  }
   auto insert = [&](const std::vector<int>& key, std::pair<Prepared*, double> pp, bool pinned) {
+    pinned = pinned || preexisting.count(pp.first) > 0;
     auto it = cache.emplace(key, Cached{pp.first, pp.second, ++use_clock, 0, pinned, key.size()}).first;
     if (cfg->plan_cache_cap > 0) {
       while (static_cast<int64_t>(cache.size()) > cfg->plan_cache_cap) {
