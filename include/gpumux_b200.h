@@ -385,7 +385,7 @@ int gm_ctx_set_policy(gm_ctx* ctx, const gm_batch_policy* p);
  *                       over K across the idle SMs; 0 = off (64);
  *                       "skinny_max_splits" (8)
  *   "ring_layouts"      narrow members use a 6 x 32 KB operand ring (1)
- *   "critical_order"    round tile order: -1 auto, 0 plan, 1 remaining work,
+ *   "critical_order"    round tile order: -1 auto (= 2), 0 plan, 1 remaining work,
  *                       2 chain progress (-1)
  *   "greedy_schedule"   greedy in-order tile claiming instead of static
  *                       round-robin (0); "dynamic_schedule": per-tenant queues (0)

@@ -215,7 +215,7 @@ struct Runtime {
   bool tall_tiles = true;         // 256-row tiles for narrow members of throughput-bound plans
   int ring_layouts = 1;           // narrow members use the 6 x 32 KB ring layout (applies at registration)
   int critical_order = -1;        // round programs: tile order 0 plan, 1 remaining chain work, 2 chain progress,
-                                  // -1 auto (2 for homogeneous tenants, else 0)
+                                  // -1 auto (2: chain progress)
   int64_t tall_min_tiles = 0;     // concurrent same-shape tiles that make a member "throughput-bound" (0 = 2 x SMs)
   int bn = 256;     // N tile of the super-kernel (== DeviceSpec.tile_n)
   uint32_t* host_one = nullptr;  // pinned 4-byte 1: DMA source that opens an input gate
@@ -1043,29 +1043,11 @@ struct Runtime {
     // longest first.  Remaining work strictly decreases along a chain, so the
     // order stays topological; with heterogeneous tenants the longest chain's
     // tiles reach the SMs first instead of following the virtual-clock plan.
-    int order = critical_order;
-    if (order < 0) {
-      // auto: progress order when every tenant of the round runs the same
-      // layer list (measured +5-9% on ResNet-50 / BERT rounds), else the
-      // virtual-clock plan order (better for mixed models)
-      std::vector<int> ts_round;
-      for (const auto& pl : plans)
-        for (int f : pl) ts_round.push_back(flat[f].tenant);
-      std::sort(ts_round.begin(), ts_round.end());
-      ts_round.erase(std::unique(ts_round.begin(), ts_round.end()), ts_round.end());
-      bool same = true;
-      for (int t2 : ts_round) {
-        const auto& a = tenant_ops[t2];
-        const auto& b = tenant_ops[ts_round.front()];
-        if (a.size() != b.size()) {
-          same = false;
-          break;
-        }
-        for (size_t j = 0; j < a.size() && same; ++j) same = flat[a[j]].shape == flat[b[j]].shape;
-        if (!same) break;
-      }
-      order = same ? 2 : 0;
-    }
+    // auto (-1): progress order.  Round 1 kept the virtual-clock plan order
+    // for mixed models; with row-block dependencies and staged CUDA-core
+    // tiles the progress order is ahead there too (C3 mix b4 1046 -> 979 us,
+    // b8 1537 -> 1506 us; homogeneous rounds +5-9% as before).
+    const int order = critical_order < 0 ? 2 : critical_order;
     if (order && !table.empty()) {
       // mode 1: remaining FLOPs (longest chain first); mode 2: chain progress
       // (fraction of the tenant's FLOPs before this layer, ascending), which

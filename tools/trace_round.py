@@ -33,12 +33,16 @@ def main():
     a = ap.parse_args()
     peaks = json.load(open("MEASURED_PEAKS.json"))
     P, BW = peaks["bf16_tflops"] * 1e12, peaks["hbm_gbs"] * 1e9
-    layers = W.resnet50(224) if a.model == "resnet50" else W.MODELS[a.model]()
+    layers = W.resnet50(224) if a.model in ("resnet50", "mix") else W.MODELS[a.model]()
     opts = {kv.split("=")[0]: int(kv.split("=")[1]) for kv in a.opt}
     from paper_1901_00041_b200.scheduler import b200_profile
     spec = b200_profile()
     spec.tile_n = a.tile_n
-    eng = SpaceTimeEngine([layers] * a.tenants, [a.batch] * a.tenants, options=opts, device_spec=spec)
+    if a.model == "mix":  # BASELINE configs[2]: ResNet-50 + VGG-16 + MobileNet-v2 @224, two each
+        tl = [W.resnet50(224), W.vgg16(224), W.mobilenet_v2(224)] * 2
+    else:
+        tl = [layers] * a.tenants
+    eng = SpaceTimeEngine(tl, [a.batch] * len(tl), options=opts, device_spec=spec)
     rnd = eng.plan_round(BatchPolicy(target_batch=0, max_waves=a.max_waves))
     s = torch.cuda.Stream()
     for _ in range(3):
@@ -58,15 +62,15 @@ def main():
         by_plan[tile.flags].append(t[i])
     rows = []
     tot_roof = 0.0
+    pos_of = {t: i for i, t in enumerate(eng.tenants)}
     for pi, k in enumerate(rnd.kernels):
         ts = by_plan[pi]
         span = (max(x[5] for x in ts) - min(x[0] for x in ts)) / 1e3
         start = (min(x[0] for x in ts) - t0) / 1e3
         mean = lambda a, b: sum(x[b] - x[a] for x in ts) / len(ts) / 1e3  # noqa: E731
-        sh = k.members[0].shape
-        layer = next(L for L in layers if tuple(L.gemm_shape(a.batch).__dict__.values()) == (sh.m, sh.n, sh.k))
-        F = len(k.members) * layer.flops(a.batch)
-        B = len(k.members) * layer.compulsory_bytes(a.batch)
+        mlayers = [eng.models[pos_of[r.tenant_index]].layers[r.layer_index] for r in k.members]
+        F = sum(L.flops(a.batch) for L in mlayers)
+        B = sum(L.compulsory_bytes(a.batch) for L in mlayers)
         roof = max(F / P, B / BW) * 1e6
         tot_roof += roof
         row = dict(plan=pi, sig=k.shape_signature, tiles=len(ts), start_us=start, span_us=span, roof_us=roof,
