@@ -33,7 +33,10 @@ def main():
     a = ap.parse_args()
     peaks = json.load(open("MEASURED_PEAKS.json"))
     P, BW = peaks["bf16_tflops"] * 1e12, peaks["hbm_gbs"] * 1e9
-    layers = W.resnet50(224) if a.model in ("resnet50", "mix") else W.MODELS[a.model]()
+    if a.model == "bert":  # BASELINE configs[3]: 12-layer BERT-base GEMM chain, seq 128
+        layers = W.bert_base_gemms(128, layers=12)
+    else:
+        layers = W.resnet50(224) if a.model in ("resnet50", "mix") else W.MODELS[a.model]()
     opts = {kv.split("=")[0]: int(kv.split("=")[1]) for kv in a.opt}
     from paper_1901_00041_b200.scheduler import b200_profile
     spec = b200_profile()
