@@ -662,6 +662,15 @@ def round_modes(torch, eng, stream, steps, warmup=3):
                      "p99_ms": nearest_rank(per, 99.0), "launches_per_step": g.kernels}
     out["packed_over_space_only"] = out["space_only"]["ms_per_step"] / out["packed"]["ms_per_step"]
     out["packed_over_time_only"] = out["time_only"]["ms_per_step"] / out["packed"]["ms_per_step"]
+    # the packed round against its rooflines (same definitions as the headline's)
+    burst, _, hbm, _ = load_peaks()
+    attain_s = sum(max(L.flops(m.batch) / (burst * 1e12), L.compulsory_bytes(m.batch) / (hbm * 1e9))
+                   for m in eng.models for L in m.layers)
+    tf = out["packed"]["tflops"]
+    out["roofline"] = {"frac_of_dense_bf16_burst": tf / burst, "attainable_tflops": eng.flops_per_round() / attain_s / 1e12,
+                       "frac_of_attainable": tf / (eng.flops_per_round() / attain_s / 1e12),
+                       "hbm_gbs": eng.compulsory_bytes_per_round() / (out["packed"]["ms_per_step"] / 1e3) / 1e9,
+                       "frac_of_hbm": eng.compulsory_bytes_per_round() / (out["packed"]["ms_per_step"] / 1e3) / 1e9 / hbm}
     return out
 
 
