@@ -581,20 +581,24 @@ def serve_session(eng, seconds, rank, world, dist, **kw):
     return st
 
 
-def serve_points(factory, seconds, rank=0, world=1, dist=None, slo_mult=2.0, **kw):
+def serve_points(factory, seconds, rank=0, world=1, dist=None, slo_mults=(2.0, 4.0), **kw):
     """Closed-loop saturation, Poisson at 50% / 80% of the saturated query
-    rate under the tenants' own SLOs, and an SLO-bound point: Poisson at 80%
-    with every SLO set to ``slo_mult`` x the saturated mean round time, so the
-    batcher's SLO trigger and the violation count are exercised.  Queries
-    carry data (per-query H2D / D2H inside the serving loop)."""
+    rate under the tenants' own SLOs, and SLO-bound points: Poisson at 80%
+    with every SLO set to each of ``slo_mults`` x the saturated mean round
+    time (2x: about one round of queueing plus the query's own round, so the
+    batcher's SLO trigger fires and violations are counted; 4x: a binding SLO
+    the loop can hold).  Queries carry data (per-query H2D / D2H inside the
+    serving loop)."""
     sat = serve_session(factory(None, None), seconds, rank, world, dist, **kw)
     pts = {"closed_loop": sat}
     for f in (0.5, 0.8):
         pts[f"poisson_{int(f * 100)}pct"] = dict(serve_session(factory(f * sat["qps"], None), seconds, rank, world,
                                                                dist, **kw), load=f)
-    slo = slo_mult * sat["mean_round_ms"] / 1e3
-    pts["slo_bound_80pct"] = dict(serve_session(factory(0.8 * sat["qps"], slo), seconds, rank, world, dist, **kw),
-                                  load=0.8, slo_ms=slo * 1e3)
+    for i, mult in enumerate(slo_mults):
+        slo = mult * sat["mean_round_ms"] / 1e3
+        key = "slo_bound_80pct" if i == 0 else f"slo_bound_80pct_{mult:g}x"
+        pts[key] = dict(serve_session(factory(0.8 * sat["qps"], slo), seconds, rank, world, dist, **kw),
+                        load=0.8, slo_ms=slo * 1e3, slo_mult=mult)
     return pts
 
 
