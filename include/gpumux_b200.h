@@ -380,6 +380,9 @@ int gm_ctx_set_policy(gm_ctx* ctx, const gm_batch_policy* p);
  *                       that count as throughput-bound (0 = 2 x SMs)
  *   "split_k"           round programs split few-tile long-K members (0);
  *                       "max_splits" (4), "split_min_kb" (8)
+ *   "split_wide_kb"     a member narrowed below 128 columns with at least this
+ *                       many k-blocks keeps 128-column tiles and splits K over
+ *                       the same tile count instead; 0 = off (0)
  *   "skinny_min_mb"     round programs split weight-streaming GEMM members
  *                       (M <= 64, at least this many MB of weights, e.g. fc6)
  *                       over K across the idle SMs; 0 = off (64);

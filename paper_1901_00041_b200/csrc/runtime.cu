@@ -208,6 +208,8 @@ struct Runtime {
   int64_t skinny_max_splits = 8;
   int64_t narrow_min_tiles = 20;  // >0: in a plan that cannot fill the SMs, narrow a member's N tile
                                  // (256 -> 128 -> 64) until it has this many tiles
+  int64_t split_wide_kb = 0;     // >0: a member narrowed below 128 columns with >= this many k-blocks keeps
+                                 // 128-column tiles and splits K instead (same tile count, half the k-blocks each)
   bool row_fold = true;          // S*Cin <= 32 convs (RGB stems) use the row-folded im2col path
   bool staged_cc = true;         // pools / depthwise convs as staged CUDA-core tiles (applies at registration)
   bool dynamic_schedule = false;  // round programs: per-tenant ready queues (else static round-robin)
@@ -933,6 +935,38 @@ struct Runtime {
             skinny_splits = static_cast<int>(sp);
           }
         }
+        // Wide split (option): a long-K member that narrowing took below 128
+        // columns keeps 128-column tiles and splits its K loop over as many
+        // tiles as the narrow variant had -- a narrow tile's k-block costs
+        // about what a 128-column one does (MMA / TMA issue bound), so each
+        // split runs a fraction of the K loop at the same per-k-block cost.
+        int wide_splits = 1;
+        if (split_wide_kb > 0 && skinny_splits == 1 && !is_tall(slot) && w < 128 &&
+            (op.shape.k + dev::kBK - 1) / dev::kBK >= split_wide_kb) {
+          int ws_slot = -1, ww = 0;
+          if (op.n_tile == 128) {
+            ws_slot = op.slot;
+            ww = 128;
+          } else {
+            for (int i = 0; i < 2; ++i)
+              if (op.narrow_slot[i] >= 0 && op.narrow_w[i] == 128) {
+                ws_slot = op.narrow_slot[i];
+                ww = 128;
+              }
+          }
+          if (ws_slot >= 0) {
+            const int64_t mt0 = (op.shape.m + dev::kBM - 1) / dev::kBM;
+            const int64_t target = mt0 * ((op.shape.n + w - 1) / w);
+            const int64_t wide = mt0 * ((op.shape.n + ww - 1) / ww);
+            const int64_t sp = std::min<int64_t>({target / wide, max_splits,
+                                                  host_desc[ws_slot].k_blocks / std::max<int64_t>(1, split_min_kb)});
+            if (sp >= 2) {
+              slot = ws_slot;
+              w = ww;
+              wide_splits = static_cast<int>(sp);
+            }
+          }
+        }
         const bool tall = is_tall(slot);
         // Dependencies.  Dataflow layers wait on the producer row blocks
         // their rows read (input and residual); a layer without a producer in
@@ -994,6 +1028,10 @@ struct Runtime {
         if (skinny_splits > 1) {
           const int kbw = host_desc[slot].k_blocks;
           const int chunk = (kbw + skinny_splits - 1) / skinny_splits;
+          splits = (kbw + chunk - 1) / chunk;
+        } else if (wide_splits > 1) {
+          const int kbw = host_desc[slot].k_blocks;
+          const int chunk = (kbw + wide_splits - 1) / wide_splits;
           splits = (kbw + chunk - 1) / chunk;
         } else if (split_k && !tall && plan_tiles < sms && kb >= 2 * split_min_kb) {
           splits = static_cast<int>(
@@ -1417,6 +1455,9 @@ int gm_ctx_set_option(gm_ctx* ctx, const char* name, int64_t value) {
     rt.pdl = value != 0;
   } else if (n == "split_k") {
     rt.split_k = value != 0;
+  } else if (n == "split_wide_kb") {
+    if (value < 0) throw std::invalid_argument("split_wide_kb must be >= 0");
+    rt.split_wide_kb = value;  // applies to round programs prepared afterwards (0 = off)
   } else if (n == "max_splits") {
     if (value < 2 || value > 64) throw std::invalid_argument("max_splits must be in [2, 64]");
     rt.max_splits = value;

@@ -292,10 +292,14 @@ def test_heterogeneous_models_round_program(oracle):
                                      {"critical_order": 1}, {"critical_order": 2, "greedy_schedule": 1},
                                      {"ring_layouts": 0}, {"skinny_min_mb": 0},
                                      {"skinny_min_mb": 1, "split_min_kb": 2},
-                                     {"skinny_min_mb": 1, "split_min_kb": 1, "skinny_max_splits": 64}])
+                                     {"skinny_min_mb": 1, "split_min_kb": 1, "skinny_max_splits": 64},
+                                     {"split_wide_kb": 2, "narrow_min_tiles": 64},
+                                     {"split_wide_kb": 2, "narrow_min_tiles": 64, "split_min_kb": 1, "max_splits": 8}])
 def test_execution_options_keep_results(oracle, options):
     eng = small_engine(tenants=2, batch=4, options=options)
     rnd = eng.plan_round()
+    if "split_wide_kb" in options:  # the option took effect: 128-column split tiles
+        assert any(t["splits"] > 1 and t["cols"] == 128 for t in rnd.tile_info())
     clear(eng)
     s = torch.cuda.Stream()
     rnd.launch_round(s.cuda_stream)
@@ -400,7 +404,8 @@ def test_round_dependency_graph():
 
 
 @pytest.mark.parametrize("options", [{}, {"greedy_schedule": 1}, {"dynamic_schedule": 1}, {"critical_order": 0},
-                                     {"split_k": 1, "narrow_min_tiles": 64}, {"staged_cc": 0}])
+                                     {"split_k": 1, "narrow_min_tiles": 64}, {"staged_cc": 0},
+                                     {"split_wide_kb": 2, "narrow_min_tiles": 64, "split_min_kb": 1}])
 def test_dataflow_chain_every_schedule(oracle, options):
     """A chained ResNet-18 + MobileNet-v2 round (layer l reads layer l-1's
     output, residual adds read earlier layers) under every tile schedule,
