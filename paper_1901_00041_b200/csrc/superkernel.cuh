@@ -1670,20 +1670,46 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr int kChunks = BN / kEpiChunk;
         float* wq = ra.ws + (static_cast<int64_t>(te.ws) * 4 + quarter) * (kChunks * 8 * 128);
         uint32_t* ctr = ra.split_ctr + te.ws * 4 + quarter;
-        const bool finisher = te.kb_end == md->k_blocks;  // the split holding the K tail
+        // Finisher: with two splits, whichever warp of the pair arrives
+        // second (per TMEM lane quarter), so it never waits for its partner's
+        // K loop, only for the partner's partial store (the first arrival
+        // counts 1, its 32 lanes release 1 each after storing, the second
+        // adds its own 1: 34); with more, the split holding the K tail waits
+        // for every other split's lanes.
+        bool finisher;
+        uint32_t want;
+        if (te.splits == 2) {
+          uint32_t old = 0;
+          if (lane == 0) old = atomicAdd(ctr, 1u);
+          finisher = __shfl_sync(0xffffffffu, old, 0) != 0;
+          want = 34u;
+        } else {
+          finisher = te.kb_end == md->k_blocks;
+          want = static_cast<uint32_t>(te.splits - 1) * 32u;
+        }
         if (!finisher) {
-          // fire and forget: reduce-add the partial, then a release arrival
-          // per lane (orders this lane's reductions before it); no waiting
+          // fire and forget: reduce-add the partial (two splits: the only
+          // other writer is the finisher, so a plain store), then a release
+          // arrival per lane (orders this lane's writes before it); no waiting
+          const bool plain = te.splits == 2;
           for (int c = 0; c < cols; c += kEpiChunk) {
             uint32_t v[32];
             tmem_ld32(taddr + c, v);
             float* wc = wq + (c / kEpiChunk) * (8 * 128) + lane * 4;
+            if (plain) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(wc + j * 128),
-                           "f"(__uint_as_float(v[4 * j])), "f"(__uint_as_float(v[4 * j + 1])),
-                           "f"(__uint_as_float(v[4 * j + 2])), "f"(__uint_as_float(v[4 * j + 3]))
-                           : "memory");
+              for (int j = 0; j < 8; ++j)
+                __stcg(reinterpret_cast<float4*>(wc + j * 128),
+                       make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                   __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3])));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(wc + j * 128),
+                             "f"(__uint_as_float(v[4 * j])), "f"(__uint_as_float(v[4 * j + 1])),
+                             "f"(__uint_as_float(v[4 * j + 2])), "f"(__uint_as_float(v[4 * j + 3]))
+                             : "memory");
+            }
           }
           tc_fence_before();
           mbar_arrive(&acc_empty[acc]);
@@ -1692,21 +1718,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           // finisher: wait for the other splits' lanes, add its own TMEM
           // partial to their sum, store bf16, clear the workspace
-          const uint32_t want = static_cast<uint32_t>(te.splits - 1) * 32u;
           wait_counter(ctr, want, 40);
+          const bool clear_ws = te.splits > 2;  // a two-split partial is overwritten, not accumulated, next time
+          // the other splits' sum for chunk c + 1 is loaded while chunk c is
+          // packed and stored: one L2 round trip in flight behind the stores
+          float4 f[8];
+          auto load_part = [&](int c) {
+            const float4* src = reinterpret_cast<const float4*>(wq + (c / kEpiChunk) * (8 * 128) + lane * 4);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) f[j] = __ldcg(src + j * 32);
+          };
+          load_part(0);
           for (int c = 0; c < cols; c += kEpiChunk) {
             uint32_t v[32];
             tmem_ld32(taddr + c, v);
-            float4* src = reinterpret_cast<float4*>(wq + (c / kEpiChunk) * (8 * 128) + lane * 4);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              const float4 f = __ldcg(src + j * 32);
-              v[4 * j] = __float_as_uint(__uint_as_float(v[4 * j]) + f.x);
-              v[4 * j + 1] = __float_as_uint(__uint_as_float(v[4 * j + 1]) + f.y);
-              v[4 * j + 2] = __float_as_uint(__uint_as_float(v[4 * j + 2]) + f.z);
-              v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + f.w);
-              __stcg(src + j * 32, make_float4(0.f, 0.f, 0.f, 0.f));
+              v[4 * j] = __float_as_uint(__uint_as_float(v[4 * j]) + f[j].x);
+              v[4 * j + 1] = __float_as_uint(__uint_as_float(v[4 * j + 1]) + f[j].y);
+              v[4 * j + 2] = __float_as_uint(__uint_as_float(v[4 * j + 2]) + f[j].z);
+              v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + f[j].w);
             }
+            if (clear_ws) {
+              float4* dst = reinterpret_cast<float4*>(wq + (c / kEpiChunk) * (8 * 128) + lane * 4);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) __stcg(dst + j * 32, make_float4(0.f, 0.f, 0.f, 0.f));
+            }
+            if (c + kEpiChunk < cols) load_part(c + kEpiChunk);
             if (m0 < md->m) store_bf16(v, c, m0);
           }
           tc_fence_before();
