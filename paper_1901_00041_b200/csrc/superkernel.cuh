@@ -1770,11 +1770,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       acc_phase ^= 1;
       if (trace && quarter == 0 && lane == 0) trace[6 * t + 5] = globaltimer();
       if (publish && lane == 0) {
-        // publish: this warp's stores of the tile are complete and visible
+        // publish: this warp's stores of the tile (all issued by this lane)
+        // are complete, ordered before generic-proxy accesses, then released
+        // with the counter increment itself (no separate sc fence)
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        __threadfence();
-        atomicAdd(counters + te.done, 1u);
+        red_release_add(counters + te.done, 1u);
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
