@@ -1039,10 +1039,12 @@ struct Runtime {
           const int chunk = (kb + splits - 1) / splits;
           splits = (kb + chunk - 1) / chunk;
         }
-        // one counter per row block: 4 epilogue warps arrive per output tile
-        // (8 for a register-path CUDA-core tile: all of them compute it; 1 for
-        // a staged one: its warpgroup publishes once), nt tiles per block
-        const int per_tile = !cuda_core_kind(op.kind) ? 4 : op.cc_rows > 0 ? 1 : 8;
+        // one counter per row block, nt tiles per block: a GEMM tile's
+        // warpgroup publishes once (4 arrivals, one per epilogue warp, for a
+        // split tile: each lane quarter's finisher is picked separately), a
+        // register-path CUDA-core tile 8 (all eight warps compute it), a
+        // staged one 1 (its warpgroup publishes once)
+        const int per_tile = !cuda_core_kind(op.kind) ? (splits > 1 ? 4 : 1) : op.cc_rows > 0 ? 1 : 8;
         for (int64_t a = 0; a < mt; ++a) targets.push_back(static_cast<uint32_t>(nt * per_tile));
         for (int64_t a = 0; a < mt; ++a) {
           const auto [dep, dep_n] = deps_of(a, false);

@@ -1769,13 +1769,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       acc_phase ^= 1;
       if (trace && quarter == 0 && lane == 0) trace[6 * t + 5] = globaltimer();
-      if (publish && lane == 0) {
-        // publish: this warp's stores of the tile (all issued by this lane)
-        // are complete, ordered before generic-proxy accesses, then released
-        // with the counter increment itself (no separate sc fence)
-        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        red_release_add(counters + te.done, 1u);
+      if (publish && te.splits > 1) {
+        // split finisher (chosen per lane quarter): this warp publishes its
+        // own stores -- complete, ordered before generic-proxy accesses,
+        // released with the counter increment itself
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          red_release_add(counters + te.done, 1u);
+        }
+      } else if (publish) {
+        // whole-tile publish: each warp's stores complete (its lane 0 issued
+        // them all), the warpgroup meets, and one release increment covers
+        // the four warps' stores (cumulative through the barrier): one
+        // MEMBAR.GPU per tile instead of one per warp
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        named_barrier(1 + static_cast<int>(acc), 128);
+        if (quarter == 0 && lane == 0) red_release_add(counters + te.done, 1u);
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
