@@ -181,6 +181,36 @@ struct TileEntry {
   uint16_t dep_n, rdep_n;
 };
 
+// The producer's per-tile inputs: the tile entry and the member's scalar
+// fields (a copy of MemberDesc m .. ring_narrow, plus cc_rows and whether a
+// residual is fused).  The scheduler lane fills one per claimed tile in shared
+// memory, so the producer -- the single issuing thread that paces narrow
+// tiles -- reads its tile's setup from smem instead of two dependent L2 round
+// trips (tile entry, then descriptor) per tile.
+struct MemberScalars {
+  int32_t m, n, k_blocks;
+  uint32_t idesc, tx_bytes;
+  int32_t a_mode, pq, q, stride, pad, s_taps, c_blocks, act, n_tile, taps, images, tall, ring_narrow;
+};
+static_assert(sizeof(MemberScalars) == 72, "MemberScalars mirrors MemberDesc m .. ring_narrow");
+struct alignas(16) TileRec {
+  TileEntry te;
+  MemberScalars ms;
+  int32_t cc_rows;
+  int32_t has_res;
+};
+static_assert(offsetof(MemberDesc, ring_narrow) - offsetof(MemberDesc, m) == sizeof(MemberScalars) - 4,
+              "MemberScalars must match MemberDesc's scalar block");
+
+__device__ __forceinline__ void load_tile_rec(const TileEntry* __restrict__ tiles, const MemberDesc* __restrict__ slots,
+                                              int t, TileRec& r) {
+  r.te = tiles[t];
+  const MemberDesc* md = slots + r.te.member;
+  r.ms = *reinterpret_cast<const MemberScalars*>(&md->m);
+  r.cc_rows = md->cc_rows;
+  r.has_res = md->res != nullptr;
+}
+
 // Wait until every counter of [first, first + n) reached its target (acquire).
 __device__ __forceinline__ void wait_range(const uint32_t* counters, const uint32_t* targets, int32_t first, int n,
                                            uint32_t sleep_ns);
@@ -885,6 +915,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   volatile int32_t* sq = tq + kTileQ;
   volatile uint32_t* tq_aux = reinterpret_cast<volatile uint32_t*>(sq + kSchedQ);  // staged tiles: ring slot
   volatile int32_t* pub_q = reinterpret_cast<volatile int32_t*>(tq_aux + kTileQ);    // [2][kPubQ] counter indices
+  TileRec* srec = reinterpret_cast<TileRec*>((reinterpret_cast<uintptr_t>(pub_q + 2 * kPubQ) + 15) & ~uintptr_t(15));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -980,11 +1011,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       for (;;) {
         int t;
+        TileRec rec;
         if (greedy) {
           t = next < n_tiles ? next : -1;
+          if (t >= 0) load_tile_rec(tiles, slots, t, rec);
         } else {
           mbar_wait(&sq_full[sslot], sphase);  // next tile from the scheduler warp
           t = sq[sslot];
+          if (t >= 0) rec = srec[sslot];  // copied before the slot is released
           mbar_arrive(&sq_empty[sslot]);
           if (++sslot == kSchedQ) {
             sslot = 0;
@@ -992,19 +1026,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         TileEntry te{};
-        const MemberDesc* md = slots;
+        const MemberDesc* md = slots;  // tensor-map addresses only; scalars come from the record
+        MemberScalars ms{};
         bool dw = false;
         if (t >= 0) {
-          te = tiles[t];
+          te = rec.te;
           md = slots + te.member;
-          dw = cuda_core_mode(md->a_mode);
+          ms = rec.ms;
+          dw = cuda_core_mode(ms.a_mode);
         }
-        const bool staged = dw && md->cc_rows > 0;
+        const bool staged = dw && rec.cc_rows > 0;
         if (staged) {
           // Name the slot to the consumers only once its previous use is
           // released: the epilogue's parity wait on it is then unambiguous
           // (one phase ahead at most), however far ahead of the ring it runs.
-          set_layout(md->ring_narrow);
+          set_layout(ms.ring_narrow);
           wait_free();
         }
         mbar_wait(&tq_empty[qslot], qphase ^ 1);
@@ -1023,9 +1059,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (staged) {
             // gate like an activation load, then the whole input window as
             // one box into the next slot of the current ring layout
-            const int m0 = te.m_tile * md->cc_rows * md->q;
-            const int img = m0 / md->pq;
-            const int h0 = (m0 - img * md->pq) / md->q * md->stride - md->pad;
+            const int m0 = te.m_tile * rec.cc_rows * ms.q;
+            const int img = m0 / ms.pq;
+            const int h0 = (m0 - img * ms.pq) / ms.q * ms.stride - ms.pad;
             prefetch_tmap(&md->a);
             if (trace) trace[6 * t + 0] = globaltimer();
             if (first) {
@@ -1038,8 +1074,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               asm volatile("fence.proxy.async.global;" ::: "memory");
             }
             if (trace) trace[6 * t + 1] = globaltimer();
-            mbar_expect_tx(&full[stage], md->tx_bytes);
-            tma_load_4d(ring + stage * sbytes, &md->a, &full[stage], te.n_tile * md->n_tile, -md->pad, h0, img);
+            mbar_expect_tx(&full[stage], ms.tx_bytes);
+            tma_load_4d(ring + stage * sbytes, &md->a, &full[stage], te.n_tile * ms.n_tile, -ms.pad, h0, img);
             advance();
           }
           if (greedy) {
@@ -1052,48 +1088,48 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         prefetch_tmap(&md->a);
         prefetch_tmap(&md->b);
-        set_layout(md->ring_narrow);
+        set_layout(ms.ring_narrow);
         const int kb_lo = te.kb_end ? te.kb_begin : 0;
-        const int k_blocks = te.kb_end ? te.kb_end : md->k_blocks;
-        const uint32_t tx = md->tx_bytes;
-        const int tall = md->tall;
+        const int k_blocks = te.kb_end ? te.kb_end : ms.k_blocks;
+        const uint32_t tx = ms.tx_bytes;
+        const int tall = ms.tall;
         const int m0 = te.m_tile * (kBM << tall);
-        const int n0 = te.n_tile * md->n_tile;
+        const int n0 = te.n_tile * ms.n_tile;
         const uint32_t b_off = static_cast<uint32_t>(kABytes << tall);
-        const bool narrow = md->a_mode == kAIm2colNarrow;
-        const bool fold = md->a_mode == kAIm2colFold;
-        const bool im2col = md->a_mode != kATiled;
+        const bool narrow = ms.a_mode == kAIm2colNarrow;
+        const bool fold = ms.a_mode == kAIm2colFold;
+        const bool im2col = ms.a_mode != kATiled;
         int img = 0, h0 = 0, w0 = 0, c_blocks = 1, s_taps = 1;
         if (im2col) {
-          img = m0 / md->pq;
-          const int rem = m0 - img * md->pq;
-          const int p0 = rem / md->q;
-          const int q0 = rem - p0 * md->q;
-          h0 = p0 * md->stride - md->pad;
-          w0 = fold ? q0 : q0 * md->stride - md->pad;  // folded columns are already strided
-          c_blocks = md->c_blocks;
-          s_taps = md->s_taps;
+          img = m0 / ms.pq;
+          const int rem = m0 - img * ms.pq;
+          const int p0 = rem / ms.q;
+          const int q0 = rem - p0 * ms.q;
+          h0 = p0 * ms.stride - ms.pad;
+          w0 = fold ? q0 : q0 * ms.stride - ms.pad;  // folded columns are already strided
+          c_blocks = ms.c_blocks;
+          s_taps = ms.s_taps;
         }
         int img1 = 0, h1 = 0, w1 = 0;  // tall tiles: the second 128-row half
         if (tall && im2col) {
           const int m1 = m0 + kBM;
-          img1 = m1 / md->pq;
-          const int rem = m1 - img1 * md->pq;
-          const int p1 = rem / md->q;
-          const int q1 = rem - p1 * md->q;
-          h1 = p1 * md->stride - md->pad;
-          w1 = fold ? q1 : q1 * md->stride - md->pad;
+          img1 = m1 / ms.pq;
+          const int rem = m1 - img1 * ms.pq;
+          const int p1 = rem / ms.q;
+          const int q1 = rem - p1 * ms.q;
+          h1 = p1 * ms.stride - ms.pad;
+          w1 = fold ? q1 : q1 * ms.stride - ms.pad;
         }
         // TMA im2col coordinates advance incrementally (load_a runs in k-block
         // order within a tile): no integer divisions on the producer's path
         int cb = 0, s_ = 0, r_ = 0;
-        if (md->a_mode == kAIm2col) {
+        if (ms.a_mode == kAIm2col) {
           const int tap = kb_lo / c_blocks;
           cb = kb_lo - tap * c_blocks;
           r_ = tap / s_taps;
           s_ = tap - r_ * s_taps;
         }
-        const int taps = md->taps, images = md->images;
+        const int taps = ms.taps, images = ms.images;
         const CUtensorMap* amap = &md->a;
 
         auto load_a = [&](int kb, uint32_t st) {
@@ -1237,17 +1273,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         using I0 = std::integral_constant<int, 0>;
         using I1 = std::integral_constant<int, 1>;
-        if (md->a_mode == kATiled) {
+        if (ms.a_mode == kATiled) {
           if (tall)
             steady(std::integral_constant<int, kATiled>{}, I1{});
           else
             steady(std::integral_constant<int, kATiled>{}, I0{});
-        } else if (md->a_mode == kAIm2col) {
+        } else if (ms.a_mode == kAIm2col) {
           if (tall)
             steady(std::integral_constant<int, kAIm2col>{}, I1{});
           else
             steady(std::integral_constant<int, kAIm2col>{}, I0{});
-        } else if (md->a_mode == kAIm2colFold) {
+        } else if (ms.a_mode == kAIm2colFold) {
           if (tall)
             steady(std::integral_constant<int, kAIm2colFold>{}, I1{});
           else
@@ -1261,11 +1297,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             advance();
           }
         }
-        if (md->res && k_blocks == md->k_blocks) {
+        if (rec.has_res && k_blocks == ms.k_blocks) {
           // residual k-blocks (the tile, or the split holding the K tail):
           // A = residual columns [n0 + 64 j, +64) of the tile's rows, B = the
           // matching 64 columns of the identity
-          const int rk = (min(md->n_tile, md->n - n0) + kBK - 1) / kBK;
+          const int rk = (min(ms.n_tile, ms.n - n0) + kBK - 1) / kBK;
           for (int j = 0; j < rk; ++j) {
             wait_free();
             uint64_t* bar = &full[stage];
@@ -1478,8 +1514,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             asm volatile("prefetch.global.L1 [%0];" ::"l"(p0 + i));
           prefetch_tmap(&reinterpret_cast<const MemberDesc*>(p0)->c);  // the epilogue's store map
         }
+        TileRec r;
+        if (t >= 0) load_tile_rec(tiles, slots, t, r);  // global reads before the slot wait
         mbar_wait(&sq_empty[sslot], sphase ^ 1);
         sq[sslot] = t;
+        if (t >= 0) srec[sslot] = r;
         mbar_arrive(&sq_full[sslot]);
         if (++sslot == kSchedQ) {
           sslot = 0;
