@@ -198,6 +198,10 @@ struct alignas(16) TileRec {
   MemberScalars ms;
   int32_t cc_rows;
   int32_t has_res;
+  // im2col start of the tile (tall: of each 128-row half) and the K walk's
+  // first (channel block, filter column, filter row); staged CUDA-core tiles:
+  // the input window's image and first row
+  int32_t img, h0, w0, img1, h1, w1, cb, r_, s_;
 };
 static_assert(offsetof(MemberDesc, ring_narrow) - offsetof(MemberDesc, m) == sizeof(MemberScalars) - 4,
               "MemberScalars must match MemberDesc's scalar block");
@@ -209,6 +213,42 @@ __device__ __forceinline__ void load_tile_rec(const TileEntry* __restrict__ tile
   r.ms = *reinterpret_cast<const MemberScalars*>(&md->m);
   r.cc_rows = md->cc_rows;
   r.has_res = md->res != nullptr;
+  // the producer's integer divisions, done here (off the issuing thread)
+  const MemberScalars& ms = r.ms;
+  const TileEntry& te = r.te;
+  r.img = r.h0 = r.w0 = r.img1 = r.h1 = r.w1 = r.cb = r.r_ = r.s_ = 0;
+  if (cuda_core_mode(ms.a_mode)) {
+    if (r.cc_rows > 0) {
+      const int m0 = te.m_tile * r.cc_rows * ms.q;
+      r.img = m0 / ms.pq;
+      r.h0 = (m0 - r.img * ms.pq) / ms.q * ms.stride - ms.pad;
+    }
+  } else if (ms.a_mode != kATiled) {
+    const bool fold = ms.a_mode == kAIm2colFold;
+    const int m0 = te.m_tile * (kBM << ms.tall);
+    r.img = m0 / ms.pq;
+    int rem = m0 - r.img * ms.pq;
+    int p = rem / ms.q;
+    int q = rem - p * ms.q;
+    r.h0 = p * ms.stride - ms.pad;
+    r.w0 = fold ? q : q * ms.stride - ms.pad;  // folded columns are already strided
+    if (ms.tall) {
+      const int m1 = m0 + kBM;
+      r.img1 = m1 / ms.pq;
+      rem = m1 - r.img1 * ms.pq;
+      p = rem / ms.q;
+      q = rem - p * ms.q;
+      r.h1 = p * ms.stride - ms.pad;
+      r.w1 = fold ? q : q * ms.stride - ms.pad;
+    }
+    if (ms.a_mode == kAIm2col) {
+      const int kb_lo = te.kb_end ? te.kb_begin : 0;
+      const int tap = kb_lo / ms.c_blocks;
+      r.cb = kb_lo - tap * ms.c_blocks;
+      r.r_ = tap / ms.s_taps;
+      r.s_ = tap - r.r_ * ms.s_taps;
+    }
+  }
 }
 
 // Wait until every counter of [first, first + n) reached its target (acquire).
@@ -245,7 +285,7 @@ struct RoundArgs {
 constexpr int kTileQ = 8;   // claimed-tile ring between producer and consumers
 constexpr int kDwTag = 1 << 30;  // tile-ring tag: a depthwise tile (no TMA / MMA work)
 constexpr int kStagedTag = 1 << 29;  // with kDwTag: a staged CUDA-core tile (one ring stage, no MMA)
-constexpr int kSchedQ = 2;  // scheduler look-ahead: tiles claimed before the producer needs them
+constexpr int kSchedQ = 2;  // scheduler look-ahead: tiles claimed (and their records loaded) before the producer needs them
 constexpr int kPubQ = 4;    // per epilogue warpgroup: staged-tile publishes queued for the publisher warp
 
 __device__ __forceinline__ bool elect_one() {
@@ -1059,10 +1099,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (staged) {
             // gate like an activation load, then the whole input window as
             // one box into the next slot of the current ring layout
-            const int m0 = te.m_tile * rec.cc_rows * ms.q;
-            const int img = m0 / ms.pq;
-            const int h0 = (m0 - img * ms.pq) / ms.q * ms.stride - ms.pad;
-            prefetch_tmap(&md->a);
+            const int img = rec.img, h0 = rec.h0;  // the window's image and first row (scheduler)
             if (trace) trace[6 * t + 0] = globaltimer();
             if (first) {
               asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -1086,8 +1123,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           continue;
         }
-        prefetch_tmap(&md->a);
-        prefetch_tmap(&md->b);
+        if (greedy) {  // otherwise the scheduler lane prefetched them with the claim
+          prefetch_tmap(&md->a);
+          prefetch_tmap(&md->b);
+        }
         set_layout(ms.ring_narrow);
         const int kb_lo = te.kb_end ? te.kb_begin : 0;
         const int k_blocks = te.kb_end ? te.kb_end : ms.k_blocks;
@@ -1099,36 +1138,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool narrow = ms.a_mode == kAIm2colNarrow;
         const bool fold = ms.a_mode == kAIm2colFold;
         const bool im2col = ms.a_mode != kATiled;
-        int img = 0, h0 = 0, w0 = 0, c_blocks = 1, s_taps = 1;
-        if (im2col) {
-          img = m0 / ms.pq;
-          const int rem = m0 - img * ms.pq;
-          const int p0 = rem / ms.q;
-          const int q0 = rem - p0 * ms.q;
-          h0 = p0 * ms.stride - ms.pad;
-          w0 = fold ? q0 : q0 * ms.stride - ms.pad;  // folded columns are already strided
-          c_blocks = ms.c_blocks;
-          s_taps = ms.s_taps;
-        }
-        int img1 = 0, h1 = 0, w1 = 0;  // tall tiles: the second 128-row half
-        if (tall && im2col) {
-          const int m1 = m0 + kBM;
-          img1 = m1 / ms.pq;
-          const int rem = m1 - img1 * ms.pq;
-          const int p1 = rem / ms.q;
-          const int q1 = rem - p1 * ms.q;
-          h1 = p1 * ms.stride - ms.pad;
-          w1 = fold ? q1 : q1 * ms.stride - ms.pad;
-        }
-        // TMA im2col coordinates advance incrementally (load_a runs in k-block
-        // order within a tile): no integer divisions on the producer's path
-        int cb = 0, s_ = 0, r_ = 0;
-        if (ms.a_mode == kAIm2col) {
-          const int tap = kb_lo / c_blocks;
-          cb = kb_lo - tap * c_blocks;
-          r_ = tap / s_taps;
-          s_ = tap - r_ * s_taps;
-        }
+        // im2col start coordinates (tall: both halves) and the K walk's first
+        // position come precomputed with the tile record; they advance
+        // incrementally (load_a runs in k-block order within a tile): no
+        // integer divisions on the producer's path
+        const int img = rec.img, h0 = rec.h0, w0 = rec.w0;
+        const int img1 = rec.img1, h1 = rec.h1, w1 = rec.w1;
+        const int c_blocks = im2col ? ms.c_blocks : 1, s_taps = im2col ? ms.s_taps : 1;
+        int cb = rec.cb, s_ = rec.s_, r_ = rec.r_;
         const int taps = ms.taps, images = ms.images;
         const CUtensorMap* amap = &md->a;
 
@@ -1512,6 +1529,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < static_cast<int>(sizeof(MemberDesc)); i += 128)
             asm volatile("prefetch.global.L1 [%0];" ::"l"(p0 + i));
+          prefetch_tmap(&reinterpret_cast<const MemberDesc*>(p0)->a);  // the producer's load maps
+          prefetch_tmap(&reinterpret_cast<const MemberDesc*>(p0)->b);
           prefetch_tmap(&reinterpret_cast<const MemberDesc*>(p0)->c);  // the epilogue's store map
         }
         TileRec r;
