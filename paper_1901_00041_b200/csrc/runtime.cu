@@ -1,6 +1,7 @@
 // B200 runtime: per-GPU context, tenant registration (member descriptors with
 // TMA maps), plan preparation (device tile tables, cached per member list) and
 // super-kernel launch.  C-ABI entry points for the device side live here.
+#include <functional>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -455,6 +456,7 @@ struct Runtime {
       Operator op;
       dev::MemberDesc md;
       std::memset(&md, 0, sizeof(md));
+      std::function<void(CUtensorMap*)> a_tall, r_tall;  // 256-row A / residual maps (tall variant)
       op.kind = L.kind;
       op.x = L.x;
       op.tenant = static_cast<int>(tenant_ops.size());
@@ -501,10 +503,12 @@ struct Runtime {
         if (pointwise && c.in_channels % 8 == 0) {
           md.a_mode = dev::kATiled;  // 1x1 stride-1 conv == GEMM over NHWC rows
           tiled_map(&md.a, L.x, op.shape.m, c.in_channels, c.in_channels, a_box_rows(op.shape.m));
+          a_tall = [=, this](CUtensorMap* mp) { tiled_map(mp, L.x, op.shape.m, c.in_channels, c.in_channels, 2 * dev::kBM); };
         } else if (c.in_channels % dev::kBK == 0 && c.kernel_h == c.kernel_w && c.stride <= 8 &&
                    c.padding <= 127 && c.kernel_h - 1 - c.padding <= 128) {
           md.a_mode = dev::kAIm2col;  // implicit GEMM through the TMA im2col unit
           im2col_map(&md.a, L.x, c, op.batch, a_box_rows(op.shape.m));
+          a_tall = [=, this](CUtensorMap* mp) { im2col_map(mp, L.x, c, op.batch, 2 * dev::kBM); };
           md.pq = static_cast<int32_t>(P * Q);
           md.q = static_cast<int32_t>(Q);
           md.stride = static_cast<int32_t>(c.stride);
@@ -575,6 +579,7 @@ struct Runtime {
           op.ldk = (K + 7) / 8 * 8;
           cuda_check(cudaMalloc(&op.scratch, static_cast<size_t>(op.shape.m * op.ldk * 2)), "cudaMalloc(im2col)");
           tiled_map(&md.a, op.scratch, op.shape.m, K, op.ldk, a_box_rows(op.shape.m));
+          a_tall = [=, this](CUtensorMap* mp) { tiled_map(mp, op.scratch, op.shape.m, K, op.ldk, 2 * dev::kBM); };
         }
       } else if (pool) {
         // max / average pool: CUDA-core tile type; planned as a K = R*S GEMM
@@ -649,6 +654,7 @@ struct Runtime {
         const int64_t ldw = L.ldw > 0 ? L.ldw : op.shape.k;
         md.a_mode = dev::kATiled;
         tiled_map(&md.a, L.x, op.shape.m, op.shape.k, ldx, a_box_rows(op.shape.m));
+        a_tall = [=, this](CUtensorMap* mp) { tiled_map(mp, L.x, op.shape.m, op.shape.k, ldx, 2 * dev::kBM); };
         tiled_map(&md.b, L.w, op.shape.n, op.shape.k, ldw, b_box_rows(op.shape.n, op.n_tile));
         op.b_ptr = L.w;
         op.b_k = op.shape.k;
@@ -683,6 +689,7 @@ struct Runtime {
         md.res = static_cast<const __nv_bfloat16*>(L.res);
         md.ldr = static_cast<int32_t>(ldr);
         tiled_map(&md.r, L.res, op.shape.m, op.shape.n, ldr, a_box_rows(op.shape.m));
+        r_tall = [=, this](CUtensorMap* mp) { tiled_map(mp, L.res, op.shape.m, op.shape.n, ldr, 2 * dev::kBM); };
         tiled_map(&md.id, ident, dev::kIdentN, dev::kIdentN, dev::kIdentN, b_box_rows(op.shape.n, op.n_tile));
       }
       op.y = static_cast<const char*>(L.y);
@@ -734,6 +741,15 @@ struct Runtime {
           throw std::logic_error("tall variant does not fit the ring slot / accumulator");
         dev::MemberDesc md3 = md;
         md3.tall = 1;
+        // tiled / im2col A (and the residual): one 256-row box per k-block
+        // (SW128 rows 128..255 land 16 KB on, where the second half's UMMA
+        // reads them): one TMA issue instead of two on the producer thread.
+        // The folded stem keeps two boxes per filter-row column.
+        if (md.a_mode != dev::kAIm2colFold) {
+          if (!a_tall) throw std::logic_error("tall variant: no 256-row A map for this operand mode");
+          a_tall(&md3.a);
+          if (md.res) r_tall(&md3.r);
+        }
         md3.ring_narrow = 0;  // two A boxes: a wide-layout stage
         md3.n_tile = 128;  // the second half's accumulator starts at column 128 of the tile's buffer
         md3.tx_bytes = static_cast<uint32_t>((2 * dev::kBM + b_box_rows(op.shape.n, op.n_tile)) * dev::kBK * 2);

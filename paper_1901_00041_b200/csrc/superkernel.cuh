@@ -1175,11 +1175,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                               static_cast<uint16_t>(s), static_cast<uint16_t>(r));
             }
           } else if (im2col) {
+            // (tall: the map's box is 256 pixels, both halves in one load)
             tma_load_im2col(a_dst, amap, &full[st], cb * kBK, w0, h0, img, static_cast<uint16_t>(s_),
                             static_cast<uint16_t>(r_));
-            if (tall)
-              tma_load_im2col(a_dst + kABytes, amap, &full[st], cb * kBK, w1, h1, img1, static_cast<uint16_t>(s_),
-                              static_cast<uint16_t>(r_));
             if (++cb == c_blocks) {
               cb = 0;
               if (++s_ == s_taps) {
@@ -1188,8 +1186,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           } else {
-            tma_load_2d(a_dst, amap, &full[st], kb * kBK, m0);
-            if (tall) tma_load_2d(a_dst + kABytes, amap, &full[st], kb * kBK, m0 + kBM);
+            tma_load_2d(a_dst, amap, &full[st], kb * kBK, m0);  // tall: one 256-row box
           }
         };
         auto load_b = [&](int kb, uint32_t st) {
@@ -1259,8 +1256,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_expect_tx(bar, tx);
             uint8_t* a_dst = ring + stage * sbytes;
             if constexpr (kMode == kATiled) {
-              tma_load_2d(a_dst, amap, bar, kb * kBK, m0);
-              if constexpr (kTall) tma_load_2d(a_dst + kABytes, amap, bar, kb * kBK, m0 + kBM);
+              tma_load_2d(a_dst, amap, bar, kb * kBK, m0);  // tall: one 256-row box
             } else if constexpr (kMode == kAIm2colFold) {
               // two filter rows; a row past R re-reads row 0 (its weights are zero)
 #pragma unroll
@@ -1272,10 +1268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             } else {
               tma_load_im2col(a_dst, amap, bar, cb * kBK, w0, h0, img, static_cast<uint16_t>(s_),
-                              static_cast<uint16_t>(r_));
-              if constexpr (kTall)
-                tma_load_im2col(a_dst + kABytes, amap, bar, cb * kBK, w1, h1, img1, static_cast<uint16_t>(s_),
-                                static_cast<uint16_t>(r_));
+                              static_cast<uint16_t>(r_));  // tall: one 256-pixel box
               if (++cb == c_blocks) {
                 cb = 0;
                 if (++s_ == s_taps) {
@@ -1324,8 +1317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint64_t* bar = &full[stage];
             mbar_expect_tx(bar, tx);
             uint8_t* a_dst = ring + stage * sbytes;
-            tma_load_2d(a_dst, &md->r, bar, n0 + j * kBK, m0);
-            if (tall) tma_load_2d(a_dst + kABytes, &md->r, bar, n0 + j * kBK, m0 + kBM);
+            tma_load_2d(a_dst, &md->r, bar, n0 + j * kBK, m0);  // tall: one 256-row box
             tma_load_2d(a_dst + b_off, &md->id, bar, j * kBK, 0);
             advance();
           }
